@@ -1,0 +1,152 @@
+/*
+ * hmx -- B200-native H-matrix assembly + H-matvec for the 3D Helmholtz and
+ * elastodynamic (U, T) Green's tensors.  C-ABI of libhmx.so.
+ *
+ * Plain pointers and sizes only.  Complex arrays are interleaved (re, im)
+ * float64 pairs -- numpy complex128 layout -- passed as double*.
+ * All functions return an int status (HMX_OK = 0); hmx_last_error() gives
+ * the message of the last failure on the calling thread.
+ *
+ * Reference interfaces each entry point replaces (paths under
+ * /root/reference/pkg/src/hmatx/ unless noted; SPEC = /root/reference/SPEC.md):
+ *   hmx_tree_build        geometry.py:182-220  build_cluster_tree
+ *   hmx_blocks_build      geometry.py:277-295  build_block_tree  (+ BlockTree.leaves :261-268)
+ *   hmx_eval_block        _kernelcore_np.py:37-130  scalar_block / elasto_u_block /
+ *                         elasto_t_block (the kernel-core backend seam; the missing
+ *                         Cython twin _kernelcore_cy, setup.py:13-22)
+ *   hmx_assemble          SPEC:381-389  hmatrix.assemble (ACA SPEC:288-306 +
+ *                         recompress SPEC:318-326 on the device)
+ *   hmx_hmatrix_stats     SPEC:431-439  hmatrix.storage_report
+ *   hmx_matvec            SPEC:391-399  hmatrix.matvec
+ *   hmx_gmres             SPEC:497-505  solve.solve_gmres
+ * Error codes map to errors.py:4-32 (see HMX_E* below).
+ */
+#ifndef HMX_H_
+#define HMX_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HMX_ABI_VERSION 1
+
+/* status codes */
+#define HMX_OK 0
+#define HMX_EINVAL 1    /* invalid argument / dimension mismatch (ValueError)          */
+#define HMX_ECUDA 2     /* CUDA runtime failure                                        */
+#define HMX_EPIVOT 3    /* FallbackNeeded with no device fallback (PivotExhaustionError) */
+#define HMX_ESINGULAR 4 /* r == 0 pair without a self rule (SingularEvaluationError)     */
+#define HMX_ENOMEM 5    /* device memory budget exceeded                               */
+
+/* kernel kinds (KernelSpec variant) */
+#define HMX_HELMHOLTZ 0 /* e^{i kappa r}/(4 pi r); kappa = 0 is Laplace, d = 1 */
+#define HMX_ELASTO_U 1  /* displacement Green's tensor, d = 3                  */
+#define HMX_ELASTO_T 2  /* traction tensor with column-point normals, d = 3    */
+
+/* recompression truncation rules (oracle/lowrank.py decision 8) */
+#define HMX_TRUNC_FROBENIUS 0
+#define HMX_TRUNC_SPECTRAL 1
+
+/* memory location of vector arguments */
+#define HMX_HOST 0
+#define HMX_DEVICE 1
+
+typedef struct hmx_ctx hmx_ctx;
+typedef struct hmx_tree hmx_tree;
+typedef struct hmx_blocks hmx_blocks;
+typedef struct hmx_hmatrix hmx_hmatrix;
+
+typedef struct {
+  int32_t kind;  /* HMX_HELMHOLTZ / HMX_ELASTO_U / HMX_ELASTO_T */
+  int32_t pad;
+  double kappa;  /* Helmholtz wavenumber */
+  double kp, ks; /* P / S wavenumbers */
+  double lam, mu;
+  double scale;  /* 1 / (rho omega^2) */
+} hmx_kernel;
+
+typedef struct {
+  double eps;            /* eps_ACA (also the recompression tolerance) */
+  int64_t max_rank;      /* <= 0: min(d m, d n) per block */
+  double sigma3_floor;   /* relative sigma_3 floor, default 1e-12 */
+  int32_t trunc_rule;    /* HMX_TRUNC_* */
+  int32_t pad;
+  double mem_budget_gb;  /* ACA workspace budget; <= 0: 40% of free device memory */
+} hmx_aca_cfg;
+
+typedef struct {
+  int64_t n_blocks, n_dense, n_lowrank;
+  int64_t n_stored;                /* stored complex entries N_s */
+  int64_t max_rank_before, max_rank_after;
+  int64_t aca_steps_total;
+  int64_t pairs_evaluated;         /* point pairs fed to the Green's kernels */
+  int64_t n_fallback, n_unconverged, n_regularized, aca_passes;
+  int64_t row_elems, v_elems, n_levels, n_tiles, n_jobs;
+  double t_dense_ms, t_aca_ms, t_recompress_ms, t_form_ms, t_total_ms;
+  double flops_assembly;           /* algorithmic FP64 flops */
+  double matvec_bytes;             /* algorithmic bytes of one matvec */
+  double dense_bytes, lowrank_bytes;
+} hmx_stats;
+
+int hmx_abi_version(void);
+int hmx_last_error(char* buf, int64_t cap);
+
+/* ---- context ------------------------------------------------------------- */
+int hmx_ctx_create(int32_t device, hmx_ctx** out);
+/* launch on an existing cudaStream_t (e.g. torch.cuda.current_stream()); 0 = own stream */
+int hmx_ctx_set_stream(hmx_ctx* ctx, uint64_t stream);
+int hmx_ctx_sync(hmx_ctx* ctx);
+int hmx_ctx_destroy(hmx_ctx* ctx);
+
+/* ---- geometry (host, bit-exact with geometry.py) -------------------------- */
+int hmx_tree_build(const double* points /* n x 3 */, int64_t n, int64_t n_leaf, hmx_tree** out);
+int64_t hmx_tree_num_nodes(const hmx_tree* t);
+/* perm: n; nodes: nn x 5 (start, stop, level, child0, child1); boxes: nn x 6 (lo, hi) -- preorder */
+int hmx_tree_export(const hmx_tree* t, int64_t* perm, int64_t* nodes, double* boxes);
+void hmx_tree_free(hmx_tree* t);
+int hmx_blocks_build(const hmx_tree* rows, const hmx_tree* cols, double eta, hmx_blocks** out);
+int64_t hmx_blocks_count(const hmx_blocks* b);
+/* table: nb x 7 (kind 0 dense / 1 admissible, r0, r1, c0, c1, row node, col node), leaves() order */
+int hmx_blocks_export(const hmx_blocks* b, int64_t* table);
+void hmx_blocks_free(hmx_blocks* b);
+
+/* ---- kernel-core seam ------------------------------------------------------- */
+/* out: (d m) x (d n) complex row-major.  has_shift = 0 and an r == 0 pair -> HMX_ESINGULAR */
+int hmx_eval_block(hmx_ctx* ctx, const hmx_kernel* k, const double* X, int64_t m, const double* Y, int64_t n,
+                   const double* NY, int32_t has_shift, double shift, double* out);
+
+/* ---- assembly --------------------------------------------------------------- */
+/* pts_tree / nrm_tree: points (normals, T only) already in cluster-tree order;
+ * perm: tree slot -> original index; table: nb x 5 (kind, r0, r1, c0, c1). */
+int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, const double* nrm_tree, int64_t n_points,
+                 const int64_t* perm, const int64_t* table, int64_t nb, const hmx_aca_cfg* cfg, double self_shift,
+                 hmx_hmatrix** out);
+/* build an H-matrix from given payloads (parity / snapshot import):
+ * dense leaf b: a[b] = (d m) x (d n) row-major; low-rank leaf: a[b] = U (d m) x r, b[b] = V (d n) x r row-major */
+int hmx_hmatrix_load(hmx_ctx* ctx, int32_t d, int64_t n_points, const int64_t* perm, const int64_t* table, int64_t nb,
+                     const int64_t* ranks, const double* const* a, const double* const* b, hmx_hmatrix** out);
+int hmx_hmatrix_stats(const hmx_hmatrix* h, hmx_stats* st);
+/* per leaf: ACA steps, rank before / after recompression, flags (bit0 converged, bit1 max_rank,
+ * bit3 fallback, bit4 Cholesky regularised) */
+int hmx_hmatrix_block_info(const hmx_hmatrix* h, int64_t* steps, int64_t* rank_before, int64_t* rank_after,
+                           int32_t* flags);
+/* copy leaf b out (layouts as in hmx_hmatrix_load) */
+int hmx_hmatrix_get_block(const hmx_hmatrix* h, int64_t b, double* a, double* v);
+void hmx_hmatrix_free(hmx_hmatrix* h);
+
+/* ---- H-matvec / GMRES ---------------------------------------------------------- */
+/* y = A_H x, x and y in ORIGINAL point order (d N complex each) */
+int hmx_matvec(hmx_hmatrix* h, const double* x, double* y, int32_t mem);
+/* device pointers; phase_ms[4] = gather, phase 1 (V^H x), phase 2 (row GEMV), finalize */
+int hmx_matvec_profile(hmx_hmatrix* h, const double* x_dev, double* y_dev, float* phase_ms);
+int hmx_gmres(hmx_hmatrix* h, const double* b, double* x, double tol, int32_t restart, int64_t max_iters,
+              int32_t mem, int64_t* iters, double* history, int64_t history_cap, int64_t* history_len,
+              int32_t* converged);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* HMX_H_ */

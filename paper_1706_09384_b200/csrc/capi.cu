@@ -1,0 +1,874 @@
+// C-ABI of libhmx.so (include/hmx.h) and the device assembly pipeline.
+//
+// hmx_assemble on the device:
+//   1. batched ACA over all admissible leaves (aca.cu), capacity-budgeted
+//      workspaces; leaves that outgrow their column capacity are re-run in a
+//      further pass with twice the capacity (deterministic -> same result);
+//   2. recompression core per leaf (recompress.cu) -> rank r and the K x r
+//      coefficient matrices W_U, W_V;
+//   3. stream layout + matvec plan from the final ranks (matvec.cu);
+//   4. dense leaves evaluated straight into the row stream (dense.cu) and
+//      U' = U W_U, V' = V W_V formed straight into the row / V streams.
+#include <algorithm>
+#include <chrono>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/hmx.h"
+#include "hmatrix.h"
+#include "hmx_host.h"
+
+static thread_local std::string g_last_error;
+
+void hmx_set_error(const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+}
+
+struct hmx_ctx {
+  hmx::Ctx c;
+};
+struct hmx_tree {
+  hmx::ClusterTree t;
+};
+struct hmx_blocks {
+  std::vector<hmx::BlockLeaf> v;
+};
+struct hmx_hmatrix {
+  hmx::DeviceH H;
+};
+
+namespace {
+
+using namespace hmx;
+
+constexpr int kMaxAcaCols = 640;  // Jacobi pair table limit (recompress.cu)
+
+GreenParams make_params(const hmx_kernel* k, int has_shift, double shift) {
+  GreenParams P;
+  P.kind = k->kind;
+  P.kappa = k->kappa;
+  P.kp = k->kp;
+  P.ks = k->ks;
+  P.lam = k->lam;
+  P.mu = k->mu;
+  P.scale = k->scale;
+  P.shift = shift;
+  P.has_shift = has_shift;
+  return P;
+}
+
+// device SoA copy of (n x 3) points (+ normals)
+struct DevPoints {
+  double* buf = nullptr;
+  PointsSoA soa{};
+  ~DevPoints() {
+    if (buf) cudaFree(buf);
+  }
+  int upload(Ctx& c, const double* pts, const double* nrm, int64_t n) {
+    const int nc = nrm ? 6 : 3;
+    std::vector<double> h((size_t)nc * n);
+    for (int64_t i = 0; i < n; ++i)
+      for (int k = 0; k < 3; ++k) {
+        h[(size_t)k * n + i] = pts[3 * i + k];
+        if (nrm) h[(size_t)(3 + k) * n + i] = nrm[3 * i + k];
+      }
+    HMX_CUDA_TRY(cudaMalloc(&buf, sizeof(double) * h.size() + 8));
+    HMX_CUDA_TRY(cudaMemcpyAsync(buf, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, c.stream));
+    HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    soa.x = buf;
+    soa.y = buf + n;
+    soa.z = buf + 2 * n;
+    soa.nx = nrm ? buf + 3 * n : nullptr;
+    soa.ny = nrm ? buf + 4 * n : nullptr;
+    soa.nz = nrm ? buf + 5 * n : nullptr;
+    return HMX_OK;
+  }
+};
+
+template <class T>
+int dev_upload(Ctx& c, T** dst, const std::vector<T>& src) {
+  HMX_CUDA_TRY(cudaMalloc(dst, sizeof(T) * std::max<size_t>(src.size(), 1)));
+  if (!src.empty())
+    HMX_CUDA_TRY(cudaMemcpyAsync(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, c.stream));
+  return HMX_OK;
+}
+
+struct DevBuf {
+  std::vector<void*> p;
+  ~DevBuf() {
+    for (void* q : p)
+      if (q) cudaFree(q);
+  }
+  template <class T>
+  int alloc(T** out, int64_t count) {
+    void* q = nullptr;
+    cudaError_t e = cudaMalloc(&q, sizeof(T) * std::max<int64_t>(count, 1));
+    if (e != cudaSuccess) {
+      hmx_set_error("cudaMalloc(%lld bytes): %s", (long long)(sizeof(T) * count), cudaGetErrorString(e));
+      return e == cudaErrorMemoryAllocation ? HMX_ENOMEM : HMX_ECUDA;
+    }
+    p.push_back(q);
+    *out = static_cast<T*>(q);
+    return HMX_OK;
+  }
+};
+
+void free_h(DeviceH& H) {
+  void* ptrs[] = {H.d_perm, H.d_row, H.d_v, H.d_s, H.d_xt, H.d_ylev, H.d_xio, H.d_yio, H.d_job1, H.d_tile2};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  H.d_perm = nullptr;
+  H.d_row = H.d_v = H.d_s = H.d_xt = H.d_ylev = H.d_xio = H.d_yio = nullptr;
+  H.d_job1 = nullptr;
+  H.d_tile2 = nullptr;
+}
+
+int validate_table(const int64_t* table, int64_t nb, int64_t np) {
+  if (nb <= 0) {
+    hmx_set_error("empty block list");
+    return HMX_EINVAL;
+  }
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t* t = table + 5 * b;
+    if ((t[0] != 0 && t[0] != 1) || t[1] < 0 || t[2] <= t[1] || t[2] > np || t[3] < 0 || t[4] <= t[3] ||
+        t[4] > np) {
+      hmx_set_error("invalid block %lld: (%lld, %lld, %lld, %lld, %lld)", (long long)b, (long long)t[0],
+                    (long long)t[1], (long long)t[2], (long long)t[3], (long long)t[4]);
+      return HMX_EINVAL;
+    }
+  }
+  return HMX_OK;
+}
+
+struct AcaPass {
+  DevBuf mem;
+  double2 *U = nullptr, *V = nullptr, *G = nullptr, *W = nullptr;
+  std::vector<int64_t> blocks;  // block ids
+  std::vector<AcaDesc> desc;
+  std::vector<AcaOut> out;
+  std::vector<int64_t> woff;
+  int kcap_max = 0;
+};
+
+}  // namespace
+
+extern "C" {
+
+int hmx_abi_version(void) { return HMX_ABI_VERSION; }
+
+int hmx_last_error(char* buf, int64_t cap) {
+  if (!buf || cap <= 0) return HMX_EINVAL;
+  std::snprintf(buf, (size_t)cap, "%s", g_last_error.c_str());
+  return HMX_OK;
+}
+
+int hmx_ctx_create(int32_t device, hmx_ctx** out) {
+  if (!out) return HMX_EINVAL;
+  int ndev = 0;
+  HMX_CUDA_TRY(cudaGetDeviceCount(&ndev));
+  if (device < 0 || device >= ndev) {
+    hmx_set_error("device %d not available (%d devices)", device, ndev);
+    return HMX_EINVAL;
+  }
+  HMX_CUDA_TRY(cudaSetDevice(device));
+  auto* c = new hmx_ctx;
+  c->c.device = device;
+  cudaDeviceProp prop;
+  HMX_CUDA_TRY(cudaGetDeviceProperties(&prop, device));
+  c->c.num_sms = prop.multiProcessorCount;
+  c->c.l2_bytes = prop.l2CacheSize;
+  HMX_CUDA_TRY(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
+  c->c.own_stream = true;
+  *out = c;
+  return HMX_OK;
+}
+
+int hmx_ctx_set_stream(hmx_ctx* ctx, uint64_t stream) {
+  if (!ctx) return HMX_EINVAL;
+  HMX_CUDA_TRY(cudaSetDevice(ctx->c.device));
+  if (ctx->c.own_stream && ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+  if (stream == 0) {
+    HMX_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
+    ctx->c.own_stream = true;
+  } else {
+    ctx->c.stream = reinterpret_cast<cudaStream_t>(stream);
+    ctx->c.own_stream = false;
+  }
+  return HMX_OK;
+}
+
+int hmx_ctx_sync(hmx_ctx* ctx) {
+  if (!ctx) return HMX_EINVAL;
+  HMX_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
+  return HMX_OK;
+}
+
+int hmx_ctx_destroy(hmx_ctx* ctx) {
+  if (!ctx) return HMX_OK;
+  cudaSetDevice(ctx->c.device);
+  if (ctx->c.own_stream && ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+  delete ctx;
+  return HMX_OK;
+}
+
+// ---- geometry -----------------------------------------------------------------
+int hmx_tree_build(const double* points, int64_t n, int64_t n_leaf, hmx_tree** out) {
+  if (!points || !out) return HMX_EINVAL;
+  if (n <= 0) {
+    hmx_set_error("empty input");
+    return HMX_EINVAL;
+  }
+  if (n_leaf < 1) {
+    hmx_set_error("n_leaf must be >= 1");
+    return HMX_EINVAL;
+  }
+  auto* t = new hmx_tree;
+  build_cluster_tree(points, n, n_leaf, t->t);
+  *out = t;
+  return HMX_OK;
+}
+
+int64_t hmx_tree_num_nodes(const hmx_tree* t) { return t ? (int64_t)t->t.nodes.size() : -1; }
+
+int hmx_tree_export(const hmx_tree* t, int64_t* perm, int64_t* nodes, double* boxes) {
+  if (!t) return HMX_EINVAL;
+  if (perm) std::memcpy(perm, t->t.perm.data(), sizeof(int64_t) * t->t.n);
+  for (size_t v = 0; v < t->t.nodes.size(); ++v) {
+    const TreeNode& N = t->t.nodes[v];
+    if (nodes) {
+      nodes[5 * v + 0] = N.start;
+      nodes[5 * v + 1] = N.stop;
+      nodes[5 * v + 2] = N.level;
+      nodes[5 * v + 3] = N.child[0];
+      nodes[5 * v + 4] = N.child[1];
+    }
+    if (boxes)
+      for (int k = 0; k < 3; ++k) {
+        boxes[6 * v + k] = N.lo[k];
+        boxes[6 * v + 3 + k] = N.hi[k];
+      }
+  }
+  return HMX_OK;
+}
+
+void hmx_tree_free(hmx_tree* t) { delete t; }
+
+int hmx_blocks_build(const hmx_tree* rows, const hmx_tree* cols, double eta, hmx_blocks** out) {
+  if (!rows || !cols || !out) return HMX_EINVAL;
+  if (!(eta > 0)) {
+    hmx_set_error("eta must be positive");
+    return HMX_EINVAL;
+  }
+  auto* b = new hmx_blocks;
+  build_block_leaves(rows->t, cols->t, eta, b->v);
+  *out = b;
+  return HMX_OK;
+}
+
+int64_t hmx_blocks_count(const hmx_blocks* b) { return b ? (int64_t)b->v.size() : -1; }
+
+int hmx_blocks_export(const hmx_blocks* b, int64_t* table) {
+  if (!b || !table) return HMX_EINVAL;
+  for (size_t i = 0; i < b->v.size(); ++i) {
+    const BlockLeaf& L = b->v[i];
+    int64_t* t = table + 7 * i;
+    t[0] = L.kind;
+    t[1] = L.r0;
+    t[2] = L.r1;
+    t[3] = L.c0;
+    t[4] = L.c1;
+    t[5] = L.rnode;
+    t[6] = L.cnode;
+  }
+  return HMX_OK;
+}
+
+void hmx_blocks_free(hmx_blocks* b) { delete b; }
+
+// ---- kernel seam ------------------------------------------------------------------
+int hmx_eval_block(hmx_ctx* ctx, const hmx_kernel* k, const double* X, int64_t m, const double* Y, int64_t n,
+                   const double* NY, int32_t has_shift, double shift, double* out) {
+  if (!ctx || !k || !X || !Y || !out || m <= 0 || n <= 0) return HMX_EINVAL;
+  if (k->kind < 0 || k->kind > 2) return HMX_EINVAL;
+  if (k->kind == HMX_ELASTO_T && !NY) {
+    hmx_set_error("elasto T requires column normals");
+    return HMX_EINVAL;
+  }
+  Ctx& c = ctx->c;
+  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  const int d = k->kind == 0 ? 1 : 3;
+  DevPoints dx, dy;
+  int rc = dx.upload(c, X, nullptr, m);
+  if (rc) return rc;
+  rc = dy.upload(c, Y, k->kind == HMX_ELASTO_T ? NY : nullptr, n);
+  if (rc) return rc;
+  DevBuf mem;
+  double2* dout;
+  int32_t* derr;
+  if ((rc = mem.alloc(&dout, (int64_t)d * d * m * n))) return rc;
+  if ((rc = mem.alloc(&derr, 1))) return rc;
+  HMX_CUDA_TRY(cudaMemsetAsync(derr, 0, sizeof(int32_t), c.stream));
+  GreenParams P = make_params(k, has_shift, shift);
+  if ((rc = launch_eval_block(c, P, dx.soa, dy.soa, m, n, dout, derr))) return rc;
+  int32_t herr = 0;
+  HMX_CUDA_TRY(cudaMemcpyAsync(&herr, derr, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+  HMX_CUDA_TRY(
+      cudaMemcpyAsync(out, dout, sizeof(double2) * d * d * m * n, cudaMemcpyDeviceToHost, c.stream));
+  HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  if (herr) {
+    hmx_set_error("singular evaluation: coincident points without a self rule");
+    return HMX_ESINGULAR;
+  }
+  return HMX_OK;
+}
+
+// ---- assembly --------------------------------------------------------------------------
+int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, const double* nrm_tree, int64_t np,
+                 const int64_t* perm, const int64_t* table, int64_t nb, const hmx_aca_cfg* cfg, double self_shift,
+                 hmx_hmatrix** out) {
+  if (!ctx || !k || !pts_tree || !perm || !table || !cfg || !out || np <= 0) return HMX_EINVAL;
+  if (k->kind < 0 || k->kind > 2) return HMX_EINVAL;
+  if (k->kind == HMX_ELASTO_T && !nrm_tree) {
+    hmx_set_error("elasto T requires normals");
+    return HMX_EINVAL;
+  }
+  if (!(cfg->eps > 0 && cfg->eps < 1)) {
+    hmx_set_error("eps_aca must be in (0, 1)");
+    return HMX_EINVAL;
+  }
+  int rc = validate_table(table, nb, np);
+  if (rc) return rc;
+  Ctx& c = ctx->c;
+  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  const auto t_start = std::chrono::steady_clock::now();
+  auto holder = new hmx_hmatrix;
+  DeviceH& H = holder->H;
+  H.ctx = &c;
+  H.kind = k->kind;
+  H.d = k->kind == 0 ? 1 : 3;
+  const int d = H.d;
+  H.np = np;
+  H.n = d * np;
+  H.nb = nb;
+  H.table.assign(table, table + 5 * nb);
+  H.steps.assign(nb, 0);
+  H.rank_before.assign(nb, 0);
+  H.rank_after.assign(nb, 0);
+  H.flags.assign(nb, 0);
+  auto fail = [&](int code) {
+    free_h(H);
+    delete holder;
+    return code;
+  };
+  DevPoints pts;
+  if ((rc = pts.upload(c, pts_tree, k->kind == HMX_ELASTO_T ? nrm_tree : nullptr, np))) return fail(rc);
+  {
+    std::vector<int64_t> p(perm, perm + np);
+    if ((rc = dev_upload(c, &H.d_perm, p))) return fail(rc);
+  }
+  const GreenParams P = make_params(k, 1, self_shift);
+  cudaEvent_t ev[6];
+  for (auto& e : ev) HMX_CUDA_TRY(cudaEventCreate(&e));
+  HMX_CUDA_TRY(cudaEventRecord(ev[0], c.stream));
+
+  // ---- 1. ACA passes --------------------------------------------------------------------
+  std::vector<int64_t> adm;
+  for (int64_t b = 0; b < nb; ++b)
+    if (table[5 * b] == 1) adm.push_back(b);
+  auto rows_of = [&](int64_t b) { return table[5 * b + 2] - table[5 * b + 1]; };
+  auto cols_of = [&](int64_t b) { return table[5 * b + 4] - table[5 * b + 3]; };
+  std::vector<int64_t> maxr(nb, 0), kcap(nb, 0);
+  for (int64_t b : adm) {
+    int64_t dmin = d * std::min(rows_of(b), cols_of(b));
+    maxr[b] = cfg->max_rank > 0 ? std::min<int64_t>(cfg->max_rank, dmin) : dmin;
+  }
+  size_t free_b = 0, total_b = 0;
+  HMX_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  const double budget = cfg->mem_budget_gb > 0 ? cfg->mem_budget_gb * 1e9 : 0.4 * (double)free_b;
+  auto round_d = [&](int64_t v) { return std::max<int64_t>(d, (v / d) * d); };
+  auto ws_bytes = [&](int64_t b, int64_t kc) {
+    return 16.0 * ((double)d * (rows_of(b) + cols_of(b)) * kc + 2.0 * kc * kc);
+  };
+  {
+    // largest uniform cap K0 whose workspace fits the budget
+    int64_t lo = d, hi = round_d(kMaxAcaCols);
+    auto need = [&](int64_t K0) {
+      double s = 0;
+      for (int64_t b : adm) s += ws_bytes(b, std::min<int64_t>(maxr[b], K0));
+      return s;
+    };
+    if (need(lo) > budget) {
+      hmx_set_error("ACA workspace for rank %d exceeds the %.1f GB budget", d, budget / 1e9);
+      return fail(HMX_ENOMEM);
+    }
+    while (lo < hi) {
+      const int64_t mid = round_d((lo + hi + d) / 2);
+      if (mid <= lo) break;
+      if (need(mid) <= budget) lo = mid;
+      else hi = mid - d;
+    }
+    for (int64_t b : adm) kcap[b] = std::min<int64_t>(maxr[b], lo);
+  }
+  std::vector<AcaPass> passes;
+  passes.reserve(8);
+  std::vector<int64_t> todo = adm;
+  int64_t m_max_all = 1;
+  for (int64_t b : adm) m_max_all = std::max(m_max_all, rows_of(b));
+  while (!todo.empty()) {
+    passes.emplace_back();
+    AcaPass& ps = passes.back();
+    std::sort(todo.begin(), todo.end(), [&](int64_t a, int64_t b) {
+      const int64_t ca = rows_of(a) + cols_of(a), cb = rows_of(b) + cols_of(b);
+      return ca != cb ? ca > cb : a < b;
+    });
+    ps.blocks = todo;
+    int64_t uo = 0, vo = 0, go = 0;
+    ps.desc.resize(todo.size());
+    for (size_t i = 0; i < todo.size(); ++i) {
+      const int64_t b = todo[i];
+      AcaDesc& D = ps.desc[i];
+      D.r0 = table[5 * b + 1];
+      D.c0 = table[5 * b + 3];
+      D.m = (int32_t)rows_of(b);
+      D.n = (int32_t)cols_of(b);
+      D.kcap = (int32_t)kcap[b];
+      D.max_rank = (int32_t)maxr[b];
+      D.uoff = uo;
+      D.voff = vo;
+      D.goff = go;
+      uo += (int64_t)d * D.m * D.kcap;
+      vo += (int64_t)d * D.n * D.kcap;
+      go += 2 * (int64_t)D.kcap * D.kcap;
+      ps.kcap_max = std::max<int>(ps.kcap_max, D.kcap);
+    }
+    if ((rc = ps.mem.alloc(&ps.U, uo))) return fail(rc);
+    if ((rc = ps.mem.alloc(&ps.V, vo))) return fail(rc);
+    if ((rc = ps.mem.alloc(&ps.G, go))) return fail(rc);
+    AcaDesc* d_desc;
+    AcaOut* d_out;
+    int32_t* d_order;
+    DevBuf tmp;
+    if ((rc = tmp.alloc(&d_desc, (int64_t)todo.size()))) return fail(rc);
+    if ((rc = tmp.alloc(&d_out, (int64_t)todo.size()))) return fail(rc);
+    if ((rc = tmp.alloc(&d_order, (int64_t)todo.size()))) return fail(rc);
+    std::vector<int32_t> order(todo.size());
+    for (size_t i = 0; i < order.size(); ++i) order[i] = (int32_t)i;
+    HMX_CUDA_TRY(cudaMemcpyAsync(d_desc, ps.desc.data(), sizeof(AcaDesc) * todo.size(), cudaMemcpyHostToDevice,
+                                 c.stream));
+    HMX_CUDA_TRY(
+        cudaMemcpyAsync(d_order, order.data(), sizeof(int32_t) * todo.size(), cudaMemcpyHostToDevice, c.stream));
+    if ((rc = launch_aca(c, d, P, pts.soa, d_desc, d_order, (int64_t)todo.size(), ps.kcap_max, (int)m_max_all,
+                         cfg->eps, cfg->sigma3_floor > 0 ? cfg->sigma3_floor : 1e-12, ps.U, ps.V, ps.G, d_out)))
+      return fail(rc);
+    ps.out.resize(todo.size());
+    HMX_CUDA_TRY(
+        cudaMemcpyAsync(ps.out.data(), d_out, sizeof(AcaOut) * todo.size(), cudaMemcpyDeviceToHost, c.stream));
+    HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    std::vector<int64_t> next;
+    int64_t nfb = 0;
+    for (size_t i = 0; i < todo.size(); ++i) {
+      const int64_t b = todo[i];
+      const AcaOut& o = ps.out[i];
+      if (o.status & 4) {
+        if (kcap[b] >= std::min<int64_t>(maxr[b], round_d(kMaxAcaCols))) {
+          hmx_set_error("block %lld: ACA rank exceeds %d columns", (long long)b, kMaxAcaCols);
+          return fail(HMX_ENOMEM);
+        }
+        kcap[b] = std::min<int64_t>(std::min<int64_t>(maxr[b], round_d(kMaxAcaCols)), 2 * kcap[b]);
+        next.push_back(b);
+        ps.out[i].rank = -1;  // superseded
+        continue;
+      }
+      if (o.status & 8) ++nfb;
+      H.steps[b] = o.steps;
+      H.rank_before[b] = o.rank;
+      H.flags[b] = o.status & 0xB;
+      H.pairs_evaluated += (int64_t)o.steps * (rows_of(b) + cols_of(b)) + (int64_t)o.zero_rows * cols_of(b);
+    }
+    H.aca_passes++;
+    if (nfb) {
+      H.n_fallback += nfb;
+      hmx_set_error("FallbackNeeded on %lld admissible blocks (all sigma_3 pivots below the floor); the device "
+                    "randomized-SVD fallback is not implemented",
+                    (long long)nfb);
+      return fail(HMX_EPIVOT);
+    }
+    todo.swap(next);
+  }
+  HMX_CUDA_TRY(cudaEventRecord(ev[1], c.stream));
+
+  // ---- 2. recompression core --------------------------------------------------------------
+  std::vector<int64_t> regularized(nb, 0);
+  for (AcaPass& ps : passes) {
+    std::vector<int64_t> live;
+    for (size_t i = 0; i < ps.blocks.size(); ++i)
+      if (ps.out[i].rank >= 0) live.push_back((int64_t)i);
+    // largest K first, launched in K classes so small leaves do not pay for big shared memory
+    std::sort(live.begin(), live.end(), [&](int64_t a, int64_t b) {
+      return ps.out[a].rank != ps.out[b].rank ? ps.out[a].rank > ps.out[b].rank : a < b;
+    });
+    std::vector<RecDesc> rd(live.size());
+    int64_t wo = 0;
+    ps.woff.assign(ps.blocks.size(), 0);
+    for (size_t q = 0; q < live.size(); ++q) {
+      const int64_t i = live[q];
+      const int K = ps.out[i].rank;
+      rd[q].goff = ps.desc[i].goff;
+      rd[q].woff = wo;
+      rd[q].K = K;
+      rd[q].kcap = ps.desc[i].kcap;
+      ps.woff[i] = wo;
+      wo += 5 * (int64_t)K * K;
+    }
+    if (live.empty()) continue;
+    if ((rc = ps.mem.alloc(&ps.W, wo))) return fail(rc);
+    DevBuf tmp;
+    RecDesc* d_rd;
+    int32_t *d_rank, *d_flag;
+    if ((rc = tmp.alloc(&d_rd, (int64_t)rd.size()))) return fail(rc);
+    if ((rc = tmp.alloc(&d_rank, (int64_t)rd.size()))) return fail(rc);
+    if ((rc = tmp.alloc(&d_flag, (int64_t)rd.size()))) return fail(rc);
+    HMX_CUDA_TRY(cudaMemcpyAsync(d_rd, rd.data(), sizeof(RecDesc) * rd.size(), cudaMemcpyHostToDevice, c.stream));
+    const int classes[] = {kMaxAcaCols, 112, 64, 32};
+    size_t q0 = 0;
+    for (int ci = 0; ci < 4 && q0 < rd.size(); ++ci) {
+      const int lim_lo = ci + 1 < 4 ? classes[ci + 1] : 0;
+      size_t q1 = q0;
+      while (q1 < rd.size() && (rd[q1].K > lim_lo || ci == 3)) ++q1;
+      if (q1 > q0) {
+        if ((rc = launch_recompress_core(c, d_rd + q0, (int64_t)(q1 - q0), rd[q0].K, cfg->eps, cfg->trunc_rule, ps.G,
+                                         ps.W, d_rank + q0, d_flag + q0)))
+          return fail(rc);
+      }
+      q0 = q1;
+    }
+    std::vector<int32_t> hr(rd.size()), hf(rd.size());
+    HMX_CUDA_TRY(cudaMemcpyAsync(hr.data(), d_rank, sizeof(int32_t) * rd.size(), cudaMemcpyDeviceToHost, c.stream));
+    HMX_CUDA_TRY(cudaMemcpyAsync(hf.data(), d_flag, sizeof(int32_t) * rd.size(), cudaMemcpyDeviceToHost, c.stream));
+    HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    for (size_t q = 0; q < live.size(); ++q) {
+      const int64_t b = ps.blocks[live[q]];
+      H.rank_after[b] = hr[q];
+      if (hf[q] & 1) {
+        H.flags[b] |= 16;
+        H.n_regularized++;
+      }
+    }
+  }
+  HMX_CUDA_TRY(cudaEventRecord(ev[2], c.stream));
+
+  // ---- 3. layout + matvec plan ----------------------------------------------------------------
+  if ((rc = build_matvec_plan(H, {}))) return fail(rc);
+
+  // ---- 4a. dense leaves ---------------------------------------------------------------------
+  HMX_CUDA_TRY(cudaEventRecord(ev[3], c.stream));
+  int32_t* d_err;
+  DevBuf tmp4;
+  if ((rc = tmp4.alloc(&d_err, 1))) return fail(rc);
+  HMX_CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int32_t), c.stream));
+  {
+    std::vector<int64_t> dd;
+    for (int64_t b = 0; b < nb; ++b) {
+      if (table[5 * b] != 0) continue;
+      dd.insert(dd.end(), {table[5 * b + 1], rows_of(b), table[5 * b + 3], cols_of(b), H.leaf_moff[b], H.leaf_ld[b]});
+    }
+    int64_t* d_dd;
+    if ((rc = tmp4.alloc(&d_dd, (int64_t)dd.size()))) return fail(rc);
+    HMX_CUDA_TRY(cudaMemcpyAsync(d_dd, dd.data(), sizeof(int64_t) * dd.size(), cudaMemcpyHostToDevice, c.stream));
+    if ((rc = launch_dense_fill(c, P, pts.soa, d_dd, (int64_t)dd.size() / 6, H.d_row, d_err))) return fail(rc);
+  }
+  HMX_CUDA_TRY(cudaEventRecord(ev[4], c.stream));
+
+  // ---- 4b. U' = U W_U, V' = V W_V -------------------------------------------------------------
+  for (AcaPass& ps : passes) {
+    if (!ps.W) continue;
+    for (int side = 0; side < 2; ++side) {
+      std::vector<FormDesc> fd;
+      std::vector<int64_t> ts;
+      int64_t ntiles = 0;
+      for (size_t i = 0; i < ps.blocks.size(); ++i) {
+        if (ps.out[i].rank < 0) continue;
+        const int64_t b = ps.blocks[i];
+        const int K = ps.out[i].rank;
+        const int r = (int)H.rank_after[b];
+        if (r == 0 || K == 0) continue;
+        FormDesc f;
+        const int64_t rows = side == 0 ? d * rows_of(b) : d * cols_of(b);
+        f.aoff = side == 0 ? ps.desc[i].uoff : ps.desc[i].voff;
+        f.woff = ps.woff[i] + 3 * (int64_t)K * K + (side == 0 ? 0 : (int64_t)K * r);
+        f.coff = side == 0 ? H.leaf_moff[b] : H.leaf_voff[b];
+        f.rows = (int32_t)rows;
+        f.K = K;
+        f.r = r;
+        f.lda = (int32_t)rows;
+        f.ldc = (int32_t)rows;
+        f.pad = 0;
+        ts.push_back(ntiles);
+        ntiles += hmx_cdiv(rows, 64) * hmx_cdiv(r, 32);
+        fd.push_back(f);
+      }
+      if (fd.empty()) continue;
+      DevBuf t5;
+      FormDesc* d_fd;
+      int64_t* d_ts;
+      if ((rc = t5.alloc(&d_fd, (int64_t)fd.size()))) return fail(rc);
+      if ((rc = t5.alloc(&d_ts, (int64_t)ts.size()))) return fail(rc);
+      HMX_CUDA_TRY(cudaMemcpyAsync(d_fd, fd.data(), sizeof(FormDesc) * fd.size(), cudaMemcpyHostToDevice, c.stream));
+      HMX_CUDA_TRY(cudaMemcpyAsync(d_ts, ts.data(), sizeof(int64_t) * ts.size(), cudaMemcpyHostToDevice, c.stream));
+      if ((rc = launch_form(c, d_fd, (int64_t)fd.size(), ntiles, d_ts, side == 0 ? ps.U : ps.V, ps.W,
+                            side == 0 ? H.d_row : H.d_v)))
+        return fail(rc);
+      HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    }
+  }
+  HMX_CUDA_TRY(cudaEventRecord(ev[5], c.stream));
+  int32_t herr = 0;
+  HMX_CUDA_TRY(cudaMemcpyAsync(&herr, d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+  HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  if (herr) {
+    hmx_set_error("singular evaluation in a dense leaf");
+    return fail(HMX_ESINGULAR);
+  }
+  float ms[5];
+  for (int i = 0; i < 5; ++i) HMX_CUDA_TRY(cudaEventElapsedTime(&ms[i], ev[i], ev[i + 1]));
+  for (auto& e : ev) cudaEventDestroy(e);
+  H.t_aca_ms = ms[0];
+  H.t_recomp_ms = ms[1];
+  H.t_dense_ms = ms[3];
+  H.t_form_ms = ms[4];
+  // algorithmic FP64 flops of the factor arithmetic (pair evaluation counted separately)
+  double fl = 0;
+  for (int64_t b : adm) {
+    const double mn = (double)(rows_of(b) + cols_of(b));
+    const int64_t s = H.steps[b];
+    for (int64_t kk = 0; kk < s; ++kk) {
+      const double K = (double)d * kk;
+      fl += 8.0 * d * d * mn * K + 8.0 * d * d * mn * (K + d);
+    }
+    const double K = (double)H.rank_before[b], r = (double)H.rank_after[b];
+    fl += 8.0 * 22.0 * K * K * K + 8.0 * d * mn * K * r;
+    if (H.flags[b] & 1) {
+    } else {
+      H.n_unconverged += 1;
+    }
+  }
+  H.flops_assembly = fl;
+  H.t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
+  *out = holder;
+  return HMX_OK;
+}
+
+int hmx_hmatrix_load(hmx_ctx* ctx, int32_t d, int64_t np, const int64_t* perm, const int64_t* table, int64_t nb,
+                     const int64_t* ranks, const double* const* a, const double* const* bptr, hmx_hmatrix** out) {
+  if (!ctx || !perm || !table || !a || !out || (d != 1 && d != 3) || np <= 0) return HMX_EINVAL;
+  int rc = validate_table(table, nb, np);
+  if (rc) return rc;
+  Ctx& c = ctx->c;
+  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  auto holder = new hmx_hmatrix;
+  DeviceH& H = holder->H;
+  H.ctx = &c;
+  H.d = d;
+  H.kind = d == 1 ? 0 : 1;
+  H.np = np;
+  H.n = d * np;
+  H.nb = nb;
+  H.table.assign(table, table + 5 * nb);
+  H.steps.assign(nb, 0);
+  H.rank_before.assign(nb, 0);
+  H.rank_after.assign(nb, 0);
+  H.flags.assign(nb, 1);
+  for (int64_t b = 0; b < nb; ++b)
+    if (table[5 * b] == 1) H.rank_after[b] = H.rank_before[b] = ranks ? ranks[b] : 0;
+  auto fail = [&](int code) {
+    free_h(H);
+    delete holder;
+    return code;
+  };
+  {
+    std::vector<int64_t> p(perm, perm + np);
+    if ((rc = dev_upload(c, &H.d_perm, p))) return fail(rc);
+  }
+  if ((rc = build_matvec_plan(H, {}))) return fail(rc);
+  std::vector<double2> row(H.row_elems), vs(std::max<int64_t>(H.v_elems, 0));
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t m = table[5 * b + 2] - table[5 * b + 1], n = table[5 * b + 4] - table[5 * b + 3];
+    const int64_t dm = d * m, dn = d * n, ld = H.leaf_ld[b];
+    const double2* A = reinterpret_cast<const double2*>(a[b]);
+    if (table[5 * b] == 0) {
+      for (int64_t i = 0; i < dm; ++i)
+        for (int64_t j = 0; j < dn; ++j) row[H.leaf_moff[b] + j * ld + i] = A[i * dn + j];
+    } else {
+      const int64_t r = H.rank_after[b];
+      if (r == 0) continue;
+      const double2* Bv = reinterpret_cast<const double2*>(bptr[b]);
+      for (int64_t i = 0; i < dm; ++i)
+        for (int64_t l = 0; l < r; ++l) row[H.leaf_moff[b] + l * ld + i] = A[i * r + l];
+      for (int64_t i = 0; i < dn; ++i)
+        for (int64_t l = 0; l < r; ++l) vs[H.leaf_voff[b] + l * dn + i] = Bv[i * r + l];
+    }
+  }
+  HMX_CUDA_TRY(cudaMemcpy(H.d_row, row.data(), sizeof(double2) * row.size(), cudaMemcpyHostToDevice));
+  if (!vs.empty()) HMX_CUDA_TRY(cudaMemcpy(H.d_v, vs.data(), sizeof(double2) * vs.size(), cudaMemcpyHostToDevice));
+  *out = holder;
+  return HMX_OK;
+}
+
+int hmx_hmatrix_stats(const hmx_hmatrix* h, hmx_stats* st) {
+  if (!h || !st) return HMX_EINVAL;
+  const DeviceH& H = h->H;
+  std::memset(st, 0, sizeof(*st));
+  st->n_blocks = H.nb;
+  for (int64_t b = 0; b < H.nb; ++b) {
+    const int64_t m = H.table[5 * b + 2] - H.table[5 * b + 1], n = H.table[5 * b + 4] - H.table[5 * b + 3];
+    if (H.table[5 * b] == 0) {
+      st->n_dense++;
+      st->n_stored += (int64_t)H.d * H.d * m * n;
+    } else {
+      st->n_lowrank++;
+      st->n_stored += H.rank_after[b] * H.d * (m + n);
+      st->max_rank_before = std::max(st->max_rank_before, H.rank_before[b]);
+      st->max_rank_after = std::max(st->max_rank_after, H.rank_after[b]);
+      st->aca_steps_total += H.steps[b];
+    }
+  }
+  st->pairs_evaluated = H.pairs_evaluated;
+  for (int64_t b = 0; b < H.nb; ++b)
+    if (H.table[5 * b] == 0)
+      st->pairs_evaluated += (H.table[5 * b + 2] - H.table[5 * b + 1]) * (H.table[5 * b + 4] - H.table[5 * b + 3]);
+  st->n_fallback = H.n_fallback;
+  st->n_unconverged = H.n_unconverged;
+  st->n_regularized = H.n_regularized;
+  st->aca_passes = H.aca_passes;
+  st->row_elems = H.row_elems;
+  st->v_elems = H.v_elems;
+  st->n_levels = H.nlevels;
+  st->n_tiles = H.ntile2;
+  st->n_jobs = H.njob1;
+  st->t_dense_ms = H.t_dense_ms;
+  st->t_aca_ms = H.t_aca_ms;
+  st->t_recompress_ms = H.t_recomp_ms;
+  st->t_form_ms = H.t_form_ms;
+  st->t_total_ms = H.t_total_ms;
+  st->flops_assembly = H.flops_assembly;
+  st->matvec_bytes = H.mv_bytes;
+  st->dense_bytes = H.dense_bytes;
+  st->lowrank_bytes = H.lr_bytes;
+  return HMX_OK;
+}
+
+int hmx_hmatrix_block_info(const hmx_hmatrix* h, int64_t* steps, int64_t* rank_before, int64_t* rank_after,
+                           int32_t* flags) {
+  if (!h) return HMX_EINVAL;
+  const DeviceH& H = h->H;
+  for (int64_t b = 0; b < H.nb; ++b) {
+    if (steps) steps[b] = H.steps[b];
+    if (rank_before) rank_before[b] = H.rank_before[b];
+    if (rank_after) rank_after[b] = H.rank_after[b];
+    if (flags) flags[b] = H.flags[b];
+  }
+  return HMX_OK;
+}
+
+int hmx_hmatrix_get_block(const hmx_hmatrix* h, int64_t b, double* a, double* v) {
+  if (!h || !a || b < 0 || b >= h->H.nb) return HMX_EINVAL;
+  const DeviceH& H = h->H;
+  HMX_CUDA_TRY(cudaSetDevice(H.ctx->device));
+  const int d = H.d;
+  const int64_t m = H.table[5 * b + 2] - H.table[5 * b + 1], n = H.table[5 * b + 4] - H.table[5 * b + 3];
+  const int64_t dm = d * m, dn = d * n, ld = H.leaf_ld[b];
+  double2* A = reinterpret_cast<double2*>(a);
+  HMX_CUDA_TRY(cudaStreamSynchronize(H.ctx->stream));
+  if (H.table[5 * b] == 0) {
+    std::vector<double2> t(dm * dn);
+    HMX_CUDA_TRY(cudaMemcpy(t.data(), H.d_row + H.leaf_moff[b], sizeof(double2) * t.size(), cudaMemcpyDeviceToHost));
+    for (int64_t i = 0; i < dm; ++i)
+      for (int64_t j = 0; j < dn; ++j) A[i * dn + j] = t[j * ld + i];
+    return HMX_OK;
+  }
+  const int64_t r = H.rank_after[b];
+  if (r == 0) return HMX_OK;
+  if (!v) return HMX_EINVAL;
+  double2* Vh = reinterpret_cast<double2*>(v);
+  std::vector<double2> tu(dm * r), tv(dn * r);
+  HMX_CUDA_TRY(cudaMemcpy(tu.data(), H.d_row + H.leaf_moff[b], sizeof(double2) * tu.size(), cudaMemcpyDeviceToHost));
+  HMX_CUDA_TRY(cudaMemcpy(tv.data(), H.d_v + H.leaf_voff[b], sizeof(double2) * tv.size(), cudaMemcpyDeviceToHost));
+  for (int64_t i = 0; i < dm; ++i)
+    for (int64_t l = 0; l < r; ++l) A[i * r + l] = tu[l * ld + i];
+  for (int64_t i = 0; i < dn; ++i)
+    for (int64_t l = 0; l < r; ++l) Vh[i * r + l] = tv[l * dn + i];
+  return HMX_OK;
+}
+
+void hmx_hmatrix_free(hmx_hmatrix* h) {
+  if (!h) return;
+  cudaSetDevice(h->H.ctx->device);
+  cudaStreamSynchronize(h->H.ctx->stream);
+  free_h(h->H);
+  delete h;
+}
+
+int hmx_matvec(hmx_hmatrix* h, const double* x, double* y, int32_t mem) {
+  if (!h || !x || !y) return HMX_EINVAL;
+  DeviceH& H = h->H;
+  Ctx& c = *H.ctx;
+  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  if (mem == HMX_DEVICE)
+    return matvec_device(H, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y), nullptr);
+  HMX_CUDA_TRY(cudaMemcpyAsync(H.d_xio, x, sizeof(double2) * H.n, cudaMemcpyHostToDevice, c.stream));
+  int rc = matvec_device(H, H.d_xio, H.d_yio, nullptr);
+  if (rc) return rc;
+  HMX_CUDA_TRY(cudaMemcpyAsync(y, H.d_yio, sizeof(double2) * H.n, cudaMemcpyDeviceToHost, c.stream));
+  HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  return HMX_OK;
+}
+
+int hmx_matvec_profile(hmx_hmatrix* h, const double* x_dev, double* y_dev, float* phase_ms) {
+  if (!h || !x_dev || !y_dev || !phase_ms) return HMX_EINVAL;
+  HMX_CUDA_TRY(cudaSetDevice(h->H.ctx->device));
+  return matvec_device(h->H, reinterpret_cast<const double2*>(x_dev), reinterpret_cast<double2*>(y_dev), phase_ms);
+}
+
+int hmx_gmres(hmx_hmatrix* h, const double* b, double* x, double tol, int32_t restart, int64_t max_iters,
+              int32_t mem, int64_t* iters, double* history, int64_t history_cap, int64_t* history_len,
+              int32_t* converged) {
+  if (!h || !b || !x || !iters || !converged || restart < 1 || !(tol > 0)) return HMX_EINVAL;
+  DeviceH& H = h->H;
+  Ctx& c = *H.ctx;
+  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  const double2* db = reinterpret_cast<const double2*>(b);
+  double2* dx = reinterpret_cast<double2*>(x);
+  DevBuf tmp;
+  int rc;
+  if (mem == HMX_HOST) {
+    double2 *tb, *tx;
+    if ((rc = tmp.alloc(&tb, H.n))) return rc;
+    if ((rc = tmp.alloc(&tx, H.n))) return rc;
+    HMX_CUDA_TRY(cudaMemcpyAsync(tb, b, sizeof(double2) * H.n, cudaMemcpyHostToDevice, c.stream));
+    db = tb;
+    dx = tx;
+  }
+  std::vector<double> hist;
+  int conv = 0;
+  rc = gmres_device(H, db, dx, tol, restart, max_iters, iters, hist, &conv);
+  if (rc) return rc;
+  if (mem == HMX_HOST) {
+    HMX_CUDA_TRY(cudaMemcpyAsync(x, dx, sizeof(double2) * H.n, cudaMemcpyDeviceToHost, c.stream));
+  }
+  HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  *converged = conv;
+  if (history_len) *history_len = (int64_t)hist.size();
+  if (history)
+    for (int64_t i = 0; i < std::min<int64_t>(history_cap, (int64_t)hist.size()); ++i) history[i] = hist[i];
+  return HMX_OK;
+}
+
+}  // extern "C"

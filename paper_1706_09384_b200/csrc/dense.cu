@@ -1,0 +1,86 @@
+// Batched Green's-tensor entry evaluation.
+//
+//  * dense_fill: every dense (non-admissible) leaf of the block partition
+//    (SPEC.md:208-216 assemble_dense + the self rule zeta = N_c)
+//    written straight into its slot of the segment-packed row stream
+//    (column-major, ld = d m), one CTA per leaf, thread per point pair.
+//  * eval_block: the kernel-core seam (reference _kernelcore_np.py:37-130,
+//    scalar_block / elasto_u_block / elasto_t_block): X (m points) x Y (n
+//    points) -> (d m) x (d n) row-major complex128, the reference's layout
+//    (row d i + a, column d j + b, _kernelcore_np.py:74-77).
+#include "green.cuh"
+#include "hmatrix.h"
+
+namespace hmx {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+// desc: ndense x 6 int64 (r0, m, c0, n, moff, ld)
+template <int D>
+__global__ void __launch_bounds__(kThreads) dense_fill(GreenParams P, PointsSoA pts, const int64_t* __restrict__ desc,
+                                                       double2* __restrict__ row, int32_t* __restrict__ err) {
+  const int64_t* dsc = desc + 6 * (int64_t)blockIdx.x;
+  const int64_t r0 = dsc[0], m = dsc[1], c0 = dsc[2], n = dsc[3], moff = dsc[4], ld = dsc[5];
+  double2* out = row + moff;
+  bool bad = false;
+  for (int64_t t = threadIdx.x; t < m * n; t += kThreads) {
+    const int64_t i = t % m, j = t / m;
+    double2 g[D * D];
+    bad |= !green_xy(P, pts, r0 + i, pts, c0 + j, g);
+#pragma unroll
+    for (int b = 0; b < D; ++b)
+#pragma unroll
+      for (int a = 0; a < D; ++a) out[(D * j + b) * ld + D * i + a] = g[a * D + b];
+  }
+  if (bad) atomicOr(err, 1);
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads) eval_block(GreenParams P, PointsSoA X, PointsSoA Y, int64_t m, int64_t n,
+                                                       double2* __restrict__ out, int32_t* __restrict__ err) {
+  const int64_t total = m * n;
+  bool bad = false;
+  for (int64_t t = blockIdx.x * (int64_t)kThreads + threadIdx.x; t < total; t += (int64_t)gridDim.x * kThreads) {
+    const int64_t i = t / n, j = t % n;
+    double2 g[D * D];
+    bad |= !green_xy(P, X, i, Y, j, g);
+    const int64_t ldo = D * n;
+#pragma unroll
+    for (int a = 0; a < D; ++a)
+#pragma unroll
+      for (int b = 0; b < D; ++b) out[(D * i + a) * ldo + D * j + b] = g[a * D + b];
+  }
+  if (bad) atomicOr(err, 1);
+}
+
+}  // namespace
+
+int launch_dense_fill(Ctx& c, const GreenParams& P, const PointsSoA& pts, const int64_t* d_desc, int64_t ndense,
+                      double2* row_stream, int32_t* d_err) {
+  if (ndense == 0) return HMX_OK;
+  if (P.kind == 0)
+    dense_fill<1><<<(unsigned)ndense, kThreads, 0, c.stream>>>(P, pts, d_desc, row_stream, d_err);
+  else
+    dense_fill<3><<<(unsigned)ndense, kThreads, 0, c.stream>>>(P, pts, d_desc, row_stream, d_err);
+  HMX_CUDA_TRY(cudaGetLastError());
+  return HMX_OK;
+}
+
+int launch_eval_block(Ctx& c, const GreenParams& P, const PointsSoA& X, const PointsSoA& Y, int64_t m, int64_t n,
+                      double2* out, int32_t* d_err) {
+  const int64_t total = m * n;
+  if (total == 0) return HMX_OK;
+  int64_t grid = hmx_cdiv(total, kThreads);
+  const int64_t cap = (int64_t)c.num_sms * 8;
+  if (grid > cap) grid = cap;
+  if (P.kind == 0)
+    eval_block<1><<<(unsigned)grid, kThreads, 0, c.stream>>>(P, X, Y, m, n, out, d_err);
+  else
+    eval_block<3><<<(unsigned)grid, kThreads, 0, c.stream>>>(P, X, Y, m, n, out, d_err);
+  HMX_CUDA_TRY(cudaGetLastError());
+  return HMX_OK;
+}
+
+}  // namespace hmx

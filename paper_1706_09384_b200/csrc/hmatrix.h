@@ -1,0 +1,146 @@
+// Internal device-side H-matrix representation and cross-module entry points.
+//
+// HBM layout:
+//  * row stream  -- every leaf's row-side payload grouped by ROW SEGMENT (all
+//    leaves sharing one row cluster [r0, r1)).  Segment g is ONE column-major
+//    (d m_g) x C_g complex128 matrix: the dense leaves' (d m) x (d n) blocks and
+//    the low-rank leaves' U factors (d m) x r side by side.
+//  * V stream    -- low-rank V factors, (d n) x r column-major per leaf.
+//  * source slots s (length sum_g C_g) -- per matvec, dense slots get the
+//    leaf's x piece, low-rank slots get t = V^H x.  Phase 2 is then a plain
+//    batched GEMV y_g += M_g s_g per segment, written (non-atomically) to a
+//    per-level partial vector; a last pass sums the levels in fixed order and
+//    scatters through the cluster-tree permutation -> deterministic y.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <vector>
+
+#include "green.cuh"
+
+namespace hmx {
+
+struct Ctx {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  int num_sms = 148;
+  size_t l2_bytes = 0;
+};
+
+// phase-1 job: one warp computes s[soff] = V[voff : voff+len]^H x_tree[xoff : xoff+len]
+// (kind 1) or copies x_tree[xoff : xoff+len] -> s[soff : soff+len] (kind 0)
+struct MvJob1 {
+  int64_t voff;
+  int64_t xoff;
+  int64_t soff;
+  int32_t len;
+  int32_t kind;
+};
+
+// phase-2 tile: rows [row0, row0 + nrows) of segment g
+struct MvTile2 {
+  int64_t moff;    // segment matrix offset in the row stream
+  int64_t soff;    // segment source offset
+  int64_t yoff;    // level-buffer offset of the segment's first row (level * n + d * r0)
+  int32_t ld;      // d * m_g
+  int32_t ncols;   // C_g
+  int32_t row0;    // first row of this tile inside the segment
+  int32_t nrows;
+};
+
+struct DeviceH {
+  Ctx* ctx = nullptr;
+  int kind = 0, d = 1;
+  int64_t np = 0, n = 0;  // points, dofs
+  int64_t nb = 0;
+  std::vector<int64_t> table;  // nb x 5 (kind, r0, r1, c0, c1)
+  std::vector<int64_t> steps, rank_before, rank_after;
+  std::vector<int32_t> flags;
+  // row-stream placement of every leaf (for export)
+  std::vector<int64_t> leaf_moff, leaf_ld, leaf_voff;
+  int64_t nlevels = 1;
+
+  int64_t* d_perm = nullptr;
+  double2* d_row = nullptr;  // row stream
+  int64_t row_elems = 0;
+  double2* d_v = nullptr;  // V stream
+  int64_t v_elems = 0;
+  double2* d_s = nullptr;  // source slots
+  int64_t s_elems = 0;
+  double2* d_xt = nullptr;  // x in tree order
+  double2* d_ylev = nullptr;  // nlevels x n partial y
+  double2* d_xio = nullptr;  // device staging for host x / y
+  double2* d_yio = nullptr;
+  MvJob1* d_job1 = nullptr;
+  int64_t njob1 = 0;
+  MvTile2* d_tile2 = nullptr;
+  int64_t ntile2 = 0;
+  int32_t* d_lev_cover = nullptr;  // unused placeholder
+  // algorithmic traffic of one matvec (bytes), SURVEY 8(d)
+  double mv_bytes = 0;
+  double dense_bytes = 0, lr_bytes = 0;
+  // assembly statistics
+  double t_dense_ms = 0, t_aca_ms = 0, t_recomp_ms = 0, t_form_ms = 0, t_total_ms = 0;
+  int64_t pairs_evaluated = 0;
+  int64_t aca_passes = 0, n_fallback = 0, n_unconverged = 0, n_regularized = 0;
+  double flops_assembly = 0;
+  // pinned host staging for host-pointer matvec
+  double2* h_pin_x = nullptr;
+  double2* h_pin_y = nullptr;
+};
+
+// matvec.cu
+int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& seg_level);
+int matvec_device(DeviceH& H, const double2* x_orig_dev, double2* y_orig_dev, float* phase_ms);
+
+// dense.cu
+int launch_dense_fill(Ctx& c, const GreenParams& P, const PointsSoA& pts, const int64_t* d_desc, int64_t ndense,
+                      double2* row_stream, int32_t* d_err);
+int launch_eval_block(Ctx& c, const GreenParams& P, const PointsSoA& X, const PointsSoA& Y, int64_t m, int64_t n,
+                      double2* out, int32_t* d_err);
+
+// aca.cu
+struct AcaDesc {
+  int64_t r0, c0;       // first row / column point (tree order)
+  int32_t m, n;         // points
+  int32_t kcap;         // column capacity of U / V
+  int32_t max_rank;     // in scalar columns
+  int64_t uoff, voff;   // workspace offsets (ld = d m, d n)
+  int64_t goff;         // Gram workspace offset (two kcap x kcap matrices)
+};
+struct AcaOut {
+  int32_t steps;
+  int32_t rank;      // d * steps
+  int32_t status;    // bit0 converged, bit1 max_rank, bit2 capacity overflow, bit3 fallback needed
+  int32_t zero_rows;
+};
+int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const AcaDesc* d_desc, const int32_t* d_order,
+               int64_t nblk, int kcap_max, int m_max, double eps, double sigma3_floor, double2* U, double2* V,
+               double2* G, AcaOut* d_out);
+
+// recompress.cu
+struct RecDesc {
+  int64_t goff;      // Gram pair (G_U at goff, G_V at goff + kcap*kcap), ld = kcap
+  int64_t woff;      // K x K scratch workspace (2 matrices) offset
+  int32_t K;         // ACA rank
+  int32_t kcap;
+};
+int launch_recompress_core(Ctx& c, const RecDesc* d_desc, int64_t nblk, int kmax, double eps, int rule, double2* G,
+                           double2* W, int32_t* d_rank, int32_t* d_flags);
+struct FormDesc {
+  int64_t aoff;   // source factor (U or V workspace), ld = lda
+  int64_t woff;   // K x r coefficient matrix in W (ld = K)
+  int64_t coff;   // destination (row stream or V stream)
+  int32_t rows, K, r, lda, ldc;
+  int32_t pad;
+};
+int launch_form(Ctx& c, const FormDesc* d_desc, int64_t nitems, int64_t ntiles_total, const int64_t* d_tile_start,
+                const double2* A, const double2* W, double2* C);
+
+// gmres.cu
+int gmres_device(DeviceH& H, const double2* b_dev, double2* x_dev, double tol, int restart, int64_t max_iters,
+                 int64_t* iters, std::vector<double>& history, int* converged);
+
+}  // namespace hmx

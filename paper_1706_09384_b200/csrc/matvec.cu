@@ -1,0 +1,269 @@
+// H-matrix-vector product y = A_H x.
+//
+// One pass over the packed HBM streams (layout in hmatrix.h):
+//   gather    x_tree[d k + a] = x[d perm[k] + a]                      (tree order)
+//   phase 1   warp per job: s[slot] = V_b(:, l)^H x_tree(cols of b)   (low-rank)
+//             or s[slot..] = x_tree(cols of b)                        (dense)
+//   phase 2   CTA per (row segment, 256-row tile): y_lev[level][rows] =
+//             M_g(rows, :) s_g -- column-major M_g, lanes over rows so each
+//             load instruction is a contiguous 512 B, columns split over up to
+//             8 thread groups for short segments, reduced in shared memory
+//   finalize  y[d perm[k] + a] = sum_level y_lev[level][d k + a]   (fixed order)
+// Every (level, row) is written by exactly one phase-2 tile, so y is
+// bit-reproducible run to run (no floating-point atomics).
+// The pass is HBM-bound (complex128 GEMV = 0.5 flop/B); bytes per call are
+// H.mv_bytes = 16 (sum dense d^2 m n + sum r d (m + n)) + 32 d N.
+#include <algorithm>
+#include <map>
+#include <numeric>
+
+#include "hmatrix.h"
+
+namespace hmx {
+
+namespace {
+
+constexpr int kThreads = 256;
+
+__global__ void mv_gather(const double2* __restrict__ x, const int64_t* __restrict__ perm, int d, int64_t np,
+                          double2* __restrict__ xt) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < np * d; k += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t p = k / d, a = k - p * d;
+    xt[k] = x[d * perm[p] + a];
+  }
+}
+
+__global__ void mv_phase1(const MvJob1* __restrict__ jobs, int64_t njobs, const double2* __restrict__ V,
+                          const double2* __restrict__ xt, double2* __restrict__ s) {
+  const int lane = threadIdx.x & 31;
+  const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+  const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+  for (int64_t j = wid; j < njobs; j += nw) {
+    const MvJob1 J = jobs[j];
+    const double2* xp = xt + J.xoff;
+    if (J.kind == 0) {
+      for (int q = lane; q < J.len; q += 32) s[J.soff + q] = xp[q];
+      continue;
+    }
+    const double2* vp = V + J.voff;
+    double2 a0 = cmk(0, 0), a1 = cmk(0, 0);
+    int q = lane;
+    for (; q + 32 < J.len; q += 64) {
+      const double2 v0 = vp[q], v1 = vp[q + 32];
+      const double2 x0 = xp[q], x1 = xp[q + 32];
+      a0 = cfma_ca(v0, x0, a0);
+      a1 = cfma_ca(v1, x1, a1);
+    }
+    if (q < J.len) a0 = cfma_ca(vp[q], xp[q], a0);
+    double2 acc = warp_sum(cadd(a0, a1));
+    if (lane == 0) s[J.soff] = acc;
+  }
+}
+
+__global__ void __launch_bounds__(kThreads) mv_phase2(const MvTile2* __restrict__ tiles,
+                                                      const double2* __restrict__ row,
+                                                      const double2* __restrict__ s, double2* __restrict__ ylev) {
+  __shared__ double2 red[kThreads];
+  const MvTile2 T = tiles[blockIdx.x];
+  const int tid = threadIdx.x;
+  int r32 = ((T.nrows + 31) / 32) * 32;
+  if (r32 > kThreads) r32 = kThreads;
+  const int parts = kThreads / r32;
+  const int rl = tid % r32, part = tid / r32;
+  const bool valid = rl < T.nrows && part < parts;
+  double2 a0 = cmk(0, 0), a1 = cmk(0, 0);
+  if (valid) {
+    const int64_t ld = T.ld;
+    const double2* mp = row + T.moff + T.row0 + rl;
+    const double2* sp = s + T.soff;
+    int c = part;
+    const int step = parts;
+    for (; c + 3 * step < T.ncols; c += 4 * step) {
+      const double2 m0 = mp[(int64_t)c * ld];
+      const double2 m1 = mp[(int64_t)(c + step) * ld];
+      const double2 m2 = mp[(int64_t)(c + 2 * step) * ld];
+      const double2 m3 = mp[(int64_t)(c + 3 * step) * ld];
+      const double2 s0 = sp[c], s1 = sp[c + step], s2 = sp[c + 2 * step], s3 = sp[c + 3 * step];
+      a0 = cfma(m0, s0, a0);
+      a1 = cfma(m1, s1, a1);
+      a0 = cfma(m2, s2, a0);
+      a1 = cfma(m3, s3, a1);
+    }
+    for (; c < T.ncols; c += step) a0 = cfma(mp[(int64_t)c * ld], sp[c], a0);
+  }
+  const double2 acc = cadd(a0, a1);
+  if (parts == 1) {
+    if (valid) ylev[T.yoff + T.row0 + rl] = acc;
+    return;
+  }
+  red[tid] = acc;
+  __syncthreads();
+  if (part == 0 && rl < T.nrows) {
+    double2 t = red[rl];
+    for (int p = 1; p < parts; ++p) t = cadd(t, red[p * r32 + rl]);
+    ylev[T.yoff + T.row0 + rl] = t;
+  }
+}
+
+__global__ void mv_finalize(const double2* __restrict__ ylev, int64_t nlev, int64_t n, const int64_t* __restrict__ perm,
+                            int d, double2* __restrict__ y) {
+  for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
+    double2 t = ylev[k];
+    for (int64_t l = 1; l < nlev; ++l) t = cadd(t, ylev[l * n + k]);
+    const int64_t p = k / d, a = k - p * d;
+    y[d * perm[p] + a] = t;
+  }
+}
+
+}  // namespace
+
+// Builds segments, levels, stream offsets and the phase-1/phase-2 work lists.
+// Requires H.table, H.rank_after (low-rank leaves), H.d, H.np.
+int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
+  const int d = H.d;
+  const int64_t nb = H.nb;
+  // ---- row segments keyed by (r0, r1)
+  std::map<std::pair<int64_t, int64_t>, int64_t> segid;
+  for (int64_t b = 0; b < nb; ++b) segid.emplace(std::make_pair(H.table[5 * b + 1], H.table[5 * b + 2]), 0);
+  std::vector<std::pair<int64_t, int64_t>> segs;
+  segs.reserve(segid.size());
+  for (auto& kv : segid) segs.push_back(kv.first);
+  // nesting order: r0 ascending, r1 descending
+  std::sort(segs.begin(), segs.end(), [](const auto& a, const auto& b) {
+    return a.first != b.first ? a.first < b.first : a.second > b.second;
+  });
+  const int64_t ns = (int64_t)segs.size();
+  for (int64_t g = 0; g < ns; ++g) segid[segs[g]] = g;
+  std::vector<int64_t> level(ns);
+  {
+    std::vector<int64_t> stack;
+    int64_t maxlev = 0;
+    for (int64_t g = 0; g < ns; ++g) {
+      while (!stack.empty() && segs[stack.back()].second <= segs[g].first) stack.pop_back();
+      level[g] = (int64_t)stack.size();
+      maxlev = std::max(maxlev, level[g]);
+      stack.push_back(g);
+    }
+    H.nlevels = maxlev + 1;
+  }
+  std::vector<int64_t> ncols(ns, 0), colstart(nb, 0), bseg(nb);
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t g = segid[std::make_pair(H.table[5 * b + 1], H.table[5 * b + 2])];
+    bseg[b] = g;
+    colstart[b] = ncols[g];
+    const int64_t n = H.table[5 * b + 4] - H.table[5 * b + 3];
+    ncols[g] += H.table[5 * b] == 0 ? d * n : H.rank_after[b];
+  }
+  std::vector<int64_t> moff(ns), soff(ns);
+  int64_t mo = 0, so = 0;
+  for (int64_t g = 0; g < ns; ++g) {
+    moff[g] = mo;
+    soff[g] = so;
+    mo += d * (segs[g].second - segs[g].first) * ncols[g];
+    so += ncols[g];
+  }
+  H.row_elems = mo;
+  H.s_elems = so;
+  H.leaf_moff.assign(nb, 0);
+  H.leaf_ld.assign(nb, 0);
+  H.leaf_voff.assign(nb, -1);
+  int64_t vo = 0;
+  double dense_b = 0, lr_b = 0;
+  std::vector<MvJob1> jobs;
+  for (int64_t b = 0; b < nb; ++b) {
+    const int64_t g = bseg[b];
+    const int64_t m = H.table[5 * b + 2] - H.table[5 * b + 1];
+    const int64_t n = H.table[5 * b + 4] - H.table[5 * b + 3];
+    const int64_t ld = d * m;
+    H.leaf_ld[b] = ld;
+    H.leaf_moff[b] = moff[g] + colstart[b] * ld;
+    const int64_t c0 = H.table[5 * b + 3];
+    if (H.table[5 * b] == 0) {
+      jobs.push_back(MvJob1{0, d * c0, soff[g] + colstart[b], (int32_t)(d * n), 0});
+      dense_b += 16.0 * ld * d * n;
+    } else {
+      const int64_t r = H.rank_after[b];
+      H.leaf_voff[b] = vo;
+      for (int64_t l = 0; l < r; ++l)
+        jobs.push_back(MvJob1{vo + l * d * n, d * c0, soff[g] + colstart[b] + l, (int32_t)(d * n), 1});
+      vo += d * n * r;
+      lr_b += 16.0 * r * d * (m + n);
+    }
+  }
+  H.v_elems = vo;
+  // longest jobs first
+  std::stable_sort(jobs.begin(), jobs.end(), [](const MvJob1& a, const MvJob1& b) { return a.len > b.len; });
+  std::vector<MvTile2> tiles;
+  for (int64_t g = 0; g < ns; ++g) {
+    if (ncols[g] == 0) continue;
+    const int64_t rows = d * (segs[g].second - segs[g].first);
+    for (int64_t r0 = 0; r0 < rows; r0 += kThreads) {
+      MvTile2 t;
+      t.moff = moff[g];
+      t.soff = soff[g];
+      t.yoff = level[g] * H.n + d * segs[g].first;
+      t.ld = (int32_t)rows;
+      t.ncols = (int32_t)ncols[g];
+      t.row0 = (int32_t)r0;
+      t.nrows = (int32_t)std::min<int64_t>(kThreads, rows - r0);
+      tiles.push_back(t);
+    }
+  }
+  std::stable_sort(tiles.begin(), tiles.end(), [](const MvTile2& a, const MvTile2& b) {
+    return (int64_t)a.nrows * a.ncols > (int64_t)b.nrows * b.ncols;
+  });
+  H.njob1 = (int64_t)jobs.size();
+  H.ntile2 = (int64_t)tiles.size();
+  H.dense_bytes = dense_b;
+  H.lr_bytes = lr_b;
+  H.mv_bytes = dense_b + lr_b + 32.0 * H.n;
+  Ctx& c = *H.ctx;
+  HMX_CUDA_TRY(cudaMalloc(&H.d_row, sizeof(double2) * std::max<int64_t>(H.row_elems, 1)));
+  HMX_CUDA_TRY(cudaMalloc(&H.d_v, sizeof(double2) * std::max<int64_t>(H.v_elems, 1)));
+  HMX_CUDA_TRY(cudaMalloc(&H.d_s, sizeof(double2) * std::max<int64_t>(H.s_elems, 1)));
+  HMX_CUDA_TRY(cudaMalloc(&H.d_xt, sizeof(double2) * H.n));
+  HMX_CUDA_TRY(cudaMalloc(&H.d_ylev, sizeof(double2) * H.n * H.nlevels));
+  HMX_CUDA_TRY(cudaMemsetAsync(H.d_ylev, 0, sizeof(double2) * H.n * H.nlevels, c.stream));
+  HMX_CUDA_TRY(cudaMalloc(&H.d_xio, sizeof(double2) * H.n));
+  HMX_CUDA_TRY(cudaMalloc(&H.d_yio, sizeof(double2) * H.n));
+  HMX_CUDA_TRY(cudaMalloc(&H.d_job1, sizeof(MvJob1) * std::max<int64_t>(H.njob1, 1)));
+  HMX_CUDA_TRY(cudaMalloc(&H.d_tile2, sizeof(MvTile2) * std::max<int64_t>(H.ntile2, 1)));
+  if (H.njob1)
+    HMX_CUDA_TRY(cudaMemcpyAsync(H.d_job1, jobs.data(), sizeof(MvJob1) * H.njob1, cudaMemcpyHostToDevice, c.stream));
+  if (H.ntile2)
+    HMX_CUDA_TRY(
+        cudaMemcpyAsync(H.d_tile2, tiles.data(), sizeof(MvTile2) * H.ntile2, cudaMemcpyHostToDevice, c.stream));
+  HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  return HMX_OK;
+}
+
+int matvec_device(DeviceH& H, const double2* x, double2* y, float* phase_ms) {
+  Ctx& c = *H.ctx;
+  cudaEvent_t ev[5];
+  if (phase_ms) {
+    for (int i = 0; i < 5; ++i) HMX_CUDA_TRY(cudaEventCreate(&ev[i]));
+    HMX_CUDA_TRY(cudaEventRecord(ev[0], c.stream));
+  }
+  const int eg = std::max<int64_t>(1, std::min<int64_t>(hmx_cdiv(H.n, kThreads), 4 * c.num_sms));
+  mv_gather<<<eg, kThreads, 0, c.stream>>>(x, H.d_perm, H.d, H.np, H.d_xt);
+  if (phase_ms) HMX_CUDA_TRY(cudaEventRecord(ev[1], c.stream));
+  if (H.njob1) {
+    const int64_t warps = std::min<int64_t>(H.njob1, (int64_t)c.num_sms * 64);
+    mv_phase1<<<(unsigned)hmx_cdiv(warps * 32, kThreads), kThreads, 0, c.stream>>>(H.d_job1, H.njob1, H.d_v, H.d_xt,
+                                                                                   H.d_s);
+  }
+  if (phase_ms) HMX_CUDA_TRY(cudaEventRecord(ev[2], c.stream));
+  if (H.ntile2) mv_phase2<<<(unsigned)H.ntile2, kThreads, 0, c.stream>>>(H.d_tile2, H.d_row, H.d_s, H.d_ylev);
+  if (phase_ms) HMX_CUDA_TRY(cudaEventRecord(ev[3], c.stream));
+  mv_finalize<<<eg, kThreads, 0, c.stream>>>(H.d_ylev, H.nlevels, H.n, H.d_perm, H.d, y);
+  HMX_CUDA_TRY(cudaGetLastError());
+  if (phase_ms) {
+    HMX_CUDA_TRY(cudaEventRecord(ev[4], c.stream));
+    HMX_CUDA_TRY(cudaEventSynchronize(ev[4]));
+    for (int i = 0; i < 4; ++i) HMX_CUDA_TRY(cudaEventElapsedTime(&phase_ms[i], ev[i], ev[i + 1]));
+    for (int i = 0; i < 5; ++i) cudaEventDestroy(ev[i]);
+  }
+  return HMX_OK;
+}
+
+}  // namespace hmx

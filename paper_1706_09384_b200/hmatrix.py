@@ -1,0 +1,198 @@
+"""H-matrix container, device assembly and H-matvec -- the reference's
+``hmatx.hmatrix`` entry points: ``assemble(spec, cloud, ct,
+bt, cfg) -> (HMatrix, StorageReport)``, ``matvec(h, x)``,
+``storage_report(h)``.  Everything numeric runs in libhmx.so (``hmx_assemble``,
+``hmx_matvec``); an assembled HMatrix is immutable and lives in HBM.
+"""
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import _lib
+from .geometry import sparsity_pattern
+from .lowrank import TRUNC_RULES, ACAConfig, LowRankFactor
+
+HOST, DEVICE = 0, 1
+
+
+@dataclass(frozen=True)
+class StorageReport:
+    """N_s, N^2, tau = N_s / N^2, max ranks, and the
+    section-5.1 bound 2 C_sp max(r_max, N_leaf) N (log2 N - log2 N_leaf + 1)."""
+
+    n_stored: int
+    n_dense_equiv: int
+    tau: float
+    max_rank_before: int
+    max_rank_after: int
+    bound: float | None = None
+
+
+class HMatrix:
+    """Device-resident H-matrix."""
+
+    def __init__(self, handle, d, n_points, block_tree=None, perm=None, spec=None, table=None, device=0):
+        self._h = handle
+        self.d = d
+        self.n_points = n_points
+        self.block_tree = block_tree
+        self.perm = perm
+        self.spec = spec
+        self.table = table
+        self.device = device
+
+    def __del__(self):
+        try:
+            if self._h:
+                _lib.lib().hmx_hmatrix_free(self._h)
+                self._h = None
+        except Exception:
+            pass
+
+    @property
+    def shape(self):
+        n = self.d * self.n_points
+        return (n, n)
+
+    @property
+    def handle(self):
+        return self._h
+
+    def stats(self):
+        st = _lib.HmxStats()
+        _lib.check(_lib.lib().hmx_hmatrix_stats(self._h, C.byref(st)), "hmx_hmatrix_stats")
+        return st.as_dict()
+
+    def block_info(self):
+        nb = len(self.table)
+        steps = np.empty(nb, np.int64)
+        rb = np.empty(nb, np.int64)
+        ra = np.empty(nb, np.int64)
+        fl = np.empty(nb, np.int32)
+        _lib.check(_lib.lib().hmx_hmatrix_block_info(self._h, _lib.ptr(steps), _lib.ptr(rb), _lib.ptr(ra),
+                                                     _lib.ptr(fl)), "block_info")
+        return dict(steps=steps, rank_before=rb, rank_after=ra, flags=fl)
+
+    def block(self, b):
+        """Leaf payload: dense ndarray or LowRankFactor (tree-order index ranges)."""
+        k, r0, r1, c0, c1 = (int(t) for t in self.table[b][:5])
+        dm, dn = self.d * (r1 - r0), self.d * (c1 - c0)
+        if k == 0:
+            a = np.empty((dm, dn), np.complex128)
+            _lib.check(_lib.lib().hmx_hmatrix_get_block(self._h, b, _lib.ptr(a), None), "get_block")
+            return a
+        r = int(self.block_info()["rank_after"][b])
+        u = np.empty((dm, r), np.complex128)
+        v = np.empty((dn, r), np.complex128)
+        if r:
+            _lib.check(_lib.lib().hmx_hmatrix_get_block(self._h, b, _lib.ptr(u), _lib.ptr(v)), "get_block")
+        return LowRankFactor(u, v)
+
+    def use_stream(self, stream_ptr):
+        """Launch on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""
+        _lib.check(_lib.lib().hmx_ctx_set_stream(_lib.context(self.device), int(stream_ptr)), "set_stream")
+
+    @classmethod
+    def from_factors(cls, d, n_points, perm, table, payload, device=0):
+        """Import leaf payloads (dense arrays / (U, V) pairs, tree-order ranges).
+        Used to run the device matvec on oracle-assembled factors."""
+        table = np.ascontiguousarray(np.asarray(table)[:, :5], dtype=np.int64)
+        nb = len(table)
+        keep = []
+        A = (C.c_void_p * nb)()
+        B = (C.c_void_p * nb)()
+        ranks = np.zeros(nb, np.int64)
+        for b, p in enumerate(payload):
+            if table[b, 0] == 0:
+                a = np.ascontiguousarray(p, dtype=np.complex128)
+                keep.append(a)
+                A[b] = a.ctypes.data
+            else:
+                u = np.ascontiguousarray(p[0], dtype=np.complex128)
+                v = np.ascontiguousarray(p[1], dtype=np.complex128)
+                keep += [u, v]
+                ranks[b] = u.shape[1]
+                A[b] = u.ctypes.data
+                B[b] = v.ctypes.data
+        perm = np.ascontiguousarray(perm, dtype=np.int64)
+        h = C.c_void_p()
+        _lib.check(_lib.lib().hmx_hmatrix_load(_lib.context(device), d, n_points, _lib.ptr(perm), _lib.ptr(table),
+                                               nb, _lib.ptr(ranks), A, B, C.byref(h)), "hmx_hmatrix_load")
+        return cls(h, d, n_points, perm=perm, table=table, device=device)
+
+
+def _spec_kernel(spec):
+    return spec.c_kernel()
+
+
+def assemble(spec, cloud, ct, bt, cfg=ACAConfig(), self_shift=None, device=0):
+    """Device assembly: dense leaves evaluated directly,
+    admissible leaves by batched ACA (scalar for d = 1, sigma_3 vector for d = 3)
+    + recompression.  ``self_shift`` defaults to zeta = N_c.
+    Returns ``(HMatrix, StorageReport)``."""
+    if spec.d != cloud.d and cloud.d != 1:
+        raise ValueError("kernel dimension does not match the cloud")
+    pts = np.ascontiguousarray(ct.points_tree, dtype=np.float64)
+    nrm = ct.normals_tree if spec.variant == "elasto_t" else None
+    if spec.variant == "elasto_t" and nrm is None:
+        raise ValueError("ElastoT requires normals on the cloud")
+    perm = np.ascontiguousarray(ct.permutation, dtype=np.int64)
+    table = bt.leaf_table
+    c = _lib.HmxAcaCfg()
+    c.eps = cfg.eps_aca
+    c.max_rank = cfg.max_rank or 0
+    c.sigma3_floor = cfg.sigma3_floor
+    c.trunc_rule = TRUNC_RULES[cfg.trunc_rule]
+    c.mem_budget_gb = cfg.mem_budget_gb
+    kern = _spec_kernel(spec)
+    shift = float(cloud.size) if self_shift is None else float(self_shift)
+    h = C.c_void_p()
+    _lib.check(_lib.lib().hmx_assemble(_lib.context(device), C.byref(kern), _lib.ptr(pts), _lib.ptr(nrm),
+                                       pts.shape[0], _lib.ptr(perm), _lib.ptr(table), len(table), C.byref(c),
+                                       shift, C.byref(h)), "hmx_assemble")
+    H = HMatrix(h, spec.d, pts.shape[0], block_tree=bt, perm=perm, spec=spec, table=bt.table, device=device)
+    return H, storage_report(H)
+
+
+def storage_report(h):
+    """SPEC.md:431-439."""
+    st = h.stats()
+    N = h.d * h.n_points
+    bound = None
+    if h.block_tree is not None:
+        csp = sparsity_pattern(h.block_tree)
+        nl = h.d * h.block_tree.rows.n_leaf
+        rmax = max(st["max_rank_after"], nl)
+        bound = 2.0 * csp * rmax * N * (math.log2(N) - math.log2(nl) + 1.0)
+    return StorageReport(n_stored=int(st["n_stored"]), n_dense_equiv=N * N, tau=st["n_stored"] / float(N * N),
+                         max_rank_before=int(st["max_rank_before"]), max_rank_after=int(st["max_rank_after"]),
+                         bound=bound)
+
+
+def _is_cuda_tensor(x):
+    return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda", False))
+
+
+def matvec(h, x, out=None):
+    """y = A_H x; x in original point order.  numpy in ->
+    numpy out (host copies inside); a CUDA complex128 torch tensor in -> a
+    CUDA tensor out (no host round trip)."""
+    n = h.d * h.n_points
+    if _is_cuda_tensor(x):
+        import torch
+
+        if x.dtype != torch.complex128 or x.numel() != n or not x.is_contiguous():
+            raise ValueError("dimension mismatch")
+        y = torch.empty_like(x) if out is None else out
+        _lib.check(_lib.lib().hmx_matvec(h.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), DEVICE),
+                   "hmx_matvec")
+        return y
+    x = np.ascontiguousarray(x, dtype=np.complex128)
+    if x.shape != (n,):
+        raise ValueError("dimension mismatch")
+    y = np.empty_like(x) if out is None else out
+    _lib.check(_lib.lib().hmx_matvec(h.handle, _lib.ptr(x), _lib.ptr(y), HOST), "hmx_matvec")
+    return y

@@ -1,0 +1,162 @@
+"""GPU parity: libhmx.so (through the C-ABI) against the CPU oracle.
+
+Tolerances (BASELINE.json north_star / SPEC.md):
+* entries: max |A_gpu - A_oracle| <= 1e-13 max |A| per block (1e-12 for the
+  low-frequency U131k regime);
+* H-matvec on identical factors: relative error <= 1e-10;
+* ACA steps and recompressed ranks: +/-1 per block;
+* compressed blocks vs dense: ||A_b - U V^H||_F <= 3 eps ||A_b||_F
+  and matvec vs dense <= 3 eps;
+* GMRES iteration counts: +/-1.
+"""
+
+import numpy as np
+import pytest
+
+import paper_1706_09384_b200 as hmx
+from oracle import hmatrix as OH
+from oracle import kernels as OK
+from oracle import solve as OS
+from tests._problems import Problem
+
+pytestmark = pytest.mark.gpu
+
+
+def _rand_pts(rng, n):
+    return rng.standard_normal((n, 3))
+
+
+@pytest.mark.parametrize("kind", ["H", "U", "T"])
+def test_eval_block_matches_oracle(kind):
+    rng = np.random.default_rng(7)
+    X = _rand_pts(rng, 37)
+    Y = _rand_pts(rng, 53)
+    Y[5] = X[3]  # coincident pair -> self rule
+    NY = rng.standard_normal((53, 3))
+    NY /= np.linalg.norm(NY, axis=1)[:, None]
+    if kind == "H":
+        args = (11.3,)
+        g, o = hmx.scalar_block, OK.scalar_block
+    elif kind == "U":
+        args = (9.26, 16.04, 1 / 16.04**2)
+        g, o = hmx.elasto_u_block, OK.elasto_u_block
+    else:
+        args = (26.2, 45.375, 1.0, 1.0, 1 / 45.375**2)
+        g, o = hmx.elasto_t_block, OK.elasto_t_block
+    extra = (NY,) if kind == "T" else ()
+    a = g(*args, X, Y, *extra, self_shift=4096.0)
+    b = o(*args, X, Y, *extra, self_shift=4096.0)
+    assert a.shape == b.shape and a.dtype == np.complex128 and a.flags.c_contiguous
+    assert np.abs(a - b).max() <= 1e-13 * np.abs(b).max()
+    # self pair exactly zeta * I
+    d = 1 if kind == "H" else 3
+    np.testing.assert_array_equal(a[d * 3 : d * 3 + d, d * 5 : d * 5 + d], 4096.0 * np.eye(d))
+    # no self rule -> None (reference returns None, caller raises)
+    assert g(*args, X, Y, *extra) is None
+
+
+def test_kernel_known_answers():
+    # SPEC.md:184-186
+    one = np.array([[0.0, 0.0, 0.0]])
+    e1 = np.array([[1.0, 0.0, 0.0]])
+    assert abs(hmx.scalar_block(np.pi, one, e1)[0, 0] - (-1 / (4 * np.pi))) < 1e-15
+    assert abs(hmx.scalar_block(0.0, one, e1)[0, 0] - 1 / (4 * np.pi)) < 1e-16
+    assert abs(hmx.scalar_block(0.0, one, 2 * e1)[0, 0] - 1 / (8 * np.pi)) < 1e-16
+    # coplanar zero patterns exact to 1e-14 scaled
+    rng = np.random.default_rng(3)
+    X = np.column_stack([rng.standard_normal((20, 2)), np.zeros(20)])
+    Y = np.column_stack([rng.standard_normal((20, 2)), np.zeros(20)])
+    U = hmx.elasto_u_block(5.0, 8.0, 1 / 64, X, Y).reshape(20, 3, 20, 3)
+    for a, b in [(0, 2), (1, 2), (2, 0), (2, 1)]:
+        assert np.abs(U[:, a, :, b]).max() <= 1e-14 * np.abs(U).max()
+    NY = np.tile([0.0, 0.0, 1.0], (20, 1))
+    T = hmx.elasto_t_block(5.0, 8.0, 1.0, 1.0, 1 / 64, X, Y, NY).reshape(20, 3, 20, 3)
+    for a, b in [(0, 0), (0, 1), (1, 0), (1, 1), (2, 2)]:
+        assert np.abs(T[:, a, :, b]).max() <= 1e-14 * np.abs(T).max()
+    # flipping n negates T
+    Tm = hmx.elasto_t_block(5.0, 8.0, 1.0, 1.0, 1 / 64, X, Y, -NY).reshape(20, 3, 20, 3)
+    np.testing.assert_allclose(Tm, -T, rtol=0, atol=1e-15 * np.abs(T).max())
+    # reciprocity U(x,y) = U(y,x)^T
+    A = hmx.elasto_u_block(5.0, 8.0, 1 / 64, X, Y)
+    B = hmx.elasto_u_block(5.0, 8.0, 1 / 64, Y, X)
+    assert np.abs(A - B.T).max() <= 1e-10 * np.abs(A).max()
+
+
+@pytest.mark.parametrize("tag,n", [("H4k", 2048), ("U8k", 1024)])
+def test_matvec_on_oracle_factors(tag, n):
+    pb = Problem(tag, n)
+    oh = pb.oracle_h()
+    H = hmx.HMatrix.from_factors(pb.d, pb.N, pb.ct.permutation, pb.table, oh.payload)
+    for seed in range(3):
+        x = pb.rhs(seed)
+        y = hmx.matvec(H, x)
+        yo = OH.matvec(oh, x)
+        assert np.linalg.norm(y - yo) <= 1e-10 * np.linalg.norm(yo)
+    z = hmx.matvec(H, np.zeros(pb.d * pb.N, complex))
+    assert not np.any(z)
+    x1, x2 = pb.rhs(1), pb.rhs(2)
+    lhs = hmx.matvec(H, 2.0 * x1 - 3j * x2)
+    rhs = 2.0 * hmx.matvec(H, x1) - 3j * hmx.matvec(H, x2)
+    assert np.linalg.norm(lhs - rhs) <= 1e-12 * np.linalg.norm(rhs)
+    # deterministic
+    np.testing.assert_array_equal(hmx.matvec(H, x1), hmx.matvec(H, x1))
+
+
+def _block_errors(pb, H, A):
+    d = pb.d
+    out = []
+    for b, (k, r0, r1, c0, c1) in enumerate(pb.table):
+        if k != 1:
+            continue
+        f = H.block(b)
+        Ab = A[d * r0 : d * r1, d * c0 : d * c1]
+        out.append(np.linalg.norm(Ab - f.dense()) / np.linalg.norm(Ab))
+    return np.array(out)
+
+
+@pytest.mark.parametrize("tag,n", [("H4k", 2048), ("U8k", 1024), ("T65k", 1024)])
+def test_assemble_vs_oracle(tag, n):
+    pb = Problem(tag, n)
+    H, rep = pb.device_h()
+    oh = pb.oracle_h()
+    info = H.block_info()
+    adm = pb.table[:, 0] == 1
+    dsteps = np.abs(info["steps"][adm] - oh.steps[adm])
+    drank = np.abs(info["rank_after"][adm] - oh.rank_after[adm])
+    assert dsteps.max() <= 1, f"ACA steps differ by {dsteps.max()}"
+    assert drank.max() <= 1, f"recompressed ranks differ by {drank.max()}"
+    # dense leaves bit-for-bit comparable to the oracle entries (1e-13 relative)
+    for b in np.flatnonzero(~adm)[:50]:
+        a = H.block(b)
+        o = oh.payload[b]
+        assert np.abs(a - o).max() <= 1e-13 * np.abs(o).max()
+    A = OH.dense_matrix(pb.kind, pb.params, pb.pts, pb.nrm, float(pb.N))
+    err = _block_errors(pb, H, A)
+    assert err.max() <= 3 * pb.w.eps
+    x = pb.rhs(0)
+    y = hmx.matvec(H, x)
+    yd = OH.from_tree(oh, A @ OH.to_tree(oh, x))
+    assert np.linalg.norm(y - yd) <= 3 * pb.w.eps * np.linalg.norm(yd)
+    # same factors quality as the oracle's matvec
+    yo = OH.matvec(oh, x)
+    assert np.linalg.norm(y - yo) <= 3 * pb.w.eps * np.linalg.norm(yd)
+    st = hmx.storage_report(H)
+    so = OH.storage_report(oh)
+    assert abs(st.max_rank_after - so["max_rank_after"]) <= 1
+    assert st.n_stored <= st.bound
+
+
+@pytest.mark.parametrize("tag,n", [("H4k", 2048), ("U8k", 1024), ("T65k", 1024)])
+def test_gmres_iterations_vs_oracle(tag, n):
+    pb = Problem(tag, n)
+    H, _ = pb.device_h()
+    b = pb.rhs(0)
+    res = hmx.solve_gmres(H, b, hmx.GmresConfig(tol=1e-4, restart=50))
+    assert res.converged
+    xo, it_o, hist_o, conv_o = OS.gmres(lambda v: hmx.matvec(H, v), b, 1e-4, 50, 1000)
+    assert abs(res.iters - it_o) <= 1
+    r = b - hmx.matvec(H, res.x)
+    assert np.linalg.norm(r) <= 1e-4 * np.linalg.norm(b) * 1.0001
+    assert all(h1 <= h0 * (1 + 1e-12) for h0, h1 in zip(res.history, res.history[1:]))
+    z = hmx.solve_gmres(H, np.zeros_like(b))
+    assert z.iters == 0 and not np.any(z.x)
