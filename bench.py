@@ -1,0 +1,376 @@
+"""Headline benchmark: elastodynamic U H-matvec at N_c = 32,768 (BASELINE.json
+config 3, "100 timed H-matvecs with seeded complex Gaussian input vectors").
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl hmx|reference] [--config U32k]
+
+A step is one H-matvec y = A_H x_j over the assembled H-matrix (x_j a fresh
+seeded complex Gaussian vector per step, already in HBM).  ``value`` is the
+algorithmic H-matvec traffic of all ranks divided by the device time of the K
+steps (max over ranks): GB/s.  The packed H streams (10.5 GB at U32k) are far
+larger than the 126 MB L2, so no L2 flush is needed between steps.
+
+Multi-GPU (torchrun): replicas only -- every rank assembles and applies its own
+copy, value = sum over ranks, scaling "weak".
+
+``--impl reference`` times the reference's CPU implementation of the same
+path (the oracle restatement, oracle/hmatrix.py, all host threads) on a
+bounded sample of the same workload and prints the same JSON line shape.
+"""
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+FALLBACK_HBM_GBS = 6650.0
+SEED = 0
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="hmx", choices=["hmx", "reference"])
+    ap.add_argument("--config", default="U32k")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return d, "measured"
+    return {"hbm_gbs": FALLBACK_HBM_GBS}, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device):
+        self.device = device
+        self.proc = None
+        self.path = None
+
+    def __enter__(self):
+        fd, self.path = tempfile.mkstemp(suffix=".csv")
+        os.close(fd)
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=open(self.path, "w"), stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+        time.sleep(0.3)
+        return self
+
+    def __exit__(self, *exc):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+
+    def summary(self):
+        rows = []
+        try:
+            with open(self.path) as f:
+                for line in f:
+                    parts = [p.strip() for p in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        except Exception:
+            pass
+        finally:
+            try:
+                os.unlink(self.path)
+            except Exception:
+                pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unavailable"]}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        smax = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(smax) if smax else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_setup(args):
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+# ----------------------------------------------------------------------------------------------
+def cpu_sample_problem(tag, stripe=8):
+    """Bounded CPU sample: every leaf whose row cluster lies in the first 1/stripe
+    of the tree-ordered rows (a block-row stripe keeps the workload's leaf mix)."""
+    from oracle import geometry as OG
+    from paper_1706_09384_b200.configs import WORKLOADS
+    import paper_1706_09384_b200 as hmx
+    from tests._problems import oracle_params, spec_for  # noqa: F401
+
+    w = WORKLOADS[tag]
+    pts, nrm = OG.sphere_cloud(w.n_points)
+    ct = OG.cluster_tree(pts, w.n_leaf)
+    lv = OG.block_leaves(ct, ct, w.eta)
+    tab = OG.leaf_table(ct, ct, lv)
+    cut = w.n_points // stripe
+    sel = np.flatnonzero(tab[:, 2] <= cut)
+    params = oracle_params(spec_for(w))
+    return w, ct, nrm, tab[sel], params, f"rows [0, {cut}) of {tag} (1/{stripe} block-row stripe, {len(sel)} leaves)"
+
+
+def run_cpu(tag, steps, warmup, budget_s=None):
+    """Oracle H-matvec throughput on the bounded sample; returns dict."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    from oracle import hmatrix as OH
+
+    w, ct, nrm, tab, params, desc = cpu_sample_problem(tag)
+    cores = os.cpu_count() or 1
+    t0 = time.perf_counter()
+    oh = OH.assemble(w.kind, params, ct.points_tree, None if w.kind != "T" else nrm[ct.perm], ct.perm, tab, w.eps,
+                     self_shift=float(w.n_points), workers=cores)
+    t_setup = time.perf_counter() - t0
+    d = w.d
+    bytes_ = 0.0
+    for (k, r0, r1, c0, c1), ra in zip(tab, oh.rank_after):
+        m, n = r1 - r0, c1 - c0
+        bytes_ += 16.0 * (d * d * m * n if k == 0 else ra * d * (m + n))
+    bytes_ += 32.0 * d * w.n_points
+    # balanced contiguous chunks of leaves by bytes
+    cost = np.array([(d * d * (r1 - r0) * (c1 - c0) if k == 0 else ra * d * ((r1 - r0) + (c1 - c0)))
+                     for (k, r0, r1, c0, c1), ra in zip(tab, oh.rank_after)], float)
+    order = np.argsort(-cost)
+    chunks = [[] for _ in range(cores)]
+    load = np.zeros(cores)
+    for b in order:
+        i = int(np.argmin(load))
+        chunks[i].append(int(b))
+        load[i] += cost[b]
+    rng = np.random.default_rng(SEED)
+    n = d * w.n_points
+    xs = [rng.standard_normal(n) + 1j * rng.standard_normal(n) for _ in range(4)]
+    from threadpoolctl import threadpool_limits
+
+    with ThreadPoolExecutor(cores) as pool, threadpool_limits(1):
+        for j in range(warmup):
+            OH.matvec_tree_threads(oh, xs[j % 4], pool, chunks)
+        t0 = time.perf_counter()
+        done = 0
+        for j in range(steps):
+            OH.matvec_tree_threads(oh, xs[j % 4], pool, chunks)
+            done += 1
+            if budget_s is not None and time.perf_counter() - t0 > budget_s:
+                break
+        dt = time.perf_counter() - t0
+    return {"value": bytes_ * done / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
+            "sample": f"{desc}; oracle factors (numpy ACA + QR/SVD recompression); {done} threaded "
+                      f"oracle H-matvecs of {bytes_ / 1e9:.3f} GB each", "ms_per_step": dt / done * 1e3,
+            "steps": done, "setup_s": t_setup}
+
+
+def reference_arm(args):
+    ws, rank, local = dist_setup(args)
+    if rank != 0:
+        return
+    r = run_cpu(args.config, args.steps, args.warmup)
+    line = {
+        "impl": "reference", "metric": f"{args.config} H-matvec algorithmic HBM throughput (elasto U)",
+        "value": r["value"], "unit": "GB/s", "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
+        "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (Fibonacci sphere, seeded complex Gaussian x)",
+        "config": {"workload": f"{args.config} H-matvec", "sample": r["sample"]},
+        "cpu_baseline": {"value": r["value"], "unit": "GB/s", "cores": r["cores"], "kind": "port",
+                         "sample": r["sample"]},
+        "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------------------------
+def hmx_arm(args):
+    import torch
+
+    import paper_1706_09384_b200 as hmx
+    from paper_1706_09384_b200 import _lib
+    from paper_1706_09384_b200.configs import WORKLOADS
+    from tests._problems import spec_for
+
+    ws, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    dist = None
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = WORKLOADS[args.config]
+    t0 = time.perf_counter()
+    cloud = hmx.make_geometry("sphere", w.n_points, 1.0, d=w.d)
+    ct = hmx.build_cluster_tree(cloud, w.n_leaf)
+    bt = hmx.build_block_tree(ct, ct, w.eta)
+    t_tree = time.perf_counter() - t0
+    spec = spec_for(w)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    H, rep = hmx.assemble(spec, cloud, ct, bt, hmx.ACAConfig(eps_aca=w.eps), device=local)
+    t_asm_wall = time.perf_counter() - t0
+    st = H.stats()
+    stream = torch.cuda.current_stream()
+    H.use_stream(stream.cuda_stream)
+    n = w.d * w.n_points
+    K, W = args.steps, args.warmup
+    rng = np.random.default_rng(SEED + rank)
+    X = torch.from_numpy(np.stack([rng.standard_normal(n) + 1j * rng.standard_normal(n) for _ in range(K + W)]))
+    Xd = X.to(f"cuda:{local}")
+    Y = torch.empty(n, dtype=torch.complex128, device=f"cuda:{local}")
+    L = _lib.lib()
+    hp = H.handle
+
+    def mv_dev(j):
+        _lib.check(L.hmx_matvec(hp, C.c_void_p(Xd[j].data_ptr()), C.c_void_p(Y.data_ptr()), 1), "matvec")
+
+    for j in range(W):
+        mv_dev(K + j)
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    peaks, peak_kind = measured_peaks()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        _lib.check(L.hmx_profile_begin(hp), "profile")
+        e0.record()
+        for j in range(K):
+            mv_dev(j)
+        e1.record()
+        torch.cuda.synchronize()
+    ncalls = C.c_int64()
+    ph = np.zeros(4)
+    _lib.check(L.hmx_profile_end(hp, C.byref(ncalls), _lib.ptr(ph)), "profile")
+    ms = e0.elapsed_time(e1)
+    clocks = clk.summary()
+    ms_max = ms
+    if dist:
+        t = torch.tensor([ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max = float(t.item())
+    mv_bytes = st["matvec_bytes"]
+    value = ws * K * mv_bytes / (ms_max * 1e-3) / 1e9
+
+    # ---- e2e through the C-ABI with pinned host buffers (H2D + kernels + D2H per step)
+    Xh = X.pin_memory()
+    Yh = torch.empty(n, dtype=torch.complex128).pin_memory()
+    for j in range(W):
+        _lib.check(L.hmx_matvec(hp, C.c_void_p(Xh[K + j].data_ptr()), C.c_void_p(Yh.data_ptr()), 0), "matvec")
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    f0.record()
+    for j in range(K):
+        _lib.check(L.hmx_matvec(hp, C.c_void_p(Xh[j].data_ptr()), C.c_void_p(Yh.data_ptr()), 0), "matvec")
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = f0.elapsed_time(f1)
+    if dist:
+        t = torch.tensor([e2e_ms], device=f"cuda:{local}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_ms = float(t.item())
+    e2e_value = ws * K * mv_bytes / (e2e_ms * 1e-3) / 1e9
+
+    # ---- roofline of the dominant kernel (phase 2: row-stream GEMV)
+    nc = max(int(ncalls.value), 1)
+    p1_ms, p2_ms = ph[1] / nc, ph[2] / nc
+    p2_gbs = st["phase2_bytes"] / (p2_ms * 1e-3) / 1e9
+    p1_gbs = st["phase1_bytes"] / (p1_ms * 1e-3) / 1e9
+    hbm_peak = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        try:
+            with open(prof) as f:
+                traffic = json.load(f).get(args.config, {}).get("mv_phase2")
+        except Exception:
+            traffic = None
+    # ---- assembly roofline (FP64)
+    dfma = C.c_double()
+    _lib.check(L.hmx_bench_dfma(_lib.context(local), C.byref(dfma)), "dfma")
+    from paper_1706_09384_b200.flops import PAIR_FLOPS
+
+    pair_flops = PAIR_FLOPS[w.kind] * st["pairs_evaluated"]
+    asm_flops = st["flops_assembly"] + pair_flops
+    t_asm = st["t_total_ms"] * 1e-3
+    entries = w.d * w.d * st["pairs_evaluated"]
+    line = {
+        "metric": f"{args.config} H-matvec algorithmic HBM throughput (elasto U)",
+        "value": value, "unit": "GB/s", "n_gpus": ws, "steps": K, "warmup": W,
+        "ms_per_step": ms_max / K, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (Fibonacci sphere, seeded complex Gaussian x, seed 0)",
+        "config": {"workload": f"{args.config} H-matvec", "kernel": "elasto U", "n_points": w.n_points,
+                   "n_leaf": w.n_leaf, "eta": w.eta, "eps_aca": w.eps, "ks": w.ks,
+                   "parallelism": f"replicas x{ws}",
+                   "l2": "inputs larger than L2 (H streams %.1f GB vs 126 MB L2), no flush" % (mv_bytes / 1e9)},
+        "gpu_launches": 4 * K,
+        "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
+                "ms_per_step": e2e_ms / K},
+        "roofline": {"bound": "hbm", "kernel": "mv_phase2", "achieved": p2_gbs, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": p2_gbs / hbm_peak, "traffic": traffic,
+                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
+                     else "fallback 6.65 TB/s (B200_PROFILING.md)",
+                     "bytes_per_launch": st["phase2_bytes"], "ms_per_launch": p2_ms,
+                     "whole_matvec_frac": (mv_bytes / (ms_max / K * 1e-3) / 1e9) / hbm_peak,
+                     "vs_8TBps": (mv_bytes / (ms_max / K * 1e-3) / 1e9) / 8000.0},
+        "matvec_phases": {"gather_ms": ph[0] / nc, "vhx_ms": p1_ms, "vhx_GBps": p1_gbs, "row_gemv_ms": p2_ms,
+                          "row_gemv_GBps": p2_gbs, "finalize_ms": ph[3] / nc, "bytes": mv_bytes},
+        "assembly": {"ms": st["t_total_ms"], "wall_s": t_asm_wall, "tree_build_s": t_tree,
+                     "aca_ms": st["t_aca_ms"], "recompress_ms": st["t_recompress_ms"],
+                     "dense_ms": st["t_dense_ms"], "form_ms": st["t_form_ms"],
+                     "green_entries_per_s": entries / t_asm, "pairs": st["pairs_evaluated"],
+                     "fp64_flops": asm_flops, "fp64_tflops": asm_flops / t_asm / 1e12,
+                     "fp64_peak_tflops": dfma.value, "fp64_frac": asm_flops / t_asm / 1e12 / dfma.value,
+                     "fp64_peak_source": "measured DFMA microkernel (hmx_bench_dfma)",
+                     "max_rank_before": rep.max_rank_before, "max_rank_after": rep.max_rank_after,
+                     "tau": rep.tau, "aca_passes": st["aca_passes"]},
+        "clocks": clocks,
+    }
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        try:
+            r = run_cpu(args.config, steps=50, warmup=1, budget_s=15.0)
+            line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
+            line["cpu_baseline"]["ms_per_step"] = r["ms_per_step"]
+        except Exception as exc:  # the baseline is reported, never fatal
+            line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
+                                    "sample": f"failed: {exc!r}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        reference_arm(a)
+    else:
+        hmx_arm(a)

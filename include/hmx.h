@@ -88,6 +88,7 @@ typedef struct {
   double flops_assembly;           /* algorithmic FP64 flops */
   double matvec_bytes;             /* algorithmic bytes of one matvec */
   double dense_bytes, lowrank_bytes;
+  double phase1_bytes, phase2_bytes; /* algorithmic bytes of the two streaming kernels */
 } hmx_stats;
 
 int hmx_abi_version(void);
@@ -95,7 +96,7 @@ int hmx_last_error(char* buf, int64_t cap);
 
 /* ---- context ------------------------------------------------------------- */
 int hmx_ctx_create(int32_t device, hmx_ctx** out);
-/* launch on an existing cudaStream_t (e.g. torch.cuda.current_stream()); 0 = own stream */
+/* launch on an existing cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream; 0 = legacy default stream) */
 int hmx_ctx_set_stream(hmx_ctx* ctx, uint64_t stream);
 int hmx_ctx_sync(hmx_ctx* ctx);
 int hmx_ctx_destroy(hmx_ctx* ctx);
@@ -141,6 +142,13 @@ void hmx_hmatrix_free(hmx_hmatrix* h);
 int hmx_matvec(hmx_hmatrix* h, const double* x, double* y, int32_t mem);
 /* device pointers; phase_ms[4] = gather, phase 1 (V^H x), phase 2 (row GEMV), finalize */
 int hmx_matvec_profile(hmx_hmatrix* h, const double* x_dev, double* y_dev, float* phase_ms);
+/* live kernel timing: every matvec between begin and end records CUDA events
+ * around its 4 phases on the launch stream (no extra synchronisation);
+ * end returns the number of calls and the summed per-phase milliseconds */
+int hmx_profile_begin(hmx_hmatrix* h);
+int hmx_profile_end(hmx_hmatrix* h, int64_t* n_calls, double* phase_ms_sum);
+/* FP64 DFMA throughput of the device (TFLOP/s), measured by a dependent-chain microkernel */
+int hmx_bench_dfma(hmx_ctx* ctx, double* tflops);
 int hmx_gmres(hmx_hmatrix* h, const double* b, double* x, double tol, int32_t restart, int64_t max_iters,
               int32_t mem, int64_t* iters, double* history, int64_t history_cap, int64_t* history_len,
               int32_t* converged);

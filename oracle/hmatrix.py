@@ -171,3 +171,30 @@ def storage_report(h):
         bound = 2 * h.c_sp * max(rmax_after, nl) * N * (math.log2(N) - math.log2(nl) + 1)
     return dict(n_stored=int(ns), n_dense_equiv=N * N, tau=ns / float(N * N),
                 max_rank_before=rmax_before, max_rank_after=rmax_after, bound=bound)
+
+
+def matvec_tree_threads(h, xt, pool, chunks):
+    """Leaf-parallel oracle matvec ("matvec parallelizes across
+    sibling blocks with per-output-range accumulation"): ``chunks`` is a list
+    of leaf-index lists; each worker thread accumulates its own y, the partial
+    vectors are summed in chunk order (deterministic).  numpy's BLAS calls
+    release the GIL, so the threads overlap the GEMV work."""
+    d = h.d
+
+    def work(idx):
+        yt = np.zeros(h.d * h.n_points, dtype=complex)
+        for b in idx:
+            k, r0, r1, c0, c1 = h.table[b]
+            p = h.payload[b]
+            xs = xt[d * c0 : d * c1]
+            if k == DENSE:
+                yt[d * r0 : d * r1] += p @ xs
+            elif p[0].shape[1]:
+                yt[d * r0 : d * r1] += p[0] @ (p[1].conj().T @ xs)
+        return yt
+
+    parts = list(pool.map(work, chunks))
+    y = parts[0]
+    for p in parts[1:]:
+        y += p
+    return y

@@ -35,7 +35,8 @@ class HmxStats(C.Structure):
         "aca_steps_total", "pairs_evaluated", "n_fallback", "n_unconverged", "n_regularized",
         "aca_passes", "row_elems", "v_elems", "n_levels", "n_tiles", "n_jobs")] + [
         (n, f64) for n in ("t_dense_ms", "t_aca_ms", "t_recompress_ms", "t_form_ms", "t_total_ms",
-                           "flops_assembly", "matvec_bytes", "dense_bytes", "lowrank_bytes")]
+                           "flops_assembly", "matvec_bytes", "dense_bytes", "lowrank_bytes",
+                           "phase1_bytes", "phase2_bytes")]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -67,6 +68,9 @@ SIGNATURES = {
     "hmx_hmatrix_free": (None, [P]),
     "hmx_matvec": (C.c_int, [P, P, P, i32]),
     "hmx_matvec_profile": (C.c_int, [P, P, P, C.POINTER(C.c_float)]),
+    "hmx_profile_begin": (C.c_int, [P]),
+    "hmx_profile_end": (C.c_int, [P, C.POINTER(i64), P]),
+    "hmx_bench_dfma": (C.c_int, [P, C.POINTER(f64)]),
     "hmx_gmres": (C.c_int, [P, P, P, f64, i32, i64, i32, C.POINTER(i64), P, i64,
                             C.POINTER(i64), C.POINTER(i32)]),
 }

@@ -61,6 +61,15 @@ class Workload:
         return {"kp": self.kp, "ks": self.ks, "lam": self.lam, "mu": self.mu,
                 "scale": self.scale}
 
+    def spec(self):
+        """The hmatx KernelSpec of this workload (Material from rho, mu, lambda, omega)."""
+        from .kernels import KernelSpec, Material
+
+        if self.kind == "H":
+            return KernelSpec.helmholtz(self.kappa)
+        mat = Material.from_lame(self.rho, self.mu, self.lam, self.omega)
+        return KernelSpec.elasto_u(mat) if self.kind == "U" else KernelSpec.elasto_t(mat)
+
     def with_points(self, n_points, rescale_ks=True):
         """Same physics at another size (kappa_s rescaled for 10 pts/lambda_s
         when the original was on that rule)."""

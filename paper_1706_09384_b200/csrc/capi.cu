@@ -194,14 +194,11 @@ int hmx_ctx_create(int32_t device, hmx_ctx** out) {
 int hmx_ctx_set_stream(hmx_ctx* ctx, uint64_t stream) {
   if (!ctx) return HMX_EINVAL;
   HMX_CUDA_TRY(cudaSetDevice(ctx->c.device));
+  HMX_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
   if (ctx->c.own_stream && ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
-  if (stream == 0) {
-    HMX_CUDA_TRY(cudaStreamCreateWithFlags(&ctx->c.stream, cudaStreamNonBlocking));
-    ctx->c.own_stream = true;
-  } else {
-    ctx->c.stream = reinterpret_cast<cudaStream_t>(stream);
-    ctx->c.own_stream = false;
-  }
+  // any value is taken as a cudaStream_t; 0 is the legacy default stream
+  ctx->c.stream = reinterpret_cast<cudaStream_t>(stream);
+  ctx->c.own_stream = false;
   return HMX_OK;
 }
 
@@ -762,6 +759,8 @@ int hmx_hmatrix_stats(const hmx_hmatrix* h, hmx_stats* st) {
   st->matvec_bytes = H.mv_bytes;
   st->dense_bytes = H.dense_bytes;
   st->lowrank_bytes = H.lr_bytes;
+  st->phase1_bytes = H.phase1_bytes;
+  st->phase2_bytes = H.phase2_bytes;
   return HMX_OK;
 }
 
@@ -835,6 +834,39 @@ int hmx_matvec_profile(hmx_hmatrix* h, const double* x_dev, double* y_dev, float
   if (!h || !x_dev || !y_dev || !phase_ms) return HMX_EINVAL;
   HMX_CUDA_TRY(cudaSetDevice(h->H.ctx->device));
   return matvec_device(h->H, reinterpret_cast<const double2*>(x_dev), reinterpret_cast<double2*>(y_dev), phase_ms);
+}
+
+int hmx_profile_begin(hmx_hmatrix* h) {
+  if (!h) return HMX_EINVAL;
+  for (cudaEvent_t e : h->H.prof_events) cudaEventDestroy(e);
+  h->H.prof_events.clear();
+  h->H.profiling = true;
+  return HMX_OK;
+}
+
+int hmx_profile_end(hmx_hmatrix* h, int64_t* n_calls, double* phase_ms_sum) {
+  if (!h || !n_calls || !phase_ms_sum) return HMX_EINVAL;
+  DeviceH& H = h->H;
+  H.profiling = false;
+  HMX_CUDA_TRY(cudaStreamSynchronize(H.ctx->stream));
+  const size_t nc = H.prof_events.size() / 5;
+  for (int i = 0; i < 4; ++i) phase_ms_sum[i] = 0.0;
+  for (size_t k = 0; k < nc; ++k)
+    for (int i = 0; i < 4; ++i) {
+      float ms = 0.f;
+      HMX_CUDA_TRY(cudaEventElapsedTime(&ms, H.prof_events[5 * k + i], H.prof_events[5 * k + i + 1]));
+      phase_ms_sum[i] += ms;
+    }
+  for (cudaEvent_t e : H.prof_events) cudaEventDestroy(e);
+  H.prof_events.clear();
+  *n_calls = (int64_t)nc;
+  return HMX_OK;
+}
+
+int hmx_bench_dfma(hmx_ctx* ctx, double* tflops) {
+  if (!ctx || !tflops) return HMX_EINVAL;
+  HMX_CUDA_TRY(cudaSetDevice(ctx->c.device));
+  return hmx::bench_dfma(ctx->c, tflops);
 }
 
 int hmx_gmres(hmx_hmatrix* h, const double* b, double* x, double tol, int32_t restart, int64_t max_iters,

@@ -55,7 +55,43 @@ __global__ void __launch_bounds__(kThreads) eval_block(GreenParams P, PointsSoA 
   if (bad) atomicOr(err, 1);
 }
 
+// 8 independent DFMA chains per thread, 2 flops each
+__global__ void __launch_bounds__(256) dfma_peak(double* out, int iters, double a, double b) {
+  double x[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) x[k] = threadIdx.x * 1e-9 + k;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int k = 0; k < 8; ++k) x[k] = fma(x[k], a, b);
+  }
+  double s = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) s += x[k];
+  if (s == 12345.678) out[0] = s;  // keep the chains alive
+}
+
 }  // namespace
+
+int bench_dfma(Ctx& c, double* tflops) {
+  double* out;
+  HMX_CUDA_TRY(cudaMalloc(&out, sizeof(double)));
+  const int blocks = c.num_sms * 8, iters = 1 << 14;
+  dfma_peak<<<blocks, 256, 0, c.stream>>>(out, 64, 0.999999, 1e-7);  // warm-up
+  cudaEvent_t e0, e1;
+  HMX_CUDA_TRY(cudaEventCreate(&e0));
+  HMX_CUDA_TRY(cudaEventCreate(&e1));
+  HMX_CUDA_TRY(cudaEventRecord(e0, c.stream));
+  dfma_peak<<<blocks, 256, 0, c.stream>>>(out, iters, 0.999999, 1e-7);
+  HMX_CUDA_TRY(cudaEventRecord(e1, c.stream));
+  HMX_CUDA_TRY(cudaEventSynchronize(e1));
+  float ms = 0;
+  HMX_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(out);
+  *tflops = 2.0 * 8.0 * iters * (double)blocks * 256 / (ms * 1e-3) / 1e12;
+  return HMX_OK;
+}
 
 int launch_dense_fill(Ctx& c, const GreenParams& P, const PointsSoA& pts, const int64_t* d_desc, int64_t ndense,
                       double2* row_stream, int32_t* d_err) {

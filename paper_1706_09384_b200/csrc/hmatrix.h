@@ -86,6 +86,10 @@ struct DeviceH {
   int64_t pairs_evaluated = 0;
   int64_t aca_passes = 0, n_fallback = 0, n_unconverged = 0, n_regularized = 0;
   double flops_assembly = 0;
+  // live per-phase timing of matvec calls (hmx_profile_begin / _end)
+  bool profiling = false;
+  std::vector<cudaEvent_t> prof_events;  // 5 per profiled call
+  double phase1_bytes = 0, phase2_bytes = 0;
   // pinned host staging for host-pointer matvec
   double2* h_pin_x = nullptr;
   double2* h_pin_y = nullptr;
@@ -138,6 +142,9 @@ struct FormDesc {
 };
 int launch_form(Ctx& c, const FormDesc* d_desc, int64_t nitems, int64_t ntiles_total, const int64_t* d_tile_start,
                 const double2* A, const double2* W, double2* C);
+
+// dense.cu: FP64 peak microbenchmark
+int bench_dfma(Ctx& c, double* tflops);
 
 // gmres.cu
 int gmres_device(DeviceH& H, const double2* b_dev, double2* x_dev, double tol, int restart, int64_t max_iters,

@@ -217,6 +217,15 @@ int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
   H.dense_bytes = dense_b;
   H.lr_bytes = lr_b;
   H.mv_bytes = dense_b + lr_b + 32.0 * H.n;
+  // per-kernel algorithmic bytes: phase 1 streams V (+ x pieces -> dense slots),
+  // phase 2 streams the row stream (dense leaves + U factors)
+  {
+    double copy_b = 0;
+    for (const MvJob1& j : jobs)
+      if (j.kind == 0) copy_b += 32.0 * j.len;
+    H.phase1_bytes = 16.0 * H.v_elems + copy_b;
+    H.phase2_bytes = 16.0 * H.row_elems;
+  }
   Ctx& c = *H.ctx;
   HMX_CUDA_TRY(cudaMalloc(&H.d_row, sizeof(double2) * std::max<int64_t>(H.row_elems, 1)));
   HMX_CUDA_TRY(cudaMalloc(&H.d_v, sizeof(double2) * std::max<int64_t>(H.v_elems, 1)));
@@ -240,25 +249,28 @@ int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
 int matvec_device(DeviceH& H, const double2* x, double2* y, float* phase_ms) {
   Ctx& c = *H.ctx;
   cudaEvent_t ev[5];
-  if (phase_ms) {
+  const bool timed = phase_ms != nullptr || H.profiling;
+  if (timed) {
     for (int i = 0; i < 5; ++i) HMX_CUDA_TRY(cudaEventCreate(&ev[i]));
     HMX_CUDA_TRY(cudaEventRecord(ev[0], c.stream));
   }
   const int eg = std::max<int64_t>(1, std::min<int64_t>(hmx_cdiv(H.n, kThreads), 4 * c.num_sms));
   mv_gather<<<eg, kThreads, 0, c.stream>>>(x, H.d_perm, H.d, H.np, H.d_xt);
-  if (phase_ms) HMX_CUDA_TRY(cudaEventRecord(ev[1], c.stream));
+  if (timed) HMX_CUDA_TRY(cudaEventRecord(ev[1], c.stream));
   if (H.njob1) {
     const int64_t warps = std::min<int64_t>(H.njob1, (int64_t)c.num_sms * 64);
     mv_phase1<<<(unsigned)hmx_cdiv(warps * 32, kThreads), kThreads, 0, c.stream>>>(H.d_job1, H.njob1, H.d_v, H.d_xt,
                                                                                    H.d_s);
   }
-  if (phase_ms) HMX_CUDA_TRY(cudaEventRecord(ev[2], c.stream));
+  if (timed) HMX_CUDA_TRY(cudaEventRecord(ev[2], c.stream));
   if (H.ntile2) mv_phase2<<<(unsigned)H.ntile2, kThreads, 0, c.stream>>>(H.d_tile2, H.d_row, H.d_s, H.d_ylev);
-  if (phase_ms) HMX_CUDA_TRY(cudaEventRecord(ev[3], c.stream));
+  if (timed) HMX_CUDA_TRY(cudaEventRecord(ev[3], c.stream));
   mv_finalize<<<eg, kThreads, 0, c.stream>>>(H.d_ylev, H.nlevels, H.n, H.d_perm, H.d, y);
   HMX_CUDA_TRY(cudaGetLastError());
-  if (phase_ms) {
-    HMX_CUDA_TRY(cudaEventRecord(ev[4], c.stream));
+  if (timed) HMX_CUDA_TRY(cudaEventRecord(ev[4], c.stream));
+  if (H.profiling && !phase_ms) {
+    H.prof_events.insert(H.prof_events.end(), ev, ev + 5);
+  } else if (phase_ms) {
     HMX_CUDA_TRY(cudaEventSynchronize(ev[4]));
     for (int i = 0; i < 4; ++i) HMX_CUDA_TRY(cudaEventElapsedTime(&phase_ms[i], ev[i], ev[i + 1]));
     for (int i = 0; i < 5; ++i) cudaEventDestroy(ev[i]);

@@ -8,10 +8,7 @@ from paper_1706_09384_b200.configs import WORKLOADS
 
 
 def spec_for(w):
-    if w.kind == "H":
-        return hmx.KernelSpec.helmholtz(w.kappa)
-    mat = hmx.Material.from_lame(w.rho, w.mu, w.lam, w.omega)
-    return hmx.KernelSpec.elasto_u(mat) if w.kind == "U" else hmx.KernelSpec.elasto_t(mat)
+    return w.spec()
 
 
 def oracle_params(spec):
