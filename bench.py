@@ -214,6 +214,7 @@ def hmx_arm(args):
     import paper_1706_09384_b200 as hmx
     from paper_1706_09384_b200 import _lib
     from paper_1706_09384_b200.configs import WORKLOADS
+    from paper_1706_09384_b200.dist import replica_throughput
     from tests._problems import spec_for
 
     ws, rank, local = dist_setup(args)
@@ -269,13 +270,8 @@ def hmx_arm(args):
     _lib.check(L.hmx_profile_end(hp, C.byref(ncalls), _lib.ptr(ph)), "profile")
     ms = e0.elapsed_time(e1)
     clocks = clk.summary()
-    ms_max = ms
-    if dist:
-        t = torch.tensor([ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max = float(t.item())
     mv_bytes = st["matvec_bytes"]
-    value = ws * K * mv_bytes / (ms_max * 1e-3) / 1e9
+    value, ms_max = replica_throughput(ms, mv_bytes, K, f"cuda:{local}")
 
     # ---- e2e through the C-ABI with pinned host buffers (H2D + kernels + D2H per step)
     Xh = X.pin_memory()
@@ -291,12 +287,7 @@ def hmx_arm(args):
         _lib.check(L.hmx_matvec(hp, C.c_void_p(Xh[j].data_ptr()), C.c_void_p(Yh.data_ptr()), 0), "matvec")
     f1.record()
     torch.cuda.synchronize()
-    e2e_ms = f0.elapsed_time(f1)
-    if dist:
-        t = torch.tensor([e2e_ms], device=f"cuda:{local}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_ms = float(t.item())
-    e2e_value = ws * K * mv_bytes / (e2e_ms * 1e-3) / 1e9
+    e2e_value, e2e_ms = replica_throughput(f0.elapsed_time(f1), mv_bytes, K, f"cuda:{local}")
 
     # ---- roofline of the dominant kernel (phase 2: row-stream GEMV)
     nc = max(int(ncalls.value), 1)

@@ -9,6 +9,6 @@ columns, recompression, forming U' V') is counted exactly by libhmx
 (hmx_stats.flops_assembly) from the actual ranks and step counts.
 """
 
-# kind -> flops per pair (initial hand estimates; replaced by the ncu
-# calibration recorded in profiles/README.md)
-PAIR_FLOPS = {"H": 60.0, "U": 200.0, "T": 330.0}
+# kind -> flops per pair, ncu round 1 (profiles/r01_pairflops.csv, 512 x 512
+# pairs per launch): H 29 DFMA + 3 DADD + 10 DMUL; U 64 + 10 + 54; T 123 + 16 + 97
+PAIR_FLOPS = {"H": 71.0, "U": 192.0, "T": 359.0}

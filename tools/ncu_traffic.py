@@ -28,7 +28,7 @@ for r in rows[2:]:
         u = units[idx[k]]
         x = float(v)
         scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-9, "usecond": 1e-6,
-                 "msecond": 1e-3, "second": 1}.get(u, 1)
+                 "msecond": 1e-3, "second": 1, "ns": 1e-9, "us": 1e-6, "ms": 1e-3}.get(u, 1)
         return x * scale
     ent = res.setdefault(name, [])
     ent.append({"dram_bytes": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
