@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -49,7 +50,7 @@ namespace {
 
 using namespace hmx;
 
-constexpr int kMaxAcaCols = 640;  // Jacobi pair table limit (recompress.cu)
+constexpr int kMaxAcaCols = 1020;  // per-leaf ACA column limit (recompress.cu vector sizes)
 
 GreenParams make_params(const hmx_kernel* k, int has_shift, double shift) {
   GreenParams P;
@@ -375,6 +376,14 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   cudaEvent_t ev[6];
   for (auto& e : ev) HMX_CUDA_TRY(cudaEventCreate(&e));
   HMX_CUDA_TRY(cudaEventRecord(ev[0], c.stream));
+  const bool verbose = std::getenv("HMX_VERBOSE") != nullptr;
+  auto tick = [&](const char* what) {
+    if (!verbose) return;
+    cudaStreamSynchronize(c.stream);
+    std::fprintf(stderr, "[hmx] %-28s %9.2f ms\n", what,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+  };
+  tick("upload");
 
   // ---- 1. ACA passes --------------------------------------------------------------------
   std::vector<int64_t> adm;
@@ -446,6 +455,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       go += 2 * (int64_t)D.kcap * D.kcap;
       ps.kcap_max = std::max<int>(ps.kcap_max, D.kcap);
     }
+    tick("aca: descriptors");
     if ((rc = ps.mem.alloc(&ps.U, uo))) return fail(rc);
     if ((rc = ps.mem.alloc(&ps.V, vo))) return fail(rc);
     if ((rc = ps.mem.alloc(&ps.G, go))) return fail(rc);
@@ -462,6 +472,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
                                  c.stream));
     HMX_CUDA_TRY(
         cudaMemcpyAsync(d_order, order.data(), sizeof(int32_t) * todo.size(), cudaMemcpyHostToDevice, c.stream));
+    tick("aca: workspace alloc");
     if ((rc = launch_aca(c, d, P, pts.soa, d_desc, d_order, (int64_t)todo.size(), ps.kcap_max, (int)m_max_all,
                          cfg->eps, cfg->sigma3_floor > 0 ? cfg->sigma3_floor : 1e-12, ps.U, ps.V, ps.G, d_out)))
       return fail(rc);
@@ -501,6 +512,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     todo.swap(next);
   }
   HMX_CUDA_TRY(cudaEventRecord(ev[1], c.stream));
+  tick("aca done");
 
   // ---- 2. recompression core --------------------------------------------------------------
   std::vector<int64_t> regularized(nb, 0);
@@ -523,7 +535,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       rd[q].K = K;
       rd[q].kcap = ps.desc[i].kcap;
       ps.woff[i] = wo;
-      wo += 5 * (int64_t)K * K;
+      wo += 6 * (int64_t)K * K;
     }
     if (live.empty()) continue;
     if ((rc = ps.mem.alloc(&ps.W, wo))) return fail(rc);
@@ -534,12 +546,14 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     if ((rc = tmp.alloc(&d_rank, (int64_t)rd.size()))) return fail(rc);
     if ((rc = tmp.alloc(&d_flag, (int64_t)rd.size()))) return fail(rc);
     HMX_CUDA_TRY(cudaMemcpyAsync(d_rd, rd.data(), sizeof(RecDesc) * rd.size(), cudaMemcpyHostToDevice, c.stream));
-    const int classes[] = {kMaxAcaCols, 112, 64, 32};
+    // shared-memory size classes (smem ~ 16 K^2 bytes): more CTAs per SM for small K
+    const int classes[] = {kMaxAcaCols, kRecompressSmemMax, 88, 64, 48, 32};
+    const int ncls = 6;
     size_t q0 = 0;
-    for (int ci = 0; ci < 4 && q0 < rd.size(); ++ci) {
-      const int lim_lo = ci + 1 < 4 ? classes[ci + 1] : 0;
+    for (int ci = 0; ci < ncls && q0 < rd.size(); ++ci) {
+      const int lim_lo = ci + 1 < ncls ? classes[ci + 1] : 0;
       size_t q1 = q0;
-      while (q1 < rd.size() && (rd[q1].K > lim_lo || ci == 3)) ++q1;
+      while (q1 < rd.size() && (rd[q1].K > lim_lo || ci == ncls - 1)) ++q1;
       if (q1 > q0) {
         if ((rc = launch_recompress_core(c, d_rd + q0, (int64_t)(q1 - q0), rd[q0].K, cfg->eps, cfg->trunc_rule, ps.G,
                                          ps.W, d_rank + q0, d_flag + q0)))
@@ -561,12 +575,15 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     }
   }
   HMX_CUDA_TRY(cudaEventRecord(ev[2], c.stream));
+  tick("recompress done");
 
   // ---- 3. layout + matvec plan ----------------------------------------------------------------
+  if (verbose) setenv("HMX_VERBOSE_PLAN", "1", 1);
   if ((rc = build_matvec_plan(H, {}))) return fail(rc);
 
   // ---- 4a. dense leaves ---------------------------------------------------------------------
   HMX_CUDA_TRY(cudaEventRecord(ev[3], c.stream));
+  tick("layout + plan");
   int32_t* d_err;
   DevBuf tmp4;
   if ((rc = tmp4.alloc(&d_err, 1))) return fail(rc);
@@ -583,6 +600,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     if ((rc = launch_dense_fill(c, P, pts.soa, d_dd, (int64_t)dd.size() / 6, H.d_row, d_err))) return fail(rc);
   }
   HMX_CUDA_TRY(cudaEventRecord(ev[4], c.stream));
+  tick("dense leaves");
 
   // ---- 4b. U' = U W_U, V' = V W_V -------------------------------------------------------------
   for (AcaPass& ps : passes) {
@@ -600,7 +618,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
         FormDesc f;
         const int64_t rows = side == 0 ? d * rows_of(b) : d * cols_of(b);
         f.aoff = side == 0 ? ps.desc[i].uoff : ps.desc[i].voff;
-        f.woff = ps.woff[i] + 3 * (int64_t)K * K + (side == 0 ? 0 : (int64_t)K * r);
+        f.woff = ps.woff[i] + 4 * (int64_t)K * K + (side == 0 ? 0 : (int64_t)K * r);
         f.coff = side == 0 ? H.leaf_moff[b] : H.leaf_voff[b];
         f.rows = (int32_t)rows;
         f.K = K;
@@ -620,13 +638,16 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       if ((rc = t5.alloc(&d_ts, (int64_t)ts.size()))) return fail(rc);
       HMX_CUDA_TRY(cudaMemcpyAsync(d_fd, fd.data(), sizeof(FormDesc) * fd.size(), cudaMemcpyHostToDevice, c.stream));
       HMX_CUDA_TRY(cudaMemcpyAsync(d_ts, ts.data(), sizeof(int64_t) * ts.size(), cudaMemcpyHostToDevice, c.stream));
+      tick(side == 0 ? "form: U descriptors" : "form: V descriptors");
       if ((rc = launch_form(c, d_fd, (int64_t)fd.size(), ntiles, d_ts, side == 0 ? ps.U : ps.V, ps.W,
                             side == 0 ? H.d_row : H.d_v)))
         return fail(rc);
       HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+      tick(side == 0 ? "form: U kernel" : "form: V kernel");
     }
   }
   HMX_CUDA_TRY(cudaEventRecord(ev[5], c.stream));
+  tick("form U' V'");
   int32_t herr = 0;
   HMX_CUDA_TRY(cudaMemcpyAsync(&herr, d_err, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
   HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
@@ -658,6 +679,8 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     }
   }
   H.flops_assembly = fl;
+  passes.clear();
+  tick("free workspaces");
   H.t_total_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   *out = holder;
   return HMX_OK;

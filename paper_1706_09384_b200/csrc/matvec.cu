@@ -14,6 +14,9 @@
 // The pass is HBM-bound (complex128 GEMV = 0.5 flop/B); bytes per call are
 // H.mv_bytes = 16 (sum dense d^2 m n + sum r d (m + n)) + 32 d N.
 #include <algorithm>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <map>
 #include <numeric>
 
@@ -33,8 +36,9 @@ __global__ void mv_gather(const double2* __restrict__ x, const int64_t* __restri
   }
 }
 
-__global__ void mv_phase1(const MvJob1* __restrict__ jobs, int64_t njobs, const double2* __restrict__ V,
-                          const double2* __restrict__ xt, double2* __restrict__ s) {
+__global__ void __launch_bounds__(kThreads) mv_phase1(const MvJob1* __restrict__ jobs, int64_t njobs,
+                                                         const double2* __restrict__ V,
+                                                         const double2* __restrict__ xt, double2* __restrict__ s) {
   const int lane = threadIdx.x & 31;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -48,13 +52,16 @@ __global__ void mv_phase1(const MvJob1* __restrict__ jobs, int64_t njobs, const 
     const double2* vp = V + J.voff;
     double2 a0 = cmk(0, 0), a1 = cmk(0, 0);
     int q = lane;
-    for (; q + 32 < J.len; q += 64) {
-      const double2 v0 = vp[q], v1 = vp[q + 32];
-      const double2 x0 = xp[q], x1 = xp[q + 32];
-      a0 = cfma_ca(v0, x0, a0);
-      a1 = cfma_ca(v1, x1, a1);
+    // 4 independent 16-byte loads of V in flight per lane
+    for (; q + 96 < J.len; q += 128) {
+      const double2 v0 = __ldcs(vp + q), v1 = __ldcs(vp + q + 32), v2 = __ldcs(vp + q + 64),
+                    v3 = __ldcs(vp + q + 96);
+      a0 = cfma_ca(v0, xp[q], a0);
+      a1 = cfma_ca(v1, xp[q + 32], a1);
+      a0 = cfma_ca(v2, xp[q + 64], a0);
+      a1 = cfma_ca(v3, xp[q + 96], a1);
     }
-    if (q < J.len) a0 = cfma_ca(vp[q], xp[q], a0);
+    for (; q < J.len; q += 32) a0 = cfma_ca(__ldcs(vp + q), xp[q], a0);
     double2 acc = warp_sum(cadd(a0, a1));
     if (lane == 0) s[J.soff] = acc;
   }
@@ -79,17 +86,17 @@ __global__ void __launch_bounds__(kThreads) mv_phase2(const MvTile2* __restrict_
     int c = part;
     const int step = parts;
     for (; c + 3 * step < T.ncols; c += 4 * step) {
-      const double2 m0 = mp[(int64_t)c * ld];
-      const double2 m1 = mp[(int64_t)(c + step) * ld];
-      const double2 m2 = mp[(int64_t)(c + 2 * step) * ld];
-      const double2 m3 = mp[(int64_t)(c + 3 * step) * ld];
+      const double2 m0 = __ldcs(mp + (int64_t)c * ld);
+      const double2 m1 = __ldcs(mp + (int64_t)(c + step) * ld);
+      const double2 m2 = __ldcs(mp + (int64_t)(c + 2 * step) * ld);
+      const double2 m3 = __ldcs(mp + (int64_t)(c + 3 * step) * ld);
       const double2 s0 = sp[c], s1 = sp[c + step], s2 = sp[c + 2 * step], s3 = sp[c + 3 * step];
       a0 = cfma(m0, s0, a0);
       a1 = cfma(m1, s1, a1);
       a0 = cfma(m2, s2, a0);
       a1 = cfma(m3, s3, a1);
     }
-    for (; c < T.ncols; c += step) a0 = cfma(mp[(int64_t)c * ld], sp[c], a0);
+    for (; c < T.ncols; c += step) a0 = cfma(__ldcs(mp + (int64_t)c * ld), sp[c], a0);
   }
   const double2 acc = cadd(a0, a1);
   if (parts == 1) {
@@ -120,6 +127,13 @@ __global__ void mv_finalize(const double2* __restrict__ ylev, int64_t nlev, int6
 // Builds segments, levels, stream offsets and the phase-1/phase-2 work lists.
 // Requires H.table, H.rank_after (low-rank leaves), H.d, H.np.
 int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
+  const auto t0 = std::chrono::steady_clock::now();
+  const bool verbose = std::getenv("HMX_VERBOSE_PLAN") != nullptr;
+  auto tick = [&](const char* what) {
+    if (verbose)
+      std::fprintf(stderr, "[hmx]   plan %-22s %9.2f ms\n", what,
+                   std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+  };
   const int d = H.d;
   const int64_t nb = H.nb;
   // ---- row segments keyed by (r0, r1)
@@ -191,8 +205,17 @@ int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
     }
   }
   H.v_elems = vo;
-  // longest jobs first
-  std::stable_sort(jobs.begin(), jobs.end(), [](const MvJob1& a, const MvJob1& b) { return a.len > b.len; });
+  // longest jobs first (stable counting sort on the job length)
+  {
+    int32_t maxlen = 0;
+    for (const MvJob1& j : jobs) maxlen = std::max(maxlen, j.len);
+    std::vector<int64_t> cnt((size_t)maxlen + 2, 0);
+    for (const MvJob1& j : jobs) cnt[(size_t)(maxlen - j.len) + 1]++;
+    for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
+    std::vector<MvJob1> sorted(jobs.size());
+    for (const MvJob1& j : jobs) sorted[(size_t)cnt[(size_t)(maxlen - j.len)]++] = j;
+    jobs.swap(sorted);
+  }
   std::vector<MvTile2> tiles;
   for (int64_t g = 0; g < ns; ++g) {
     if (ncols[g] == 0) continue;
@@ -226,9 +249,11 @@ int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
     H.phase1_bytes = 16.0 * H.v_elems + copy_b;
     H.phase2_bytes = 16.0 * H.row_elems;
   }
+  tick("host layout");
   Ctx& c = *H.ctx;
   HMX_CUDA_TRY(cudaMalloc(&H.d_row, sizeof(double2) * std::max<int64_t>(H.row_elems, 1)));
   HMX_CUDA_TRY(cudaMalloc(&H.d_v, sizeof(double2) * std::max<int64_t>(H.v_elems, 1)));
+  tick("malloc row + V");
   HMX_CUDA_TRY(cudaMalloc(&H.d_s, sizeof(double2) * std::max<int64_t>(H.s_elems, 1)));
   HMX_CUDA_TRY(cudaMalloc(&H.d_xt, sizeof(double2) * H.n));
   HMX_CUDA_TRY(cudaMalloc(&H.d_ylev, sizeof(double2) * H.n * H.nlevels));
@@ -243,6 +268,7 @@ int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
     HMX_CUDA_TRY(
         cudaMemcpyAsync(H.d_tile2, tiles.data(), sizeof(MvTile2) * H.ntile2, cudaMemcpyHostToDevice, c.stream));
   HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  tick("rest");
   return HMX_OK;
 }
 
@@ -258,7 +284,7 @@ int matvec_device(DeviceH& H, const double2* x, double2* y, float* phase_ms) {
   mv_gather<<<eg, kThreads, 0, c.stream>>>(x, H.d_perm, H.d, H.np, H.d_xt);
   if (timed) HMX_CUDA_TRY(cudaEventRecord(ev[1], c.stream));
   if (H.njob1) {
-    const int64_t warps = std::min<int64_t>(H.njob1, (int64_t)c.num_sms * 64);
+    const int64_t warps = std::min<int64_t>(H.njob1, (int64_t)c.num_sms * 64);  // 8 CTAs x 8 warps per SM
     mv_phase1<<<(unsigned)hmx_cdiv(warps * 32, kThreads), kThreads, 0, c.stream>>>(H.d_job1, H.njob1, H.d_v, H.d_xt,
                                                                                    H.d_s);
   }
