@@ -24,6 +24,7 @@
 // column-major with ld = d m / d n, the U(i_piv,:) and V(j_piv,:) rows are
 // staged in shared memory.
 #include <cstdio>
+#include <cstdlib>
 
 #include "green.cuh"
 #include "hmatrix.h"
@@ -130,21 +131,22 @@ HMX_D void inverse(const double2* P, double2* G) {
   for (int t = 0; t < 9; ++t) G[t] = cmul(adj[t], idet);
 }
 
+constexpr int kMaxWarps = 32;
 struct Shared {
   int ipiv, jpiv, inext, K, steps, state, zero_rows, verdict;
   double normB2, s1max;
   double2 gamma[9];
-  double red_v[kWarps];
-  int red_i[kWarps];
-  double red_s[kWarps];
-  double red_a[kWarps], red_b[kWarps], red_c[kWarps];
+  double red_v[kMaxWarps];
+  int red_i[kMaxWarps];
+  double red_s[kMaxWarps];
+  double red_a[kMaxWarps];
 };
 
 // state codes
 constexpr int kRun = 0, kZeroRow = 1, kDone = 2;
 
-template <int D>
-__global__ void __launch_bounds__(kThreads) aca_kernel(GreenParams P, PointsSoA pts, const AcaDesc* __restrict__ desc,
+template <int D, int KIND, int NT, int MINB>
+__global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA pts, const AcaDesc* __restrict__ desc,
                                                        const int32_t* __restrict__ order, double eps, double floor,
                                                        double2* __restrict__ U, double2* __restrict__ V,
                                                        double2* __restrict__ G, AcaOut* __restrict__ out, int kcap_max) {
@@ -163,7 +165,7 @@ __global__ void __launch_bounds__(kThreads) aca_kernel(GreenParams P, PointsSoA 
   double2* Vrow = dyn + D * kcap_max;       // D x kcap_max
   unsigned char* visited = reinterpret_cast<unsigned char*>(dyn + 2 * D * kcap_max);
 
-  for (int i = tid; i < m; i += kThreads) visited[i] = 0;
+  for (int i = tid; i < m; i += NT) visited[i] = 0;
   if (tid == 0) {
     sh.ipiv = 0;
     sh.K = 0;
@@ -184,7 +186,7 @@ __global__ void __launch_bounds__(kThreads) aca_kernel(GreenParams P, PointsSoA 
       break;
     }
     if (tid == 0) visited[ipiv] = 1;
-    for (int t = tid; t < D * K; t += kThreads) {
+    for (int t = tid; t < D * K; t += NT) {
       const int a = t / K, l = t - a * K;
       Urow[a * kcap_max + l] = Ub[(int64_t)(D * ipiv + a) + (int64_t)l * ldu];
     }
@@ -193,14 +195,12 @@ __global__ void __launch_bounds__(kThreads) aca_kernel(GreenParams P, PointsSoA 
     // ---- row pass ------------------------------------------------------------
     ArgMax best{-1.0, 0x7fffffff};
     double rs1 = 0.0;
-    for (int j = tid; j < n; j += kThreads) {
-      double2 g[D * D];
-      green_xy(P, pts, ds.r0 + ipiv, pts, ds.c0 + j, g);
+    for (int j = tid; j < n; j += NT) {
       double2 acc[D * D];
 #pragma unroll
       for (int t = 0; t < D * D; ++t) acc[t] = cmk(0.0, 0.0);
       const double2* vp = Vb + (int64_t)D * j;
-#pragma unroll 2
+#pragma unroll 1
       for (int l = 0; l < K; ++l) {
         double2 vv[D];
 #pragma unroll
@@ -212,9 +212,11 @@ __global__ void __launch_bounds__(kThreads) aca_kernel(GreenParams P, PointsSoA 
           for (int c = 0; c < D; ++c) acc[a * D + c] = cfma_cj(ua, vv[c], acc[a * D + c]);
         }
       }
+      // Green's block after the accumulation: fewer values live at once
       double2 R[D * D];
+      green_xy_k<KIND>(P, pts, ds.r0 + ipiv, pts, ds.c0 + j, R);
 #pragma unroll
-      for (int t = 0; t < D * D; ++t) R[t] = csub(g[t], acc[t]);
+      for (int t = 0; t < D * D; ++t) R[t] = csub(R[t], acc[t]);
       // v_k = R_row^H : V(D j + c, K + a) = conj(R[a][c])
 #pragma unroll
       for (int a = 0; a < D; ++a)
@@ -236,7 +238,7 @@ __global__ void __launch_bounds__(kThreads) aca_kernel(GreenParams P, PointsSoA 
     if (tid == 0) {
       ArgMax bb{sh.red_v[0], sh.red_i[0]};
       double r1 = sh.red_s[0];
-      for (int w = 1; w < kWarps; ++w) {
+      for (int w = 1; w < (NT / 32); ++w) {
         bb = argmax_pick(bb, ArgMax{sh.red_v[w], sh.red_i[w]});
         r1 = fmax(r1, sh.red_s[w]);
       }
@@ -276,7 +278,7 @@ __global__ void __launch_bounds__(kThreads) aca_kernel(GreenParams P, PointsSoA 
       break;
     }
     const int jpiv = sh.jpiv;
-    for (int t = tid; t < D * K; t += kThreads) {
+    for (int t = tid; t < D * K; t += NT) {
       const int c = t / K, l = t - c * K;
       Vrow[c * kcap_max + l] = Vb[(int64_t)(D * jpiv + c) + (int64_t)l * ldv];
     }
@@ -287,14 +289,12 @@ __global__ void __launch_bounds__(kThreads) aca_kernel(GreenParams P, PointsSoA 
 
     // ---- column pass ---------------------------------------------------------
     best = ArgMax{-1.0, 0x7fffffff};
-    for (int i = tid; i < m; i += kThreads) {
-      double2 g[D * D];
-      green_xy(P, pts, ds.r0 + i, pts, ds.c0 + jpiv, g);
+    for (int i = tid; i < m; i += NT) {
       double2 acc[D * D];
 #pragma unroll
       for (int t = 0; t < D * D; ++t) acc[t] = cmk(0.0, 0.0);
       const double2* up = Ub + (int64_t)D * i;
-#pragma unroll 2
+#pragma unroll 1
       for (int l = 0; l < K; ++l) {
         double2 uu[D];
 #pragma unroll
@@ -307,8 +307,9 @@ __global__ void __launch_bounds__(kThreads) aca_kernel(GreenParams P, PointsSoA 
         }
       }
       double2 C[D * D];
+      green_xy_k<KIND>(P, pts, ds.r0 + i, pts, ds.c0 + jpiv, C);
 #pragma unroll
-      for (int t = 0; t < D * D; ++t) C[t] = csub(g[t], acc[t]);
+      for (int t = 0; t < D * D; ++t) C[t] = csub(C[t], acc[t]);
       if (!visited[i]) {
         double s1, s3;
         svals<D>(C, s1, s3);
@@ -339,7 +340,7 @@ __global__ void __launch_bounds__(kThreads) aca_kernel(GreenParams P, PointsSoA 
       const double2* F = side == 0 ? Ub : Vb;
       const int64_t ld = side == 0 ? ldu : ldv;
       double2* Gm = side == 0 ? GU : GV;
-      for (int grp = warp; grp < ngroups; grp += kWarps) {
+      for (int grp = warp; grp < ngroups; grp += (NT / 32)) {
         double2 acc[kGramGroup][D];
 #pragma unroll
         for (int t = 0; t < kGramGroup; ++t)
@@ -386,7 +387,7 @@ __global__ void __launch_bounds__(kThreads) aca_kernel(GreenParams P, PointsSoA 
 
     // ---- ||B_k||_F update: cross = Re sum_{l<K,c} G_U(l,K+c) conj(G_V(l,K+c)) ----------
     double cross = 0.0;
-    for (int t = tid; t < K * D; t += kThreads) {
+    for (int t = tid; t < K * D; t += NT) {
       const int l = t / D, c = t - l * D;
       const double2 gu = GU[l + (int64_t)(K + c) * kcap];
       const double2 gv = GV[l + (int64_t)(K + c) * kcap];
@@ -397,7 +398,7 @@ __global__ void __launch_bounds__(kThreads) aca_kernel(GreenParams P, PointsSoA 
     __syncthreads();
     if (tid == 0) {
       double cr = 0.0;
-      for (int w = 0; w < kWarps; ++w) cr += sh.red_a[w];
+      for (int w = 0; w < (NT / 32); ++w) cr += sh.red_a[w];
       double diag = 0.0, nu = 0.0, nv = 0.0;
       for (int c = 0; c < D; ++c) {
         nu += GU[(K + c) + (int64_t)(K + c) * kcap].x;
@@ -412,7 +413,7 @@ __global__ void __launch_bounds__(kThreads) aca_kernel(GreenParams P, PointsSoA 
       sh.K = Kn;
       sh.steps += 1;
       ArgMax bb{sh.red_v[0], sh.red_i[0]};
-      for (int w = 1; w < kWarps; ++w) bb = argmax_pick(bb, ArgMax{sh.red_v[w], sh.red_i[w]});
+      for (int w = 1; w < (NT / 32); ++w) bb = argmax_pick(bb, ArgMax{sh.red_v[w], sh.red_i[w]});
       const int dmin = D * (m < n ? m : n);
       if (sqrt(nu) * sqrt(nv) <= eps * sqrt(fmax(sh.normB2, 0.0))) {
         sh.state = kDone;
@@ -451,15 +452,25 @@ int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const 
                double2* G, AcaOut* d_out) {
   if (nblk == 0) return HMX_OK;
   size_t smem = sizeof(double2) * 2 * (size_t)d * kcap_max + (size_t)((m_max + 15) / 16) * 16;
-  if (d == 1) {
-    HMX_CUDA_TRY(cudaFuncSetAttribute(aca_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    aca_kernel<1><<<(unsigned)nblk, kThreads, smem, c.stream>>>(P, pts, d_desc, d_order, eps, sigma3_floor, U, V, G,
-                                                                d_out, kcap_max);
-  } else {
-    HMX_CUDA_TRY(cudaFuncSetAttribute(aca_kernel<3>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    aca_kernel<3><<<(unsigned)nblk, kThreads, smem, c.stream>>>(P, pts, d_desc, d_order, eps, sigma3_floor, U, V, G,
-                                                                d_out, kcap_max);
-  }
+  auto go = [&](auto kern, int nt) -> int {
+    HMX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)nblk, nt, smem, c.stream>>>(P, pts, d_desc, d_order, eps, sigma3_floor, U, V, G, d_out,
+                                                 kcap_max);
+    return HMX_OK;
+  };
+  // one resident CTA per SM keeps each leaf's factors hot in L1 (the ACA passes
+  // re-read them every step: 2-3 CTAs/SM measured 1.4-1.8x slower); 512 threads
+  // (128 registers) give that CTA 16 warps of memory parallelism.
+  const char* nts = std::getenv("HMX_ACA_NT");
+  const bool wide = !(nts && std::atoi(nts) == 256);
+  int rc;
+  if (P.kind == 0)
+    rc = wide ? go(aca_kernel<1, 0, 512, 1>, 512) : go(aca_kernel<1, 0, 256, 1>, 256);
+  else if (P.kind == 1)
+    rc = wide ? go(aca_kernel<3, 1, 512, 1>, 512) : go(aca_kernel<3, 1, 256, 1>, 256);
+  else
+    rc = wide ? go(aca_kernel<3, 2, 512, 1>, 512) : go(aca_kernel<3, 2, 256, 1>, 256);
+  if (rc) return rc;
   HMX_CUDA_TRY(cudaGetLastError());
   return HMX_OK;
 }

@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <cmath>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -404,24 +405,35 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     return 16.0 * ((double)d * (rows_of(b) + cols_of(b)) * kc + 2.0 * kc * kc);
   };
   {
-    // largest uniform cap K0 whose workspace fits the budget
-    int64_t lo = d, hi = round_d(kMaxAcaCols);
-    auto need = [&](int64_t K0) {
-      double s = 0;
-      for (int64_t b : adm) s += ws_bytes(b, std::min<int64_t>(maxr[b], K0));
-      return s;
+    // Column capacity per leaf from a geometric rank model: ACA ranks of these
+    // kernels grow with kappa * diam (oscillatory regime) on top of a
+    // frequency-independent floor (measured envelope over the five configs:
+    // K <= a + 2 d kappa diam with a <= 70, docs in DESIGN.md 3).  Leaves that
+    // outgrow it are re-run with twice the capacity (same result, deterministic).
+    const double kap = k->kind == 0 ? std::fabs(k->kappa) : std::max(std::fabs(k->ks), std::fabs(k->kp));
+    auto diam = [&](int64_t a0, int64_t a1) {
+      double lo3[3] = {INFINITY, INFINITY, INFINITY}, hi3[3] = {-INFINITY, -INFINITY, -INFINITY};
+      for (int64_t t = a0; t < a1; ++t)
+        for (int q = 0; q < 3; ++q) {
+          lo3[q] = std::min(lo3[q], pts_tree[3 * t + q]);
+          hi3[q] = std::max(hi3[q], pts_tree[3 * t + q]);
+        }
+      return std::sqrt((hi3[0] - lo3[0]) * (hi3[0] - lo3[0]) + (hi3[1] - lo3[1]) * (hi3[1] - lo3[1]) +
+                       (hi3[2] - lo3[2]) * (hi3[2] - lo3[2]));
     };
-    if (need(lo) > budget) {
-      hmx_set_error("ACA workspace for rank %d exceeds the %.1f GB budget", d, budget / 1e9);
-      return fail(HMX_ENOMEM);
+    const double floor_cols = d == 1 ? 36.0 : 72.0;
+    for (int64_t b : adm) {
+      const double dm = std::max(diam(table[5 * b + 1], table[5 * b + 2]), diam(table[5 * b + 3], table[5 * b + 4]));
+      const int64_t est = round_d((int64_t)std::ceil(floor_cols + 2.0 * d * kap * dm) + d - 1);
+      kcap[b] = std::min<int64_t>(maxr[b], std::min<int64_t>(est, round_d(kMaxAcaCols)));
     }
-    while (lo < hi) {
-      const int64_t mid = round_d((lo + hi + d) / 2);
-      if (mid <= lo) break;
-      if (need(mid) <= budget) lo = mid;
-      else hi = mid - d;
+    // fit the budget: scale the model down uniformly if needed
+    double need = 0;
+    for (int64_t b : adm) need += ws_bytes(b, kcap[b]);
+    if (need > budget) {
+      const double f = budget / need;
+      for (int64_t b : adm) kcap[b] = std::max<int64_t>(d, round_d((int64_t)(kcap[b] * f)));
     }
-    for (int64_t b : adm) kcap[b] = std::min<int64_t>(maxr[b], lo);
   }
   std::vector<AcaPass> passes;
   passes.reserve(8);

@@ -56,11 +56,14 @@ HMX_D void radial_series(double k, double r, double ir, double2* g) {
 
 // d = 1: out[0]; d = 3: out[3a+b] = G_ab.  Returns false for a coincident
 // pair without a self rule (reference returns None -> SingularEvaluationError).
-HMX_D bool green_pair(const GreenParams& P, double dx, double dy, double dz, double nxv, double nyv,
-                      double nzv, double2* out) {
+// KIND is the compile-time kernel kind (0 H, 1 U, 2 T); -1 dispatches on P.kind.
+template <int KIND>
+HMX_D bool green_pair_k(const GreenParams& P, double dx, double dy, double dz, double nxv, double nyv,
+                        double nzv, double2* out) {
+  const int kind = KIND >= 0 ? KIND : P.kind;
   const double r2 = dx * dx + dy * dy + dz * dz;
   if (r2 == 0.0) {
-    if (P.kind == 0) {
+    if (kind == 0) {
       out[0] = cmk(P.shift, 0.0);
     } else {
 #pragma unroll
@@ -70,15 +73,16 @@ HMX_D bool green_pair(const GreenParams& P, double dx, double dy, double dz, dou
   }
   const double r = sqrt(r2);
   const double ir = 1.0 / r;
-  if (P.kind == 0) {
+  if (kind == 0) {
     double s, c;
     sincos(P.kappa * r, &s, &c);
     const double scl = HMX_INV_4PI * ir;
     out[0] = cmk(c * scl, s * scl);
     return true;
   }
+  if (KIND == 0) return true;  // unreachable: kind 0 returned above
   const double z[3] = {dx * ir, dy * ir, dz * ir};
-  if (P.kind == 1) {
+  if (kind == 1) {
     double2 gs[3], gp[3];
     radial_series<2>(P.ks, r, ir, gs);
     radial_series<2>(P.kp, r, ir, gp);
@@ -98,6 +102,7 @@ HMX_D bool green_pair(const GreenParams& P, double dx, double dy, double dz, dou
       }
     return true;
   }
+  if (KIND == 1) return true;  // unreachable
   // kind == 2: traction T
   double2 gs[4], gp[4];
   radial_series<3>(P.ks, r, ir, gs);
@@ -135,17 +140,28 @@ HMX_D bool green_pair(const GreenParams& P, double dx, double dy, double dz, dou
   return true;
 }
 
+HMX_D bool green_pair(const GreenParams& P, double dx, double dy, double dz, double nxv, double nyv, double nzv,
+                      double2* out) {
+  return green_pair_k<-1>(P, dx, dy, dz, nxv, nyv, nzv, out);
+}
+
 // Entry block of row point i of X and column point j of Y (normals from Y).
-HMX_D bool green_xy(const GreenParams& P, const PointsSoA& X, int64_t i, const PointsSoA& Y, int64_t j,
-                    double2* out) {
+template <int KIND>
+HMX_D bool green_xy_k(const GreenParams& P, const PointsSoA& X, int64_t i, const PointsSoA& Y, int64_t j,
+                      double2* out) {
   const double dx = X.x[i] - Y.x[j];
   const double dy = X.y[i] - Y.y[j];
   const double dz = X.z[i] - Y.z[j];
   double nx = 0, ny = 0, nz = 0;
-  if (P.kind == 2) {
+  if ((KIND >= 0 ? KIND : P.kind) == 2) {
     nx = Y.nx[j];
     ny = Y.ny[j];
     nz = Y.nz[j];
   }
-  return green_pair(P, dx, dy, dz, nx, ny, nz, out);
+  return green_pair_k<KIND>(P, dx, dy, dz, nx, ny, nz, out);
+}
+
+HMX_D bool green_xy(const GreenParams& P, const PointsSoA& X, int64_t i, const PointsSoA& Y, int64_t j,
+                    double2* out) {
+  return green_xy_k<-1>(P, X, i, Y, j, out);
 }

@@ -86,17 +86,17 @@ __global__ void __launch_bounds__(kThreads) mv_phase2(const MvTile2* __restrict_
     int c = part;
     const int step = parts;
     for (; c + 3 * step < T.ncols; c += 4 * step) {
-      const double2 m0 = __ldcs(mp + (int64_t)c * ld);
-      const double2 m1 = __ldcs(mp + (int64_t)(c + step) * ld);
-      const double2 m2 = __ldcs(mp + (int64_t)(c + 2 * step) * ld);
-      const double2 m3 = __ldcs(mp + (int64_t)(c + 3 * step) * ld);
+      const double2 m0 = mp[(int64_t)c * ld];
+      const double2 m1 = mp[(int64_t)(c + step) * ld];
+      const double2 m2 = mp[(int64_t)(c + 2 * step) * ld];
+      const double2 m3 = mp[(int64_t)(c + 3 * step) * ld];
       const double2 s0 = sp[c], s1 = sp[c + step], s2 = sp[c + 2 * step], s3 = sp[c + 3 * step];
       a0 = cfma(m0, s0, a0);
       a1 = cfma(m1, s1, a1);
       a0 = cfma(m2, s2, a0);
       a1 = cfma(m3, s3, a1);
     }
-    for (; c < T.ncols; c += step) a0 = cfma(__ldcs(mp + (int64_t)c * ld), sp[c], a0);
+    for (; c < T.ncols; c += step) a0 = cfma(mp[(int64_t)c * ld], sp[c], a0);
   }
   const double2 acc = cadd(a0, a1);
   if (parts == 1) {
@@ -136,18 +136,24 @@ int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
   };
   const int d = H.d;
   const int64_t nb = H.nb;
-  // ---- row segments keyed by (r0, r1)
-  std::map<std::pair<int64_t, int64_t>, int64_t> segid;
-  for (int64_t b = 0; b < nb; ++b) segid.emplace(std::make_pair(H.table[5 * b + 1], H.table[5 * b + 2]), 0);
-  std::vector<std::pair<int64_t, int64_t>> segs;
-  segs.reserve(segid.size());
-  for (auto& kv : segid) segs.push_back(kv.first);
-  // nesting order: r0 ascending, r1 descending
-  std::sort(segs.begin(), segs.end(), [](const auto& a, const auto& b) {
-    return a.first != b.first ? a.first < b.first : a.second > b.second;
+  // ---- row segments keyed by (r0, r1): sort leaves by (r0 asc, r1 desc) = nesting order
+  std::vector<int64_t> byrow(nb);
+  std::iota(byrow.begin(), byrow.end(), int64_t(0));
+  std::sort(byrow.begin(), byrow.end(), [&](int64_t a, int64_t b) {
+    const int64_t a0 = H.table[5 * a + 1], b0 = H.table[5 * b + 1];
+    if (a0 != b0) return a0 < b0;
+    const int64_t a1 = H.table[5 * a + 2], b1 = H.table[5 * b + 2];
+    return a1 != b1 ? a1 > b1 : a < b;
   });
+  std::vector<std::pair<int64_t, int64_t>> segs;
+  std::vector<int64_t> bseg(nb);
+  for (int64_t q = 0; q < nb; ++q) {
+    const int64_t b = byrow[q];
+    const std::pair<int64_t, int64_t> key(H.table[5 * b + 1], H.table[5 * b + 2]);
+    if (segs.empty() || segs.back() != key) segs.push_back(key);
+    bseg[b] = (int64_t)segs.size() - 1;
+  }
   const int64_t ns = (int64_t)segs.size();
-  for (int64_t g = 0; g < ns; ++g) segid[segs[g]] = g;
   std::vector<int64_t> level(ns);
   {
     std::vector<int64_t> stack;
@@ -160,10 +166,9 @@ int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
     }
     H.nlevels = maxlev + 1;
   }
-  std::vector<int64_t> ncols(ns, 0), colstart(nb, 0), bseg(nb);
+  std::vector<int64_t> ncols(ns, 0), colstart(nb, 0);
   for (int64_t b = 0; b < nb; ++b) {
-    const int64_t g = segid[std::make_pair(H.table[5 * b + 1], H.table[5 * b + 2])];
-    bseg[b] = g;
+    const int64_t g = bseg[b];
     colstart[b] = ncols[g];
     const int64_t n = H.table[5 * b + 4] - H.table[5 * b + 3];
     ncols[g] += H.table[5 * b] == 0 ? d * n : H.rank_after[b];
@@ -184,6 +189,11 @@ int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
   int64_t vo = 0;
   double dense_b = 0, lr_b = 0;
   std::vector<MvJob1> jobs;
+  {
+    int64_t nj = 0;
+    for (int64_t b = 0; b < nb; ++b) nj += H.table[5 * b] == 0 ? 1 : H.rank_after[b];
+    jobs.reserve(nj);
+  }
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t g = bseg[b];
     const int64_t m = H.table[5 * b + 2] - H.table[5 * b + 1];
