@@ -99,6 +99,8 @@ int hmx_ctx_create(int32_t device, hmx_ctx** out);
 /* launch on an existing cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream; 0 = legacy default stream) */
 int hmx_ctx_set_stream(hmx_ctx* ctx, uint64_t stream);
 int hmx_ctx_sync(hmx_ctx* ctx);
+/* release device memory cached by the context's stream-ordered pool */
+int hmx_ctx_release_cache(hmx_ctx* ctx);
 int hmx_ctx_destroy(hmx_ctx* ctx);
 
 /* ---- geometry (host, bit-exact with geometry.py) -------------------------- */

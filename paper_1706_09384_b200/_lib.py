@@ -49,6 +49,7 @@ SIGNATURES = {
     "hmx_ctx_create": (C.c_int, [i32, C.POINTER(P)]),
     "hmx_ctx_set_stream": (C.c_int, [P, u64]),
     "hmx_ctx_sync": (C.c_int, [P]),
+    "hmx_ctx_release_cache": (C.c_int, [P]),
     "hmx_ctx_destroy": (C.c_int, [P]),
     "hmx_tree_build": (C.c_int, [P, i64, i64, C.POINTER(P)]),
     "hmx_tree_num_nodes": (i64, [P]),

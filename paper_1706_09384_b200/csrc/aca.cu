@@ -26,15 +26,17 @@
 #include <cstdio>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "green.cuh"
 #include "hmatrix.h"
+
+namespace cg = cooperative_groups;
 
 namespace hmx {
 
 namespace {
 
-constexpr int kThreads = 256;
-constexpr int kWarps = kThreads / 32;
 constexpr int kGramGroup = 4;
 
 // sigma_1 and sigma_3 of a 3x3 complex matrix from the characteristic
@@ -133,7 +135,7 @@ HMX_D void inverse(const double2* P, double2* G) {
 
 constexpr int kMaxWarps = 32;
 struct Shared {
-  int ipiv, jpiv, inext, K, steps, state, zero_rows, verdict;
+  int ipiv, jpiv, K, steps, state, zero_rows, verdict;
   double normB2, s1max;
   double2 gamma[9];
   double red_v[kMaxWarps];
@@ -142,18 +144,48 @@ struct Shared {
   double red_a[kMaxWarps];
 };
 
+// What each CTA of a cluster publishes for the cluster-wide reductions
+// (read by the other CTAs through distributed shared memory).
+struct Pub {
+  double row_v, row_s1, col_v, cross;
+  int row_i, col_i;
+};
+
 // state codes
 constexpr int kRun = 0, kZeroRow = 1, kDone = 2;
 
-template <int D, int KIND, int NT, int MINB>
+template <int CS>
+HMX_D void cluster_sync() {
+  if constexpr (CS > 1) cg::this_cluster().sync();
+}
+
+template <int CS, class T>
+HMX_D T* peer(T* p, int r) {
+  if constexpr (CS > 1) return cg::this_cluster().map_shared_rank(p, r);
+  return p;
+}
+
+// CS CTAs (a thread-block cluster, distributed shared memory for the
+// reductions) cooperate on one admissible leaf; CS = 1 is one CTA per leaf.
+// Every CTA keeps an identical copy of the ACA state (all decisions are made
+// from the same reduced values in the same order -> deterministic).
+// CTA rank cr owns column points [n cr/CS, n (cr+1)/CS) in the row pass and
+// row points [m cr/CS, ...) in the column pass; its Gram partial sums run over
+// exactly the factor rows it wrote, so no barrier is needed before the Gram pass.
+template <int D, int KIND, int NT, int MINB, int CS>
 __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA pts, const AcaDesc* __restrict__ desc,
                                                        const int32_t* __restrict__ order, double eps, double floor,
                                                        double2* __restrict__ U, double2* __restrict__ V,
-                                                       double2* __restrict__ G, AcaOut* __restrict__ out, int kcap_max) {
+                                                       double2* __restrict__ G, AcaOut* __restrict__ out,
+                                                       int kcap_max) {
   extern __shared__ double2 dyn[];
   __shared__ Shared sh;
+  __shared__ Pub pub;
+  constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int b = order[blockIdx.x];
+  int cr = 0;
+  if constexpr (CS > 1) cr = (int)cg::this_cluster().block_rank();
+  const int b = order[blockIdx.x / CS];
   const AcaDesc ds = desc[b];
   const int m = ds.m, n = ds.n, kcap = ds.kcap;
   const int64_t ldu = (int64_t)D * m, ldv = (int64_t)D * n;
@@ -161,9 +193,12 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
   double2* __restrict__ Vb = V + ds.voff;
   double2* __restrict__ GU = G + ds.goff;
   double2* __restrict__ GV = GU + (int64_t)kcap * kcap;
-  double2* Urow = dyn;                      // D x kcap_max
-  double2* Vrow = dyn + D * kcap_max;       // D x kcap_max
-  unsigned char* visited = reinterpret_cast<unsigned char*>(dyn + 2 * D * kcap_max);
+  const int j0 = (int)((int64_t)n * cr / CS), j1 = (int)((int64_t)n * (cr + 1) / CS);
+  const int i0 = (int)((int64_t)m * cr / CS), i1 = (int)((int64_t)m * (cr + 1) / CS);
+  double2* Urow = dyn;                 // D x kcap_max
+  double2* Vrow = dyn + D * kcap_max;  // D x kcap_max
+  double2* pubG = Vrow + D * kcap_max; // (CS > 1) 2 x D x kcap_max partial Gram columns
+  unsigned char* visited = reinterpret_cast<unsigned char*>(pubG + (CS > 1 ? 2 * D * kcap_max : 0));
 
   for (int i = tid; i < m; i += NT) visited[i] = 0;
   if (tid == 0) {
@@ -192,16 +227,34 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
     }
     __syncthreads();
 
-    // ---- row pass ------------------------------------------------------------
+    // ---- row pass (own column points) -----------------------------------------
     ArgMax best{-1.0, 0x7fffffff};
     double rs1 = 0.0;
-    for (int j = tid; j < n; j += NT) {
+    for (int j = j0 + tid; j < j1; j += NT) {
       double2 acc[D * D];
 #pragma unroll
       for (int t = 0; t < D * D; ++t) acc[t] = cmk(0.0, 0.0);
       const double2* vp = Vb + (int64_t)D * j;
+      // 4 factor columns per iteration: 4 D independent loads in flight
+      int l = 0;
 #pragma unroll 1
-      for (int l = 0; l < K; ++l) {
+      for (; l + 3 < K; l += 4) {
+        double2 vv[4][D];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int c = 0; c < D; ++c) vv[u][c] = vp[(int64_t)(l + u) * ldv + c];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int a = 0; a < D; ++a) {
+            const double2 ua = Urow[a * kcap_max + l + u];
+#pragma unroll
+            for (int c = 0; c < D; ++c) acc[a * D + c] = cfma_cj(ua, vv[u][c], acc[a * D + c]);
+          }
+      }
+#pragma unroll 1
+      for (; l < K; ++l) {
         double2 vv[D];
 #pragma unroll
         for (int c = 0; c < D; ++c) vv[c] = vp[(int64_t)l * ldv + c];
@@ -238,9 +291,22 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
     if (tid == 0) {
       ArgMax bb{sh.red_v[0], sh.red_i[0]};
       double r1 = sh.red_s[0];
-      for (int w = 1; w < (NT / 32); ++w) {
+      for (int w = 1; w < NW; ++w) {
         bb = argmax_pick(bb, ArgMax{sh.red_v[w], sh.red_i[w]});
         r1 = fmax(r1, sh.red_s[w]);
+      }
+      pub.row_v = bb.v;
+      pub.row_i = bb.i;
+      pub.row_s1 = r1;
+    }
+    cluster_sync<CS>();  // row-pass results (and the new V columns) visible cluster-wide
+    if (tid == 0) {
+      ArgMax bb{-1.0, 0x7fffffff};
+      double r1 = 0.0;
+      for (int r = 0; r < CS; ++r) {
+        const Pub* q = peer<CS>(&pub, r);
+        bb = argmax_pick(bb, ArgMax{q->row_v, q->row_i});
+        r1 = fmax(r1, q->row_s1);
       }
       sh.s1max = fmax(sh.s1max, r1);
       if (r1 <= floor * sh.s1max || sh.s1max == 0.0) {
@@ -272,7 +338,10 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
       }
     }
     __syncthreads();
-    if (sh.state == kZeroRow) continue;
+    if (sh.state == kZeroRow) {
+      cluster_sync<CS>();  // everyone has read pub.row_* before it is rewritten
+      continue;
+    }
     if (sh.state == kDone) {
       status = sh.verdict;
       break;
@@ -287,15 +356,32 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
     for (int t = 0; t < D * D; ++t) gam[t] = sh.gamma[t];
     __syncthreads();
 
-    // ---- column pass ---------------------------------------------------------
+    // ---- column pass (own row points) -------------------------------------------
     best = ArgMax{-1.0, 0x7fffffff};
-    for (int i = tid; i < m; i += NT) {
+    for (int i = i0 + tid; i < i1; i += NT) {
       double2 acc[D * D];
 #pragma unroll
       for (int t = 0; t < D * D; ++t) acc[t] = cmk(0.0, 0.0);
       const double2* up = Ub + (int64_t)D * i;
+      int l = 0;
 #pragma unroll 1
-      for (int l = 0; l < K; ++l) {
+      for (; l + 3 < K; l += 4) {
+        double2 uu[4][D];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int a = 0; a < D; ++a) uu[u][a] = up[(int64_t)(l + u) * ldu + a];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+#pragma unroll
+          for (int c = 0; c < D; ++c) {
+            const double2 vc = Vrow[c * kcap_max + l + u];
+#pragma unroll
+            for (int a = 0; a < D; ++a) acc[a * D + c] = cfma_cj(uu[u][a], vc, acc[a * D + c]);
+          }
+      }
+#pragma unroll 1
+      for (; l < K; ++l) {
         double2 uu[D];
 #pragma unroll
         for (int a = 0; a < D; ++a) uu[a] = up[(int64_t)l * ldu + a];
@@ -332,22 +418,30 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
       sh.red_i[warp] = best.i;
     }
     __syncthreads();
+    if (tid == 0) {
+      ArgMax bb{sh.red_v[0], sh.red_i[0]};
+      for (int w = 1; w < NW; ++w) bb = argmax_pick(bb, ArgMax{sh.red_v[w], sh.red_i[w]});
+      pub.col_v = bb.v;
+      pub.col_i = bb.i;
+    }
 
-    // ---- Gram pass: G(:, K:K+D) = F^H f_new for F = U and V -----------------------
+    // ---- Gram pass: G(:, K:K+D) = F^H f_new over this CTA's factor rows -----------
     const int Kn = K + D;
     const int ngroups = (Kn + kGramGroup - 1) / kGramGroup;
     for (int side = 0; side < 2; ++side) {
       const double2* F = side == 0 ? Ub : Vb;
       const int64_t ld = side == 0 ? ldu : ldv;
+      const int64_t q0 = (int64_t)D * (side == 0 ? i0 : j0), q1 = (int64_t)D * (side == 0 ? i1 : j1);
       double2* Gm = side == 0 ? GU : GV;
-      for (int grp = warp; grp < ngroups; grp += (NT / 32)) {
+      for (int grp = warp; grp < ngroups; grp += NW) {
         double2 acc[kGramGroup][D];
 #pragma unroll
         for (int t = 0; t < kGramGroup; ++t)
 #pragma unroll
           for (int c = 0; c < D; ++c) acc[t][c] = cmk(0.0, 0.0);
         const int l0 = grp * kGramGroup;
-        for (int64_t q = lane; q < ld; q += 32) {
+#pragma unroll 2
+        for (int64_t q = q0 + lane; q < q1; q += 32) {
           double2 nf[D];
 #pragma unroll
           for (int c = 0; c < D; ++c) nf[c] = F[q + (int64_t)(K + c) * ld];
@@ -371,15 +465,38 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
             if (l >= Kn) continue;
 #pragma unroll
             for (int c = 0; c < D; ++c) {
-              const int col = K + c;
-              if (l < K || l < col) {
-                Gm[l + (int64_t)col * kcap] = acc[t][c];
-                Gm[col + (int64_t)l * kcap] = cconj(acc[t][c]);
-              } else if (l == col) {
-                Gm[l + (int64_t)col * kcap] = cmk(acc[t][c].x, 0.0);
+              if constexpr (CS > 1) {
+                pubG[(side * D + c) * kcap_max + l] = acc[t][c];
+              } else {
+                const int col = K + c;
+                if (l < K || l < col) {
+                  Gm[l + (int64_t)col * kcap] = acc[t][c];
+                  Gm[col + (int64_t)l * kcap] = cconj(acc[t][c]);
+                } else if (l == col) {
+                  Gm[l + (int64_t)col * kcap] = cmk(acc[t][c].x, 0.0);
+                }
               }
             }
           }
+        }
+      }
+    }
+    if constexpr (CS > 1) {
+      // combine the CS partial Gram columns (fixed rank order); CTA cr finalises
+      // the entries l = cr, cr + CS, ... and writes them to global G
+      cluster_sync<CS>();
+      for (int t = tid; t < 2 * D * Kn; t += NT) {
+        const int l = t % Kn, sc = t / Kn;  // sc = side * D + c
+        if (l % CS != cr) continue;
+        double2 v = cmk(0.0, 0.0);
+        for (int r = 0; r < CS; ++r) v = cadd(v, peer<CS>(pubG, r)[sc * kcap_max + l]);
+        const int side = sc / D, c = sc - side * D, col = K + c;
+        double2* Gm = side == 0 ? GU : GV;
+        if (l < K || l < col) {
+          Gm[l + (int64_t)col * kcap] = v;
+          Gm[col + (int64_t)l * kcap] = cconj(v);
+        } else if (l == col) {
+          Gm[l + (int64_t)col * kcap] = cmk(v.x, 0.0);
         }
       }
     }
@@ -389,6 +506,7 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
     double cross = 0.0;
     for (int t = tid; t < K * D; t += NT) {
       const int l = t / D, c = t - l * D;
+      if (l % CS != cr) continue;  // this CTA's finalised entries
       const double2 gu = GU[l + (int64_t)(K + c) * kcap];
       const double2 gv = GV[l + (int64_t)(K + c) * kcap];
       cross += gu.x * gv.x + gu.y * gv.y;
@@ -397,8 +515,19 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
     if (lane == 0) sh.red_a[warp] = cross;
     __syncthreads();
     if (tid == 0) {
-      double cr = 0.0;
-      for (int w = 0; w < (NT / 32); ++w) cr += sh.red_a[w];
+      double cr_sum = 0.0;
+      for (int w = 0; w < NW; ++w) cr_sum += sh.red_a[w];
+      pub.cross = cr_sum;
+    }
+    cluster_sync<CS>();  // cross partials, column argmax and G entries visible
+    if (tid == 0) {
+      double crs = 0.0;
+      ArgMax bb{-1.0, 0x7fffffff};
+      for (int r = 0; r < CS; ++r) {
+        const Pub* q = peer<CS>(&pub, r);
+        crs += q->cross;
+        bb = argmax_pick(bb, ArgMax{q->col_v, q->col_i});
+      }
       double diag = 0.0, nu = 0.0, nv = 0.0;
       for (int c = 0; c < D; ++c) {
         nu += GU[(K + c) + (int64_t)(K + c) * kcap].x;
@@ -409,11 +538,9 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
           diag += a.x * bq.x - a.y * bq.y;
         }
       }
-      sh.normB2 = sh.normB2 + 2.0 * cr + diag;
+      sh.normB2 = sh.normB2 + 2.0 * crs + diag;
       sh.K = Kn;
       sh.steps += 1;
-      ArgMax bb{sh.red_v[0], sh.red_i[0]};
-      for (int w = 1; w < (NT / 32); ++w) bb = argmax_pick(bb, ArgMax{sh.red_v[w], sh.red_i[w]});
       const int dmin = D * (m < n ? m : n);
       if (sqrt(nu) * sqrt(nv) <= eps * sqrt(fmax(sh.normB2, 0.0))) {
         sh.state = kDone;
@@ -430,12 +557,13 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
       }
     }
     __syncthreads();
+    cluster_sync<CS>();  // all peers done reading pub before the next step rewrites it
     if (sh.state == kDone) {
       status = sh.verdict;
       break;
     }
   }
-  if (tid == 0) {
+  if (tid == 0 && cr == 0) {
     AcaOut o;
     o.steps = sh.steps;
     o.rank = sh.K;
@@ -447,29 +575,65 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
 
 }  // namespace
 
+void warm_aca() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, aca_kernel<1, 0, 512, 1, 1>);
+  cudaFuncGetAttributes(&a, aca_kernel<3, 1, 512, 1, 1>);
+  cudaFuncGetAttributes(&a, aca_kernel<3, 2, 512, 1, 1>);
+}
+
 int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const AcaDesc* d_desc, const int32_t* d_order,
                int64_t nblk, int kcap_max, int m_max, double eps, double sigma3_floor, double2* U, double2* V,
-               double2* G, AcaOut* d_out) {
+               double2* G, AcaOut* d_out, int cluster) {
   if (nblk == 0) return HMX_OK;
-  size_t smem = sizeof(double2) * 2 * (size_t)d * kcap_max + (size_t)((m_max + 15) / 16) * 16;
-  auto go = [&](auto kern, int nt) -> int {
+  const int CSv = cluster > 1 ? cluster : 1;
+  size_t smem = sizeof(double2) * (CSv > 1 ? 4 : 2) * (size_t)d * kcap_max + (size_t)((m_max + 15) / 16) * 16;
+  // One resident CTA per SM keeps each leaf's factors hot in L1 (the ACA passes
+  // re-read them every step: 2-3 CTAs/SM measured 1.4-1.8x slower); 512 threads
+  // (128 registers) give that CTA 16 warps of memory parallelism.  Large
+  // leaves run on a cluster of kAcaCluster CTAs (SMs) so they do not set the
+  // critical path of the whole launch.
+  auto go = [&](auto kern) -> int {
     HMX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)nblk, nt, smem, c.stream>>>(P, pts, d_desc, d_order, eps, sigma3_floor, U, V, G, d_out,
-                                                 kcap_max);
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)(nblk * CSv));
+    cfg.blockDim = dim3(512);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = c.stream;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CSv;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    HMX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, P, pts, d_desc, d_order, eps, sigma3_floor, U, V, G, d_out,
+                                    kcap_max));
     return HMX_OK;
   };
-  // one resident CTA per SM keeps each leaf's factors hot in L1 (the ACA passes
-  // re-read them every step: 2-3 CTAs/SM measured 1.4-1.8x slower); 512 threads
-  // (128 registers) give that CTA 16 warps of memory parallelism.
-  const char* nts = std::getenv("HMX_ACA_NT");
-  const bool wide = !(nts && std::atoi(nts) == 256);
   int rc;
-  if (P.kind == 0)
-    rc = wide ? go(aca_kernel<1, 0, 512, 1>, 512) : go(aca_kernel<1, 0, 256, 1>, 256);
-  else if (P.kind == 1)
-    rc = wide ? go(aca_kernel<3, 1, 512, 1>, 512) : go(aca_kernel<3, 1, 256, 1>, 256);
-  else
-    rc = wide ? go(aca_kernel<3, 2, 512, 1>, 512) : go(aca_kernel<3, 2, 256, 1>, 256);
+  if (CSv == 8) {
+    if (P.kind == 0)
+      rc = go(aca_kernel<1, 0, 512, 1, 8>);
+    else if (P.kind == 1)
+      rc = go(aca_kernel<3, 1, 512, 1, 8>);
+    else
+      rc = go(aca_kernel<3, 2, 512, 1, 8>);
+  } else if (CSv == 4) {
+    if (P.kind == 0)
+      rc = go(aca_kernel<1, 0, 512, 1, 4>);
+    else if (P.kind == 1)
+      rc = go(aca_kernel<3, 1, 512, 1, 4>);
+    else
+      rc = go(aca_kernel<3, 2, 512, 1, 4>);
+  } else {
+    if (P.kind == 0)
+      rc = go(aca_kernel<1, 0, 512, 1, 1>);
+    else if (P.kind == 1)
+      rc = go(aca_kernel<3, 1, 512, 1, 1>);
+    else
+      rc = go(aca_kernel<3, 2, 512, 1, 1>);
+  }
   if (rc) return rc;
   HMX_CUDA_TRY(cudaGetLastError());
   return HMX_OK;

@@ -37,6 +37,20 @@ void hmx_set_error(const char* fmt, ...) {
 struct hmx_ctx {
   hmx::Ctx c;
 };
+
+namespace hmx {
+cudaError_t dev_alloc(Ctx& c, void** p, size_t bytes) {
+  if (c.pool) return cudaMallocFromPoolAsync(p, bytes, c.pool, c.stream);
+  return cudaMalloc(p, bytes);
+}
+void dev_free(Ctx& c, void* p) {
+  if (!p) return;
+  if (c.pool)
+    cudaFreeAsync(p, c.stream);
+  else
+    cudaFree(p);
+}
+}  // namespace hmx
 struct hmx_tree {
   hmx::ClusterTree t;
 };
@@ -69,10 +83,11 @@ GreenParams make_params(const hmx_kernel* k, int has_shift, double shift) {
 
 // device SoA copy of (n x 3) points (+ normals)
 struct DevPoints {
+  Ctx* ctx = nullptr;
   double* buf = nullptr;
   PointsSoA soa{};
   ~DevPoints() {
-    if (buf) cudaFree(buf);
+    if (buf) dev_free(*ctx, buf);
   }
   int upload(Ctx& c, const double* pts, const double* nrm, int64_t n) {
     const int nc = nrm ? 6 : 3;
@@ -82,7 +97,8 @@ struct DevPoints {
         h[(size_t)k * n + i] = pts[3 * i + k];
         if (nrm) h[(size_t)(3 + k) * n + i] = nrm[3 * i + k];
       }
-    HMX_CUDA_TRY(cudaMalloc(&buf, sizeof(double) * h.size() + 8));
+    ctx = &c;
+    HMX_CUDA_TRY(dev_alloc(c, reinterpret_cast<void**>(&buf), sizeof(double) * h.size() + 8));
     HMX_CUDA_TRY(cudaMemcpyAsync(buf, h.data(), sizeof(double) * h.size(), cudaMemcpyHostToDevice, c.stream));
     HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
     soa.x = buf;
@@ -97,22 +113,25 @@ struct DevPoints {
 
 template <class T>
 int dev_upload(Ctx& c, T** dst, const std::vector<T>& src) {
-  HMX_CUDA_TRY(cudaMalloc(dst, sizeof(T) * std::max<size_t>(src.size(), 1)));
+  HMX_CUDA_TRY(dev_alloc_t(c, dst, src.size()));
   if (!src.empty())
     HMX_CUDA_TRY(cudaMemcpyAsync(*dst, src.data(), sizeof(T) * src.size(), cudaMemcpyHostToDevice, c.stream));
   return HMX_OK;
 }
 
 struct DevBuf {
+  Ctx* ctx = nullptr;
   std::vector<void*> p;
+  explicit DevBuf(Ctx& c) : ctx(&c) {}
+  DevBuf(DevBuf&& o) noexcept : ctx(o.ctx), p(std::move(o.p)) { o.p.clear(); }
+  DevBuf(const DevBuf&) = delete;
   ~DevBuf() {
-    for (void* q : p)
-      if (q) cudaFree(q);
+    for (void* q : p) dev_free(*ctx, q);
   }
   template <class T>
   int alloc(T** out, int64_t count) {
     void* q = nullptr;
-    cudaError_t e = cudaMalloc(&q, sizeof(T) * std::max<int64_t>(count, 1));
+    cudaError_t e = dev_alloc(*ctx, &q, sizeof(T) * std::max<int64_t>(count, 1));
     if (e != cudaSuccess) {
       hmx_set_error("cudaMalloc(%lld bytes): %s", (long long)(sizeof(T) * count), cudaGetErrorString(e));
       return e == cudaErrorMemoryAllocation ? HMX_ENOMEM : HMX_ECUDA;
@@ -126,7 +145,7 @@ struct DevBuf {
 void free_h(DeviceH& H) {
   void* ptrs[] = {H.d_perm, H.d_row, H.d_v, H.d_s, H.d_xt, H.d_ylev, H.d_xio, H.d_yio, H.d_job1, H.d_tile2};
   for (void* p : ptrs)
-    if (p) cudaFree(p);
+    if (p) dev_free(*H.ctx, p);
   H.d_perm = nullptr;
   H.d_row = H.d_v = H.d_s = H.d_xt = H.d_ylev = H.d_xio = H.d_yio = nullptr;
   H.d_job1 = nullptr;
@@ -151,6 +170,7 @@ int validate_table(const int64_t* table, int64_t nb, int64_t np) {
 }
 
 struct AcaPass {
+  explicit AcaPass(Ctx& c) : mem(c) {}
   DevBuf mem;
   double2 *U = nullptr, *V = nullptr, *G = nullptr, *W = nullptr;
   std::vector<int64_t> blocks;  // block ids
@@ -189,6 +209,23 @@ int hmx_ctx_create(int32_t device, hmx_ctx** out) {
   c->c.l2_bytes = prop.l2CacheSize;
   HMX_CUDA_TRY(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
   c->c.own_stream = true;
+  HMX_CUDA_TRY(cudaStreamCreateWithFlags(&c->c.aux, cudaStreamNonBlocking));
+  // HMX_POOL=1: stream-ordered pool allocations (measured slower for the first
+  // assembly and for T65k on this driver; off by default)
+  if (const char* ep = std::getenv("HMX_POOL"); ep && ep[0] == '1') {
+    cudaMemPoolProps props = {};
+    props.allocType = cudaMemAllocationTypePinned;
+    props.location.type = cudaMemLocationTypeDevice;
+    props.location.id = device;
+    HMX_CUDA_TRY(cudaMemPoolCreate(&c->c.pool, &props));
+    uint64_t keep = UINT64_MAX;
+    HMX_CUDA_TRY(cudaMemPoolSetAttribute(c->c.pool, cudaMemPoolAttrReleaseThreshold, &keep));
+  }
+  warm_aca();
+  warm_recompress();
+  warm_dense();
+  warm_matvec();
+  warm_gmres();
   *out = c;
   return HMX_OK;
 }
@@ -204,6 +241,14 @@ int hmx_ctx_set_stream(hmx_ctx* ctx, uint64_t stream) {
   return HMX_OK;
 }
 
+int hmx_ctx_release_cache(hmx_ctx* ctx) {
+  if (!ctx) return HMX_EINVAL;
+  HMX_CUDA_TRY(cudaSetDevice(ctx->c.device));
+  HMX_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
+  if (ctx->c.pool) HMX_CUDA_TRY(cudaMemPoolTrimTo(ctx->c.pool, 0));
+  return HMX_OK;
+}
+
 int hmx_ctx_sync(hmx_ctx* ctx) {
   if (!ctx) return HMX_EINVAL;
   HMX_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
@@ -214,6 +259,8 @@ int hmx_ctx_destroy(hmx_ctx* ctx) {
   if (!ctx) return HMX_OK;
   cudaSetDevice(ctx->c.device);
   if (ctx->c.own_stream && ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
+  if (ctx->c.aux) cudaStreamDestroy(ctx->c.aux);
+  if (ctx->c.pool) cudaMemPoolDestroy(ctx->c.pool);
   delete ctx;
   return HMX_OK;
 }
@@ -309,7 +356,7 @@ int hmx_eval_block(hmx_ctx* ctx, const hmx_kernel* k, const double* X, int64_t m
   if (rc) return rc;
   rc = dy.upload(c, Y, k->kind == HMX_ELASTO_T ? NY : nullptr, n);
   if (rc) return rc;
-  DevBuf mem;
+  DevBuf mem(c);
   double2* dout;
   int32_t* derr;
   if ((rc = mem.alloc(&dout, (int64_t)d * d * m * n))) return rc;
@@ -441,7 +488,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   int64_t m_max_all = 1;
   for (int64_t b : adm) m_max_all = std::max(m_max_all, rows_of(b));
   while (!todo.empty()) {
-    passes.emplace_back();
+    passes.emplace_back(c);
     AcaPass& ps = passes.back();
     std::sort(todo.begin(), todo.end(), [&](int64_t a, int64_t b) {
       const int64_t ca = rows_of(a) + cols_of(a), cb = rows_of(b) + cols_of(b);
@@ -474,7 +521,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     AcaDesc* d_desc;
     AcaOut* d_out;
     int32_t* d_order;
-    DevBuf tmp;
+    DevBuf tmp(c);
     if ((rc = tmp.alloc(&d_desc, (int64_t)todo.size()))) return fail(rc);
     if ((rc = tmp.alloc(&d_out, (int64_t)todo.size()))) return fail(rc);
     if ((rc = tmp.alloc(&d_order, (int64_t)todo.size()))) return fail(rc);
@@ -485,9 +532,35 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     HMX_CUDA_TRY(
         cudaMemcpyAsync(d_order, order.data(), sizeof(int32_t) * todo.size(), cudaMemcpyHostToDevice, c.stream));
     tick("aca: workspace alloc");
-    if ((rc = launch_aca(c, d, P, pts.soa, d_desc, d_order, (int64_t)todo.size(), ps.kcap_max, (int)m_max_all,
-                         cfg->eps, cfg->sigma3_floor > 0 ? cfg->sigma3_floor : 1e-12, ps.U, ps.V, ps.G, d_out)))
-      return fail(rc);
+    {
+      // large leaves (a prefix of the size-sorted list) on CTA clusters in an
+      // auxiliary stream, concurrently with the one-CTA-per-leaf launch
+      const char* e_cs = std::getenv("HMX_ACA_CS");
+      const char* e_min = std::getenv("HMX_ACA_CLUSTER_MIN");
+      const int cs = e_cs ? std::atoi(e_cs) : 1;  // clusters measured slower
+      const int64_t cmin = e_min ? std::atoll(e_min) : kAcaClusterMin;
+      size_t nbig = 0;
+      while (cs > 1 && nbig < todo.size() && rows_of(todo[nbig]) + cols_of(todo[nbig]) >= cmin) ++nbig;
+      const double s3f = cfg->sigma3_floor > 0 ? cfg->sigma3_floor : 1e-12;
+      cudaEvent_t fork, join;
+      HMX_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      HMX_CUDA_TRY(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+      HMX_CUDA_TRY(cudaEventRecord(fork, c.stream));
+      HMX_CUDA_TRY(cudaStreamWaitEvent(c.aux, fork, 0));
+      Ctx caux = c;
+      caux.stream = c.aux;
+      if (nbig && (rc = launch_aca(caux, d, P, pts.soa, d_desc, d_order, (int64_t)nbig, ps.kcap_max, (int)m_max_all,
+                                   cfg->eps, s3f, ps.U, ps.V, ps.G, d_out, cs)))
+        return fail(rc);
+      if (todo.size() > nbig &&
+          (rc = launch_aca(c, d, P, pts.soa, d_desc, d_order + nbig, (int64_t)(todo.size() - nbig), ps.kcap_max,
+                           (int)m_max_all, cfg->eps, s3f, ps.U, ps.V, ps.G, d_out, 1)))
+        return fail(rc);
+      HMX_CUDA_TRY(cudaEventRecord(join, c.aux));
+      HMX_CUDA_TRY(cudaStreamWaitEvent(c.stream, join, 0));
+      cudaEventDestroy(fork);
+      cudaEventDestroy(join);
+    }
     ps.out.resize(todo.size());
     HMX_CUDA_TRY(
         cudaMemcpyAsync(ps.out.data(), d_out, sizeof(AcaOut) * todo.size(), cudaMemcpyDeviceToHost, c.stream));
@@ -551,7 +624,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     }
     if (live.empty()) continue;
     if ((rc = ps.mem.alloc(&ps.W, wo))) return fail(rc);
-    DevBuf tmp;
+    DevBuf tmp(c);
     RecDesc* d_rd;
     int32_t *d_rank, *d_flag;
     if ((rc = tmp.alloc(&d_rd, (int64_t)rd.size()))) return fail(rc);
@@ -562,17 +635,30 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     const int classes[] = {kMaxAcaCols, kRecompressSmemMax, 88, 64, 48, 32};
     const int ncls = 6;
     size_t q0 = 0;
+    // the large-K class (few long CTAs) runs on the auxiliary stream,
+    // overlapping the many short CTAs of the shared-memory classes
+    cudaEvent_t fork, join;
+    HMX_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    HMX_CUDA_TRY(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    HMX_CUDA_TRY(cudaEventRecord(fork, c.stream));
+    HMX_CUDA_TRY(cudaStreamWaitEvent(c.aux, fork, 0));
     for (int ci = 0; ci < ncls && q0 < rd.size(); ++ci) {
       const int lim_lo = ci + 1 < ncls ? classes[ci + 1] : 0;
       size_t q1 = q0;
       while (q1 < rd.size() && (rd[q1].K > lim_lo || ci == ncls - 1)) ++q1;
       if (q1 > q0) {
-        if ((rc = launch_recompress_core(c, d_rd + q0, (int64_t)(q1 - q0), rd[q0].K, cfg->eps, cfg->trunc_rule, ps.G,
+        Ctx cc = c;
+        if (ci == 0) cc.stream = c.aux;
+        if ((rc = launch_recompress_core(cc, d_rd + q0, (int64_t)(q1 - q0), rd[q0].K, cfg->eps, cfg->trunc_rule, ps.G,
                                          ps.W, d_rank + q0, d_flag + q0)))
           return fail(rc);
       }
       q0 = q1;
     }
+    HMX_CUDA_TRY(cudaEventRecord(join, c.aux));
+    HMX_CUDA_TRY(cudaStreamWaitEvent(c.stream, join, 0));
+    cudaEventDestroy(fork);
+    cudaEventDestroy(join);
     std::vector<int32_t> hr(rd.size()), hf(rd.size());
     HMX_CUDA_TRY(cudaMemcpyAsync(hr.data(), d_rank, sizeof(int32_t) * rd.size(), cudaMemcpyDeviceToHost, c.stream));
     HMX_CUDA_TRY(cudaMemcpyAsync(hf.data(), d_flag, sizeof(int32_t) * rd.size(), cudaMemcpyDeviceToHost, c.stream));
@@ -597,7 +683,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   HMX_CUDA_TRY(cudaEventRecord(ev[3], c.stream));
   tick("layout + plan");
   int32_t* d_err;
-  DevBuf tmp4;
+  DevBuf tmp4(c);
   if ((rc = tmp4.alloc(&d_err, 1))) return fail(rc);
   HMX_CUDA_TRY(cudaMemsetAsync(d_err, 0, sizeof(int32_t), c.stream));
   {
@@ -643,7 +729,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
         fd.push_back(f);
       }
       if (fd.empty()) continue;
-      DevBuf t5;
+      DevBuf t5(c);
       FormDesc* d_fd;
       int64_t* d_ts;
       if ((rc = t5.alloc(&d_fd, (int64_t)fd.size()))) return fail(rc);
@@ -913,7 +999,7 @@ int hmx_gmres(hmx_hmatrix* h, const double* b, double* x, double tol, int32_t re
   HMX_CUDA_TRY(cudaSetDevice(c.device));
   const double2* db = reinterpret_cast<const double2*>(b);
   double2* dx = reinterpret_cast<double2*>(x);
-  DevBuf tmp;
+  DevBuf tmp(c);
   int rc;
   if (mem == HMX_HOST) {
     double2 *tb, *tx;

@@ -72,6 +72,14 @@ __global__ void __launch_bounds__(256) dfma_peak(double* out, int iters, double 
 
 }  // namespace
 
+void warm_dense() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, dense_fill<1>);
+  cudaFuncGetAttributes(&a, dense_fill<3>);
+  cudaFuncGetAttributes(&a, eval_block<1>);
+  cudaFuncGetAttributes(&a, eval_block<3>);
+}
+
 int bench_dfma(Ctx& c, double* tflops) {
   double* out;
   HMX_CUDA_TRY(cudaMalloc(&out, sizeof(double)));

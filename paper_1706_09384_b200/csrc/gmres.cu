@@ -90,6 +90,16 @@ using cplx = std::complex<double>;
 
 }  // namespace
 
+void warm_gmres() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, k_dot_partial);
+  cudaFuncGetAttributes(&a, k_dot_final);
+  cudaFuncGetAttributes(&a, k_axpy_dev);
+  cudaFuncGetAttributes(&a, k_axpy);
+  cudaFuncGetAttributes(&a, k_scale);
+  cudaFuncGetAttributes(&a, k_sub);
+}
+
 int gmres_device(DeviceH& H, const double2* b, double2* x, double tol, int restart, int64_t max_iters,
                  int64_t* iters_out, std::vector<double>& history, int* converged) {
   Ctx& c = *H.ctx;
@@ -99,17 +109,18 @@ int gmres_device(DeviceH& H, const double2* b, double2* x, double tol, int resta
   *iters_out = 0;
   *converged = 0;
   double2 *Vb = nullptr, *w = nullptr, *tmp = nullptr, *part = nullptr, *hcol = nullptr;
-  HMX_CUDA_TRY(cudaMalloc(&Vb, sizeof(double2) * n * (m + 1)));
-  HMX_CUDA_TRY(cudaMalloc(&w, sizeof(double2) * n));
-  HMX_CUDA_TRY(cudaMalloc(&tmp, sizeof(double2) * n));
-  HMX_CUDA_TRY(cudaMalloc(&part, sizeof(double2) * kRedBlocks));
-  HMX_CUDA_TRY(cudaMalloc(&hcol, sizeof(double2) * (m + 2)));
+  HMX_CUDA_TRY(dev_alloc_t(c, &Vb, (size_t)n * (m + 1)));
+  HMX_CUDA_TRY(dev_alloc_t(c, &w, (size_t)n));
+  HMX_CUDA_TRY(dev_alloc_t(c, &tmp, (size_t)n));
+  HMX_CUDA_TRY(dev_alloc_t(c, &part, (size_t)kRedBlocks));
+  HMX_CUDA_TRY(dev_alloc_t(c, &hcol, (size_t)(m + 2)));
   struct Guard {
+    Ctx* c;
     std::vector<void*> p;
     ~Guard() {
-      for (void* q : p) cudaFree(q);
+      for (void* q : p) dev_free(*c, q);
     }
-  } guard{{Vb, w, tmp, part, hcol}};
+  } guard{&c, {Vb, w, tmp, part, hcol}};
   const int grid = (int)std::max<int64_t>(1, std::min<int64_t>(hmx_cdiv(n, kThreads), 4 * c.num_sms));
   Blas1 B{&c, n, part, grid};
   HMX_CUDA_TRY(cudaMemsetAsync(x, 0, sizeof(double2) * n, c.stream));

@@ -23,7 +23,9 @@ namespace hmx {
 
 struct Ctx {
   int device = 0;
+  cudaMemPool_t pool = nullptr;  // stream-ordered pool, never released to the driver between assemblies
   cudaStream_t stream = nullptr;
+  cudaStream_t aux = nullptr;  // second stream for concurrent launches inside assembly
   bool own_stream = false;
   int num_sms = 148;
   size_t l2_bytes = 0;
@@ -95,6 +97,21 @@ struct DeviceH {
   double2* h_pin_y = nullptr;
 };
 
+// capi.cu: stream-ordered device memory from the context pool (no device-wide
+// synchronisation, memory reused across assemblies instead of re-mapped)
+cudaError_t dev_alloc(Ctx& c, void** p, size_t bytes);
+void dev_free(Ctx& c, void* p);
+template <class T>
+cudaError_t dev_alloc_t(Ctx& c, T** p, size_t count) {
+  return dev_alloc(c, reinterpret_cast<void**>(p), sizeof(T) * (count ? count : 1));
+}
+// per-file kernel warm-up (forces lazy module loading at context creation)
+void warm_aca();
+void warm_recompress();
+void warm_dense();
+void warm_matvec();
+void warm_gmres();
+
 // matvec.cu
 int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& seg_level);
 int matvec_device(DeviceH& H, const double2* x_orig_dev, double2* y_orig_dev, float* phase_ms);
@@ -120,9 +137,12 @@ struct AcaOut {
   int32_t status;    // bit0 converged, bit1 max_rank, bit2 capacity overflow, bit3 fallback needed
   int32_t zero_rows;
 };
+// leaves with m + n >= kAcaClusterMin points run on a cluster of kAcaCluster CTAs
+constexpr int kAcaCluster = 8;
+constexpr int kAcaClusterMin = 1024;
 int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const AcaDesc* d_desc, const int32_t* d_order,
                int64_t nblk, int kcap_max, int m_max, double eps, double sigma3_floor, double2* U, double2* V,
-               double2* G, AcaOut* d_out);
+               double2* G, AcaOut* d_out, int cluster);
 
 // recompress.cu
 // recompress_core keeps E and the QL eigenvector matrix in shared memory up to this ACA rank

@@ -124,6 +124,14 @@ __global__ void mv_finalize(const double2* __restrict__ ylev, int64_t nlev, int6
 
 }  // namespace
 
+void warm_matvec() {
+  cudaFuncAttributes a;
+  cudaFuncGetAttributes(&a, mv_gather);
+  cudaFuncGetAttributes(&a, mv_phase1);
+  cudaFuncGetAttributes(&a, mv_phase2);
+  cudaFuncGetAttributes(&a, mv_finalize);
+}
+
 // Builds segments, levels, stream offsets and the phase-1/phase-2 work lists.
 // Requires H.table, H.rank_after (low-rank leaves), H.d, H.np.
 int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
@@ -261,17 +269,17 @@ int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
   }
   tick("host layout");
   Ctx& c = *H.ctx;
-  HMX_CUDA_TRY(cudaMalloc(&H.d_row, sizeof(double2) * std::max<int64_t>(H.row_elems, 1)));
-  HMX_CUDA_TRY(cudaMalloc(&H.d_v, sizeof(double2) * std::max<int64_t>(H.v_elems, 1)));
+  HMX_CUDA_TRY(dev_alloc_t(c, &H.d_row, (size_t)(std::max<int64_t>(H.row_elems, 1))));
+  HMX_CUDA_TRY(dev_alloc_t(c, &H.d_v, (size_t)(std::max<int64_t>(H.v_elems, 1))));
   tick("malloc row + V");
-  HMX_CUDA_TRY(cudaMalloc(&H.d_s, sizeof(double2) * std::max<int64_t>(H.s_elems, 1)));
-  HMX_CUDA_TRY(cudaMalloc(&H.d_xt, sizeof(double2) * H.n));
-  HMX_CUDA_TRY(cudaMalloc(&H.d_ylev, sizeof(double2) * H.n * H.nlevels));
+  HMX_CUDA_TRY(dev_alloc_t(c, &H.d_s, (size_t)(std::max<int64_t>(H.s_elems, 1))));
+  HMX_CUDA_TRY(dev_alloc_t(c, &H.d_xt, (size_t)(H.n)));
+  HMX_CUDA_TRY(dev_alloc_t(c, &H.d_ylev, (size_t)(H.n * H.nlevels)));
   HMX_CUDA_TRY(cudaMemsetAsync(H.d_ylev, 0, sizeof(double2) * H.n * H.nlevels, c.stream));
-  HMX_CUDA_TRY(cudaMalloc(&H.d_xio, sizeof(double2) * H.n));
-  HMX_CUDA_TRY(cudaMalloc(&H.d_yio, sizeof(double2) * H.n));
-  HMX_CUDA_TRY(cudaMalloc(&H.d_job1, sizeof(MvJob1) * std::max<int64_t>(H.njob1, 1)));
-  HMX_CUDA_TRY(cudaMalloc(&H.d_tile2, sizeof(MvTile2) * std::max<int64_t>(H.ntile2, 1)));
+  HMX_CUDA_TRY(dev_alloc_t(c, &H.d_xio, (size_t)(H.n)));
+  HMX_CUDA_TRY(dev_alloc_t(c, &H.d_yio, (size_t)(H.n)));
+  HMX_CUDA_TRY(dev_alloc_t(c, &H.d_job1, (size_t)(std::max<int64_t>(H.njob1, 1))));
+  HMX_CUDA_TRY(dev_alloc_t(c, &H.d_tile2, (size_t)(std::max<int64_t>(H.ntile2, 1))));
   if (H.njob1)
     HMX_CUDA_TRY(cudaMemcpyAsync(H.d_job1, jobs.data(), sizeof(MvJob1) * H.njob1, cudaMemcpyHostToDevice, c.stream));
   if (H.ntile2)
