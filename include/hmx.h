@@ -132,7 +132,7 @@ int hmx_hmatrix_load(hmx_ctx* ctx, int32_t d, int64_t n_points, const int64_t* p
                      const int64_t* ranks, const double* const* a, const double* const* b, hmx_hmatrix** out);
 int hmx_hmatrix_stats(const hmx_hmatrix* h, hmx_stats* st);
 /* per leaf: ACA steps, rank before / after recompression, flags (bit0 converged, bit1 max_rank,
- * bit3 fallback, bit4 Cholesky regularised) */
+ * bit3 fallback, bit4 Cholesky regularised, bit5 QL eigen fallback, bit6 QL not converged) */
 int hmx_hmatrix_block_info(const hmx_hmatrix* h, int64_t* steps, int64_t* rank_before, int64_t* rank_after,
                            int32_t* flags);
 /* copy leaf b out (layouts as in hmx_hmatrix_load) */

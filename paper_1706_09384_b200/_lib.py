@@ -12,7 +12,7 @@ import numpy as np
 
 from .errors import STATUS_EXCEPTIONS
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhmx.so")
+LIB_PATH = os.environ.get("HMX_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libhmx.so")
 
 i32, i64, f64, u64 = C.c_int32, C.c_int64, C.c_double, C.c_uint64
 P = C.c_void_p

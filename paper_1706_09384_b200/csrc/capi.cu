@@ -670,6 +670,8 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
         H.flags[b] |= 16;
         H.n_regularized++;
       }
+      if (hf[q] & 4) H.flags[b] |= 32;  // eigenvectors from the QL fallback
+      if (hf[q] & 2) H.flags[b] |= 64;  // QL did not converge
     }
   }
   HMX_CUDA_TRY(cudaEventRecord(ev[2], c.stream));

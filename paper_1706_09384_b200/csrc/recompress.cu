@@ -55,6 +55,76 @@ struct Scalars {
   int done, istop, m, fail;
 };
 
+// CTA-wide complex GEMM through shared-memory tiles (32 x 32 outputs, k-chunks
+// of 16): C (M x N, ldc) = op(A) (M x Kd) * op(B) (Kd x N), column-major, with
+// op(A)(i,k) = ACT ? conj(A(k,i)) : A(i,k) and op(B)(k,j) = BCT ? conj(B(j,k)) : B(k,j).
+// Each thread owns (32 / (NT/16)) x 2 outputs; tile holds 2 x 16 x 33 complex.
+constexpr int kGemmTile = 2 * 16 * 33;
+template <int NT, bool ACT, bool BCT>
+__device__ void cta_zgemm(int M, int N, int Kd, const double2* A, int lda, const double2* B, int ldb, double2* C,
+                          int ldc, double2* tile) {
+  constexpr int BM = 32, BN = 32, BK = 16, RS = NT / 16, RPT = BM / RS;
+  double2* As = tile;              // [BK][BM + 1]
+  double2* Bs = tile + BK * (BM + 1);  // [BK][BN + 1]
+  const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
+  for (int i0 = 0; i0 < M; i0 += BM)
+    for (int j0 = 0; j0 < N; j0 += BN) {
+      double2 acc[RPT][2];
+#pragma unroll
+      for (int q = 0; q < RPT; ++q) acc[q][0] = acc[q][1] = cmk(0.0, 0.0);
+      for (int k0 = 0; k0 < Kd; k0 += BK) {
+        for (int t = tid; t < BM * BK; t += NT) {
+          int ii, kk;
+          if (ACT) {
+            kk = t % BK;
+            ii = t / BK;
+          } else {
+            ii = t % BM;
+            kk = t / BM;
+          }
+          const int gi = i0 + ii, gk = k0 + kk;
+          double2 v = cmk(0.0, 0.0);
+          if (gi < M && gk < Kd) v = ACT ? cconj(A[gk + (int64_t)gi * lda]) : A[gi + (int64_t)gk * lda];
+          As[kk * (BM + 1) + ii] = v;
+        }
+        for (int t = tid; t < BK * BN; t += NT) {
+          int kk, jj;
+          if (BCT) {
+            jj = t % BN;
+            kk = t / BN;
+          } else {
+            kk = t % BK;
+            jj = t / BK;
+          }
+          const int gk = k0 + kk, gj = j0 + jj;
+          double2 v = cmk(0.0, 0.0);
+          if (gk < Kd && gj < N) v = BCT ? cconj(B[gj + (int64_t)gk * ldb]) : B[gk + (int64_t)gj * ldb];
+          Bs[kk * (BN + 1) + jj] = v;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = 0; kk < BK; ++kk) {
+          const double2 b0 = Bs[kk * (BN + 1) + tx], b1 = Bs[kk * (BN + 1) + tx + 16];
+#pragma unroll
+          for (int q = 0; q < RPT; ++q) {
+            const double2 a = As[kk * (BM + 1) + ty + q * RS];
+            acc[q][0] = cfma(a, b0, acc[q][0]);
+            acc[q][1] = cfma(a, b1, acc[q][1]);
+          }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int q = 0; q < RPT; ++q)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int gi = i0 + ty + q * RS, gj = j0 + tx + 16 * h;
+          if (gi < M && gj < N) C[gi + (int64_t)gj * ldc] = acc[q][h];
+        }
+    }
+  __syncthreads();
+}
+
 // Householder reduction of the Hermitian E (K x K, ld K, full storage) to a
 // real symmetric tridiagonal (d, e): E = Q T Q^H, Q = H_0 ... H_{K-2},
 // H_k = I - tau_k v_k v_k^H (LAPACK zhetd2 / zlarfg conventions, beta real).
@@ -228,6 +298,193 @@ __device__ void tridiag_ql(double* d, double* e, double* Z, int ldz, int K, doub
   }
 }
 
+// ---- fast tridiagonal eigen-solver: bisection + twisted factorisations ----------
+// All K eigenvalues of the real symmetric tridiagonal (d, e) by bisection on
+// Sturm counts (thread t finds the t-th smallest; parallel, no serial chain);
+// eigenvectors of the r kept eigenvalues from the twisted LDL^T / UDU^T
+// factorisation of T - lambda I (one thread per vector, Dhillon's getvec
+// without the RRR machinery), orthonormalised by classical Gram-Schmidt twice
+// in descending-eigenvalue order.  A vector that is mostly in the span of the
+// previous ones (near-degenerate cluster) makes the caller fall back to QL.
+HMX_D int sturm_count(const double* d, const double* e2, int K, double x, double pivmin) {
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  int cnt = q < 0.0;
+  for (int i = 1; i < K; ++i) {
+    q = (d[i] - x) - e2[i - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    cnt += q < 0.0;
+  }
+  return cnt;
+}
+
+// lam_asc[j] = j-th smallest eigenvalue
+template <int NT>
+__device__ void bisect_all(const double* d, const double* e, double* e2, int K, double* lam_asc, double* red,
+                           double& pivmin_out) {
+  const int tid = threadIdx.x;
+  double lo = INFINITY, hi = -INFINITY, emax2 = 0.0;
+  for (int i = tid; i < K; i += NT) {
+    const double ei = i + 1 < K ? fabs(e[i]) : 0.0, em = i > 0 ? fabs(e[i - 1]) : 0.0;
+    lo = fmin(lo, d[i] - ei - em);
+    hi = fmax(hi, d[i] + ei + em);
+    if (i + 1 < K) {
+      e2[i] = e[i] * e[i];
+      emax2 = fmax(emax2, e2[i]);
+    }
+  }
+  // block min / max via shared memory
+  __shared__ double s_lo[NT / 32], s_hi[NT / 32], s_e2[NT / 32];
+  {
+    double a = lo, b = hi, c = emax2;
+    for (int o = 16; o > 0; o >>= 1) {
+      a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+      c = fmax(c, __shfl_xor_sync(0xffffffffu, c, o));
+    }
+    if ((tid & 31) == 0) {
+      s_lo[tid >> 5] = a;
+      s_hi[tid >> 5] = b;
+      s_e2[tid >> 5] = c;
+    }
+    __syncthreads();
+    a = s_lo[0];
+    b = s_hi[0];
+    c = s_e2[0];
+    for (int w = 1; w < NT / 32; ++w) {
+      a = fmin(a, s_lo[w]);
+      b = fmax(b, s_hi[w]);
+      c = fmax(c, s_e2[w]);
+    }
+    lo = a;
+    hi = b;
+    emax2 = c;
+  }
+  const double pivmin = 2.2250738585072014e-308 * fmax(1.0, emax2) * 4.0;
+  pivmin_out = pivmin;
+  const double span = fmax(fabs(lo), fabs(hi));
+  lo -= 2.2e-16 * span * K + pivmin;
+  hi += 2.2e-16 * span * K + pivmin;
+  for (int j = tid; j < K; j += NT) {
+    double a = lo, b = hi;
+    for (int it = 0; it < 80; ++it) {
+      if (b - a <= 4.4e-16 * fmax(fabs(a), fabs(b)) + pivmin) break;
+      const double mid = 0.5 * (a + b);
+      if (sturm_count(d, e2, K, mid, pivmin) > j)
+        b = mid;
+      else
+        a = mid;
+    }
+    lam_asc[j] = 0.5 * (a + b);
+  }
+  __syncthreads();
+}
+
+// eigenvector of T for eigenvalue lam into Z column (real parts of zc[0..K)),
+// scratch: K doubles (U multipliers)
+HMX_D void twisted_vector(const double* d, const double* e, int K, double lam, double pivmin, double2* zc,
+                          double* scratch) {
+  // forward D+ / L, stored as (L_i, D+_i) in zc
+  double dp = d[0] - lam;
+  for (int i = 0; i + 1 < K; ++i) {
+    if (fabs(dp) < pivmin) dp = dp < 0.0 ? -pivmin : pivmin;
+    const double L = e[i] / dp;
+    zc[i] = cmk(L, dp);
+    dp = (d[i + 1] - lam) - L * e[i];
+  }
+  if (fabs(dp) < pivmin) dp = dp < 0.0 ? -pivmin : pivmin;
+  zc[K - 1] = cmk(0.0, dp);
+  // backward D- / U, twist index k = argmin |gamma_k|
+  double dm = d[K - 1] - lam;
+  double best = fabs(zc[K - 1].y);
+  int k = K - 1;
+  for (int i = K - 1; i >= 1; --i) {
+    if (fabs(dm) < pivmin) dm = dm < 0.0 ? -pivmin : pivmin;
+    const double U = e[i - 1] / dm;
+    scratch[i] = U;
+    dm = (d[i - 1] - lam) - U * e[i - 1];
+    const double g = fabs(zc[i - 1].y + dm - (d[i - 1] - lam));
+    if (g < best) {
+      best = g;
+      k = i - 1;
+    }
+  }
+  // z_k = 1, z_i = -L_i z_{i+1} (i < k), z_i = -U_i z_{i-1} (i > k)
+  double z = 1.0, nrm = 1.0;
+  for (int i = k - 1; i >= 0; --i) {
+    z = -zc[i].x * z;
+    zc[i] = cmk(z, 0.0);
+    nrm = fma(z, z, nrm);
+  }
+  zc[k] = cmk(1.0, 0.0);
+  z = 1.0;
+  for (int i = k + 1; i < K; ++i) {
+    z = -scratch[i] * z;
+    zc[i] = cmk(z, 0.0);
+    nrm = fma(z, z, nrm);
+  }
+  const double inv = rsqrt(nrm);
+  for (int i = 0; i < K; ++i) zc[i].x *= inv;
+}
+
+// classical Gram-Schmidt twice on the real parts of the r columns of Zr (ld K);
+// returns false if a column is (numerically) in the span of its predecessors
+template <int NT>
+__device__ bool cgs2_columns(double2* Zr, int K, int r, double* h, double* red) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  __shared__ int s_bad;
+  if (tid == 0) s_bad = 0;
+  for (int c = 0; c < r; ++c) {
+    double2* zc = Zr + (int64_t)c * K;
+    for (int pass = 0; pass < 2; ++pass) {
+      for (int j = warp; j < c; j += NT / 32) {
+        const double2* zj = Zr + (int64_t)j * K;
+        double acc = 0.0;
+        for (int i = lane; i < K; i += 32) acc = fma(zj[i].x, zc[i].x, acc);
+        acc = warp_sum(acc);
+        if (lane == 0) h[j] = acc;
+      }
+      __syncthreads();
+      double nrm = 0.0;
+      for (int i = tid; i < K; i += NT) {
+        double v = zc[i].x;
+        for (int j = 0; j < c; ++j) v = fma(-h[j], Zr[i + (int64_t)j * K].x, v);
+        zc[i].x = v;
+        nrm = fma(v, v, nrm);
+      }
+      nrm = block_sum<NT>(nrm, red);
+      if (pass == 0 && tid == 0 && !(nrm > 0.25)) s_bad = 1;  // lost > 87% to earlier vectors
+      const double inv = nrm > 0.0 ? rsqrt(nrm) : 0.0;
+      for (int i = tid; i < K; i += NT) zc[i].x *= inv;
+      __syncthreads();
+    }
+  }
+  return s_bad == 0;
+}
+
+// truncation rank (oracle/lowrank.py truncation_rank) from eigenvalues
+// lam[ordr[k]] in descending order; thread 0 writes r
+HMX_D void recompress_truncate(const double* lam, const int* ordr, int K, double eps, int rule, int& r_out) {
+  if (threadIdx.x != 0) return;
+  int r = 0;
+  const double l1 = lam[ordr[0]];
+  if (l1 > 0.0) {
+    if (rule == 1) {
+      for (int k = 0; k < K; ++k) r += lam[ordr[k]] > eps * eps * l1;
+    } else {
+      double total = 0.0;
+      for (int k = K - 1; k >= 0; --k) total += lam[ordr[k]];
+      r = K;
+      double acc = 0.0;
+      for (int k = K - 1; k >= 0; --k) {  // smallest r with sum_{k >= r} lam <= eps^2 total
+        acc += lam[ordr[k]];
+        if (acc <= eps * eps * total) r = k;
+      }
+    }
+  }
+  r_out = r;
+}
+
 // Workspace per leaf, 6 K x K complex slots: 0 R, 1 T then L_r, 2 E (global
 // variant), 3 Z (real, global variant), 4-5 W_U | W_V.
 template <bool SMEM, int NT>
@@ -270,9 +527,10 @@ __global__ void __launch_bounds__(NT) recompress_core(const RecDesc* __restrict_
   double2* E;
   double* Z;
   int ldz;
+  double2* gtile = reinterpret_cast<double2*>(ordr + K + (K & 1) + 2);
+  gtile = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(gtile) + 15) & ~uintptr_t(15));
   if (SMEM) {
-    E = reinterpret_cast<double2*>(ordr + K + (K & 1) + 2);
-    E = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(E) + 15) & ~uintptr_t(15));
+    E = gtile;  // no GEMM tiles in the shared-memory variant
     Z = reinterpret_cast<double*>(E);  // overlays E after the reduction (8 K (K+1) <= 16 K^2 bytes)
     ldz = K + 1;
   } else {
@@ -323,20 +581,26 @@ __global__ void __launch_bounds__(NT) recompress_core(const RecDesc* __restrict_
   }
   __syncthreads();
   // ---- T = R G_U (B), E = T R^H --------------------------------------------------
-  for (int t = tid; t < K * K; t += NT) {
-    const int i = t % K, j = t / K;
-    double2 s = cmk(0.0, 0.0);
-    for (int k = i; k < K; ++k) s = cfma(A[i + (int64_t)k * K], GU[k + (int64_t)j * kcap], s);
-    B[t] = s;
+  if constexpr (!SMEM) {
+    // large K: shared-memory tiled products (the naive loops are L2-latency bound)
+    cta_zgemm<NT, false, false>(K, K, K, A, K, GU, kcap, B, K, gtile);
+    cta_zgemm<NT, false, true>(K, K, K, B, K, A, K, E, K, gtile);
+  } else {
+    for (int t = tid; t < K * K; t += NT) {
+      const int i = t % K, j = t / K;
+      double2 s = cmk(0.0, 0.0);
+      for (int k = i; k < K; ++k) s = cfma(A[i + (int64_t)k * K], GU[k + (int64_t)j * kcap], s);
+      B[t] = s;
+    }
+    __syncthreads();
+    for (int t = tid; t < K * K; t += NT) {
+      const int i = t % K, j = t / K;
+      double2 s = cmk(0.0, 0.0);
+      for (int k = j; k < K; ++k) s = cfma_cj(B[i + (int64_t)k * K], A[j + (int64_t)k * K], s);
+      E[i + (int64_t)j * K] = s;
+    }
+    __syncthreads();
   }
-  __syncthreads();
-  for (int t = tid; t < K * K; t += NT) {
-    const int i = t % K, j = t / K;
-    double2 s = cmk(0.0, 0.0);
-    for (int k = j; k < K; ++k) s = cfma_cj(B[i + (int64_t)k * K], A[j + (int64_t)k * K], s);
-    E[i + (int64_t)j * K] = s;
-  }
-  __syncthreads();
   for (int t = tid; t < K * K; t += NT) {  // Hermitian symmetrise (roundoff)
     const int i = t % K, j = t / K;
     if (i < j) {
@@ -352,58 +616,62 @@ __global__ void __launch_bounds__(NT) recompress_core(const RecDesc* __restrict_
   // ---- eigen-decomposition E = Q Z diag(lam) Z^T Q^H --------------------------------
   tridiagonalize<NT>(E, K, d, e, tau, vbuf, pbuf, S, red);
   double2* Hv = E;  // Householder vectors v_k = Hv(k+1:, k)
-  if (SMEM) {
-    // keep the reflectors in L2 (workspace slot 2) and let the QL eigenvector
-    // matrix Z reuse E's shared memory: 16 K^2 bytes of smem per CTA in total
-    Hv = A + 2 * KK;
-    for (int t = tid; t < K * K; t += NT) {
-      const int i = t % K, j = t / K;
-      if (i > j) Hv[t] = E[t];
+  // fast path: bisection eigenvalues + twisted eigenvectors (rc: e^2 scratch)
+  double pivmin = 0.0;
+  bisect_all<NT>(d, e, rc, K, rs, red, pivmin);  // rs = ascending eigenvalues
+  for (int i = tid; i < K; i += NT) {
+    lam[i] = fmax(rs[K - 1 - i], 0.0);  // descending
+    ordr[i] = i;
+  }
+  __syncthreads();
+  recompress_truncate(lam, ordr, K, eps, rule, s_r);
+  __syncthreads();
+  int r = s_r;
+  bool fast_ok = true;
+  if (r > 0) {
+    double* uscr = reinterpret_cast<double*>(Wuv);  // K doubles per kept vector
+    for (int c2 = tid; c2 < r; c2 += NT)
+      twisted_vector(d, e, K, rs[K - 1 - c2], pivmin, B + (int64_t)c2 * K, uscr + (int64_t)c2 * K);
+    __syncthreads();
+    fast_ok = cgs2_columns<NT>(B, K, r, reinterpret_cast<double*>(pbuf), red);
+  }
+  if (!fast_ok) {
+    // near-degenerate eigenvalues: implicit QL with accumulated vectors
+    if (SMEM) {
+      // reflectors to L2 (workspace slot 2); Z reuses E's shared memory
+      Hv = A + 2 * KK;
+      for (int t = tid; t < K * K; t += NT) {
+        const int i = t % K, j = t / K;
+        if (i > j) Hv[t] = E[t];
+      }
+      __syncthreads();
+    }
+    tridiag_ql<NT>(d, e, Z, ldz, K, rc, rs, S);
+    if (tid == 0) s_flag |= S.fail ? 6 : 4;
+    for (int i = tid; i < K; i += NT) lam[i] = fmax(d[i], 0.0);
+    __syncthreads();
+    for (int i = tid; i < K; i += NT) {
+      int rk = 0;
+      const double li = lam[i];
+      for (int j = 0; j < K; ++j) rk += (lam[j] > li) || (lam[j] == li && j < i);
+      ordr[rk] = i;
+    }
+    __syncthreads();
+    recompress_truncate(lam, ordr, K, eps, rule, s_r);
+    __syncthreads();
+    r = s_r;
+    for (int t = tid; t < K * r; t += NT) {
+      const int i = t % K, c2 = t / K;
+      B[t] = cmk(Z[(int64_t)i * ldz + ordr[c2]], 0.0);
     }
     __syncthreads();
   }
-  tridiag_ql<NT>(d, e, Z, ldz, K, rc, rs, S);
-  if (tid == 0 && S.fail) s_flag |= 2;
-  for (int i = tid; i < K; i += NT) lam[i] = fmax(d[i], 0.0);
-  __syncthreads();
-  for (int i = tid; i < K; i += NT) {
-    int rk = 0;
-    const double li = lam[i];
-    for (int j = 0; j < K; ++j) rk += (lam[j] > li) || (lam[j] == li && j < i);
-    ordr[rk] = i;
-  }
-  __syncthreads();
   if (tid == 0) {
-    // truncation (oracle/lowrank.py truncation_rank)
-    int r = 0;
-    const double l1 = lam[ordr[0]];
-    if (l1 > 0.0) {
-      if (rule == 1) {
-        for (int k = 0; k < K; ++k) r += lam[ordr[k]] > eps * eps * l1;
-      } else {
-        double total = 0.0;
-        for (int k = K - 1; k >= 0; --k) total += lam[ordr[k]];
-        r = K;
-        double acc = 0.0;
-        for (int k = K - 1; k >= 0; --k) {  // smallest r with sum_{k >= r} lam <= eps^2 total
-          acc += lam[ordr[k]];
-          if (acc <= eps * eps * total) r = k;
-        }
-      }
-    }
-    s_r = r;
     rank_out[blockIdx.x] = r;
     flags_out[blockIdx.x] = s_flag;
   }
-  __syncthreads();
-  const int r = s_r;
   if (r == 0) return;
-  // ---- L_r = Q Z(:, ord[0:r]) : B (K x r) ---------------------------------------------
-  for (int t = tid; t < K * r; t += NT) {
-    const int i = t % K, c = t / K;
-    B[t] = cmk(Z[(int64_t)i * ldz + ordr[c]], 0.0);
-  }
-  __syncthreads();
+  // ---- L_r = Q Z_r : B (K x r) ------------------------------------------------------
   for (int k = K - 2; k >= 0; --k) {
     const double2 tk = tau[k];
     if (tk.x == 0.0 && tk.y == 0.0) continue;
@@ -427,11 +695,16 @@ __global__ void __launch_bounds__(NT) recompress_core(const RecDesc* __restrict_
   // ---- W_U = R^H L_r S^-1/2, W_V = R^{-1} L_r S^1/2 ------------------------------------
   double2* Wu = Wuv;
   double2* Wv = Wuv + (int64_t)K * r;
-  for (int t = tid; t < K * r; t += NT) {
-    const int i = t % K, c = t / K;
-    double2 s = cmk(0.0, 0.0);
-    for (int k = 0; k <= i; ++k) s = cfma_ca(A[k + (int64_t)i * K], B[k + (int64_t)c * K], s);
-    Wu[t] = cscale(s, 1.0 / sqrt(sqrt(lam[ordr[c]])));
+  if constexpr (!SMEM) {
+    cta_zgemm<NT, true, false>(K, r, K, A, K, B, K, Wu, K, gtile);
+    for (int t = tid; t < K * r; t += NT) Wu[t] = cscale(Wu[t], 1.0 / sqrt(sqrt(lam[ordr[t / K]])));
+  } else {
+    for (int t = tid; t < K * r; t += NT) {
+      const int i = t % K, c = t / K;
+      double2 s = cmk(0.0, 0.0);
+      for (int k = 0; k <= i; ++k) s = cfma_ca(A[k + (int64_t)i * K], B[k + (int64_t)c * K], s);
+      Wu[t] = cscale(s, 1.0 / sqrt(sqrt(lam[ordr[c]])));
+    }
   }
   // W_V: R X = L_r by column-oriented back substitution, parallel over (row, column)
   for (int t = tid; t < K * r; t += NT) Wv[t] = B[t];
@@ -543,9 +816,10 @@ int launch_recompress_core(Ctx& c, const RecDesc* d_desc, int64_t nblk, int kmax
       recompress_core<true, 256><<<(unsigned)nblk, 256, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
     }
   } else {
+    const size_t smem = vec + sizeof(double2) * kGemmTile;
     HMX_CUDA_TRY(
-        cudaFuncSetAttribute(recompress_core<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)vec));
-    recompress_core<false, 256><<<(unsigned)nblk, 256, vec, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
+        cudaFuncSetAttribute(recompress_core<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    recompress_core<false, 256><<<(unsigned)nblk, 256, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
   }
   HMX_CUDA_TRY(cudaGetLastError());
   return HMX_OK;
