@@ -580,24 +580,27 @@ void warm_aca() {
   cudaFuncGetAttributes(&a, aca_kernel<1, 0, 512, 1, 1>);
   cudaFuncGetAttributes(&a, aca_kernel<3, 1, 512, 1, 1>);
   cudaFuncGetAttributes(&a, aca_kernel<3, 2, 512, 1, 1>);
+  cudaFuncGetAttributes(&a, aca_kernel<1, 0, 128, 4, 1>);
+  cudaFuncGetAttributes(&a, aca_kernel<3, 1, 128, 4, 1>);
+  cudaFuncGetAttributes(&a, aca_kernel<3, 2, 128, 4, 1>);
 }
 
 int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const AcaDesc* d_desc, const int32_t* d_order,
                int64_t nblk, int kcap_max, int m_max, double eps, double sigma3_floor, double2* U, double2* V,
-               double2* G, AcaOut* d_out, int cluster) {
+               double2* G, AcaOut* d_out, int variant) {
   if (nblk == 0) return HMX_OK;
-  const int CSv = cluster > 1 ? cluster : 1;
+  // variant: kAcaWide (512 threads, one CTA per SM: the factors of large
+  // leaves stay hot in L1 / the SM's L2 share; 2-3 CTAs/SM measured 1.4-1.8x
+  // slower), kAcaNarrow (128 threads, 4 CTAs per SM: small leaves are latency
+  // bound and use few threads per step), >1: cluster of that many CTAs per leaf.
+  const int CSv = variant > 1 ? variant : 1;
+  const int nt = variant == kAcaNarrow ? 128 : 512;
   size_t smem = sizeof(double2) * (CSv > 1 ? 4 : 2) * (size_t)d * kcap_max + (size_t)((m_max + 15) / 16) * 16;
-  // One resident CTA per SM keeps each leaf's factors hot in L1 (the ACA passes
-  // re-read them every step: 2-3 CTAs/SM measured 1.4-1.8x slower); 512 threads
-  // (128 registers) give that CTA 16 warps of memory parallelism.  Large
-  // leaves run on a cluster of kAcaCluster CTAs (SMs) so they do not set the
-  // critical path of the whole launch.
   auto go = [&](auto kern) -> int {
     HMX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3((unsigned)(nblk * CSv));
-    cfg.blockDim = dim3(512);
+    cfg.blockDim = dim3(nt);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = c.stream;
     cudaLaunchAttribute attr[1];
@@ -613,26 +616,17 @@ int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const 
   };
   int rc;
   if (CSv == 8) {
-    if (P.kind == 0)
-      rc = go(aca_kernel<1, 0, 512, 1, 8>);
-    else if (P.kind == 1)
-      rc = go(aca_kernel<3, 1, 512, 1, 8>);
-    else
-      rc = go(aca_kernel<3, 2, 512, 1, 8>);
+    rc = P.kind == 0 ? go(aca_kernel<1, 0, 512, 1, 8>)
+                     : (P.kind == 1 ? go(aca_kernel<3, 1, 512, 1, 8>) : go(aca_kernel<3, 2, 512, 1, 8>));
   } else if (CSv == 4) {
-    if (P.kind == 0)
-      rc = go(aca_kernel<1, 0, 512, 1, 4>);
-    else if (P.kind == 1)
-      rc = go(aca_kernel<3, 1, 512, 1, 4>);
-    else
-      rc = go(aca_kernel<3, 2, 512, 1, 4>);
+    rc = P.kind == 0 ? go(aca_kernel<1, 0, 512, 1, 4>)
+                     : (P.kind == 1 ? go(aca_kernel<3, 1, 512, 1, 4>) : go(aca_kernel<3, 2, 512, 1, 4>));
+  } else if (variant == kAcaNarrow) {
+    rc = P.kind == 0 ? go(aca_kernel<1, 0, 128, 4, 1>)
+                     : (P.kind == 1 ? go(aca_kernel<3, 1, 128, 4, 1>) : go(aca_kernel<3, 2, 128, 4, 1>));
   } else {
-    if (P.kind == 0)
-      rc = go(aca_kernel<1, 0, 512, 1, 1>);
-    else if (P.kind == 1)
-      rc = go(aca_kernel<3, 1, 512, 1, 1>);
-    else
-      rc = go(aca_kernel<3, 2, 512, 1, 1>);
+    rc = P.kind == 0 ? go(aca_kernel<1, 0, 512, 1, 1>)
+                     : (P.kind == 1 ? go(aca_kernel<3, 1, 512, 1, 1>) : go(aca_kernel<3, 2, 512, 1, 1>));
   }
   if (rc) return rc;
   HMX_CUDA_TRY(cudaGetLastError());

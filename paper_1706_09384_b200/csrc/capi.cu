@@ -39,16 +39,58 @@ struct hmx_ctx {
 };
 
 namespace hmx {
+void release_cache(Ctx& c) {
+  std::lock_guard<std::mutex> lk(c.mem_mu);
+  for (auto& kv : c.cache) cudaFree(kv.second);
+  c.cache.clear();
+  c.cached_bytes = 0;
+}
 cudaError_t dev_alloc(Ctx& c, void** p, size_t bytes) {
   if (c.pool) return cudaMallocFromPoolAsync(p, bytes, c.pool, c.stream);
-  return cudaMalloc(p, bytes);
+  // 2 MiB granularity so that repeated assemblies hit the cache
+  const size_t gran = bytes >= (1u << 20) ? (size_t(2) << 20) : 256;
+  bytes = (bytes + gran - 1) / gran * gran;
+  {
+    std::lock_guard<std::mutex> lk(c.mem_mu);
+    auto it = c.cache.lower_bound(bytes);
+    if (it != c.cache.end() && it->first <= 2 * bytes + (size_t(4) << 20)) {
+      *p = it->second;
+      c.live[*p] = it->first;
+      c.cached_bytes -= it->first;
+      c.cache.erase(it);
+      return cudaSuccess;
+    }
+  }
+  cudaError_t e = cudaMalloc(p, bytes);
+  if (e == cudaErrorMemoryAllocation) {  // give the cached blocks back and retry once
+    cudaGetLastError();
+    release_cache(c);
+    e = cudaMalloc(p, bytes);
+  }
+  if (e == cudaSuccess) {
+    std::lock_guard<std::mutex> lk(c.mem_mu);
+    c.live[*p] = bytes;
+  }
+  return e;
 }
 void dev_free(Ctx& c, void* p) {
   if (!p) return;
-  if (c.pool)
+  if (c.pool) {
     cudaFreeAsync(p, c.stream);
-  else
+    return;
+  }
+  // stream-ordered reuse: every later use of a cached block is issued on the
+  // context stream after the work that used it (assembly joins its auxiliary
+  // stream before freeing), so no device synchronisation is needed here
+  std::lock_guard<std::mutex> lk(c.mem_mu);
+  auto it = c.live.find(p);
+  if (it == c.live.end()) {
     cudaFree(p);
+    return;
+  }
+  c.cache.emplace(it->second, p);
+  c.cached_bytes += it->second;
+  c.live.erase(it);
 }
 }  // namespace hmx
 struct hmx_tree {
@@ -169,6 +211,14 @@ int validate_table(const int64_t* table, int64_t nb, int64_t np) {
   return HMX_OK;
 }
 
+// launches issued inside this scope go to the context's auxiliary stream
+struct OnAux {
+  Ctx& c;
+  cudaStream_t saved;
+  explicit OnAux(Ctx& cc) : c(cc), saved(cc.stream) { c.stream = c.aux; }
+  ~OnAux() { c.stream = saved; }
+};
+
 struct AcaPass {
   explicit AcaPass(Ctx& c) : mem(c) {}
   DevBuf mem;
@@ -246,6 +296,7 @@ int hmx_ctx_release_cache(hmx_ctx* ctx) {
   HMX_CUDA_TRY(cudaSetDevice(ctx->c.device));
   HMX_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
   if (ctx->c.pool) HMX_CUDA_TRY(cudaMemPoolTrimTo(ctx->c.pool, 0));
+  release_cache(ctx->c);
   return HMX_OK;
 }
 
@@ -261,6 +312,7 @@ int hmx_ctx_destroy(hmx_ctx* ctx) {
   if (ctx->c.own_stream && ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
   if (ctx->c.aux) cudaStreamDestroy(ctx->c.aux);
   if (ctx->c.pool) cudaMemPoolDestroy(ctx->c.pool);
+  release_cache(ctx->c);
   delete ctx;
   return HMX_OK;
 }
@@ -539,23 +591,47 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       const char* e_min = std::getenv("HMX_ACA_CLUSTER_MIN");
       const int cs = e_cs ? std::atoi(e_cs) : 1;  // clusters measured slower
       const int64_t cmin = e_min ? std::atoll(e_min) : kAcaClusterMin;
-      size_t nbig = 0;
+      const char* e_nm = std::getenv("HMX_ACA_NARROW_MAX");
+      const int64_t nmax = e_nm ? std::atoll(e_nm) : kAcaNarrowMax;
+      size_t nbig = 0, nwide = 0;
       while (cs > 1 && nbig < todo.size() && rows_of(todo[nbig]) + cols_of(todo[nbig]) >= cmin) ++nbig;
+      nwide = nbig;
+      while (nwide < todo.size() && rows_of(todo[nwide]) + cols_of(todo[nwide]) >= nmax) ++nwide;
+      auto sub_max = [&](size_t q0, size_t q1, int& kc, int& mm) {
+        kc = 1;
+        mm = 1;
+        for (size_t q = q0; q < q1; ++q) {
+          kc = std::max<int>(kc, ps.desc[q].kcap);
+          mm = std::max<int>(mm, ps.desc[q].m);
+        }
+      };
       const double s3f = cfg->sigma3_floor > 0 ? cfg->sigma3_floor : 1e-12;
       cudaEvent_t fork, join;
       HMX_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
       HMX_CUDA_TRY(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
       HMX_CUDA_TRY(cudaEventRecord(fork, c.stream));
       HMX_CUDA_TRY(cudaStreamWaitEvent(c.aux, fork, 0));
-      Ctx caux = c;
-      caux.stream = c.aux;
-      if (nbig && (rc = launch_aca(caux, d, P, pts.soa, d_desc, d_order, (int64_t)nbig, ps.kcap_max, (int)m_max_all,
-                                   cfg->eps, s3f, ps.U, ps.V, ps.G, d_out, cs)))
-        return fail(rc);
-      if (todo.size() > nbig &&
-          (rc = launch_aca(c, d, P, pts.soa, d_desc, d_order + nbig, (int64_t)(todo.size() - nbig), ps.kcap_max,
-                           (int)m_max_all, cfg->eps, s3f, ps.U, ps.V, ps.G, d_out, 1)))
-        return fail(rc);
+      int kc, mm;
+      // large leaves (clusters, then wide CTAs) on the auxiliary stream, the
+      // many small leaves (narrow CTAs) concurrently on the main stream
+      if (nbig) {
+        sub_max(0, nbig, kc, mm);
+        if ((rc = [&] { OnAux on(c); return launch_aca(c, d, P, pts.soa, d_desc, d_order, (int64_t)nbig, kc, mm, cfg->eps, s3f, ps.U, ps.V,
+                             ps.G, d_out, cs); }()))
+          return fail(rc);
+      }
+      if (nwide > nbig) {
+        sub_max(nbig, nwide, kc, mm);
+        if ((rc = [&] { OnAux on(c); return launch_aca(c, d, P, pts.soa, d_desc, d_order + nbig, (int64_t)(nwide - nbig), kc, mm, cfg->eps,
+                             s3f, ps.U, ps.V, ps.G, d_out, kAcaWide); }()))
+          return fail(rc);
+      }
+      if (todo.size() > nwide) {
+        sub_max(nwide, todo.size(), kc, mm);
+        if ((rc = launch_aca(c, d, P, pts.soa, d_desc, d_order + nwide, (int64_t)(todo.size() - nwide), kc, mm,
+                             cfg->eps, s3f, ps.U, ps.V, ps.G, d_out, kAcaNarrow)))
+          return fail(rc);
+      }
       HMX_CUDA_TRY(cudaEventRecord(join, c.aux));
       HMX_CUDA_TRY(cudaStreamWaitEvent(c.stream, join, 0));
       cudaEventDestroy(fork);
@@ -647,11 +723,12 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       size_t q1 = q0;
       while (q1 < rd.size() && (rd[q1].K > lim_lo || ci == ncls - 1)) ++q1;
       if (q1 > q0) {
-        Ctx cc = c;
-        if (ci == 0) cc.stream = c.aux;
-        if ((rc = launch_recompress_core(cc, d_rd + q0, (int64_t)(q1 - q0), rd[q0].K, cfg->eps, cfg->trunc_rule, ps.G,
-                                         ps.W, d_rank + q0, d_flag + q0)))
-          return fail(rc);
+        const cudaStream_t saved = c.stream;
+        if (ci == 0) c.stream = c.aux;
+        rc = launch_recompress_core(c, d_rd + q0, (int64_t)(q1 - q0), rd[q0].K, cfg->eps, cfg->trunc_rule, ps.G,
+                                    ps.W, d_rank + q0, d_flag + q0);
+        c.stream = saved;
+        if (rc) return fail(rc);
       }
       q0 = q1;
     }

@@ -15,6 +15,9 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <map>
+#include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "green.cuh"
@@ -29,6 +32,12 @@ struct Ctx {
   bool own_stream = false;
   int num_sms = 148;
   size_t l2_bytes = 0;
+  // caching allocator: freed device blocks are kept (by size) and reused by
+  // later allocations of the context instead of cudaFree / cudaMalloc
+  std::mutex mem_mu;
+  std::multimap<size_t, void*> cache;  // size -> free block
+  std::unordered_map<void*, size_t> live;  // block -> size
+  size_t cached_bytes = 0;
 };
 
 // phase-1 job: one warp computes s[soff] = V[voff : voff+len]^H x_tree[xoff : xoff+len]
@@ -137,12 +146,16 @@ struct AcaOut {
   int32_t status;    // bit0 converged, bit1 max_rank, bit2 capacity overflow, bit3 fallback needed
   int32_t zero_rows;
 };
-// leaves with m + n >= kAcaClusterMin points run on a cluster of kAcaCluster CTAs
+// launch variants of the ACA kernel; leaves with m + n < kAcaNarrowMax points use
+// the narrow variant, optionally m + n >= kAcaClusterMin a cluster of CTAs
+constexpr int kAcaWide = 0;
+constexpr int kAcaNarrow = 1;
+constexpr int kAcaNarrowMax = 320;
 constexpr int kAcaCluster = 8;
 constexpr int kAcaClusterMin = 1024;
 int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const AcaDesc* d_desc, const int32_t* d_order,
                int64_t nblk, int kcap_max, int m_max, double eps, double sigma3_floor, double2* U, double2* V,
-               double2* G, AcaOut* d_out, int cluster);
+               double2* G, AcaOut* d_out, int variant);
 
 // recompress.cu
 // recompress_core keeps E and the QL eigenvector matrix in shared memory up to this ACA rank

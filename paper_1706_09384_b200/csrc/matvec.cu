@@ -196,12 +196,17 @@ int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
   H.leaf_voff.assign(nb, -1);
   int64_t vo = 0;
   double dense_b = 0, lr_b = 0;
-  std::vector<MvJob1> jobs;
-  {
-    int64_t nj = 0;
-    for (int64_t b = 0; b < nb; ++b) nj += H.table[5 * b] == 0 ? 1 : H.rank_after[b];
-    jobs.reserve(nj);
+  // phase-1 jobs placed directly in longest-first order (counting sort on the
+  // job length, stable in leaf order): one pass to count, one to place
+  int32_t maxlen = 1;
+  for (int64_t b = 0; b < nb; ++b) maxlen = std::max<int32_t>(maxlen, (int32_t)(d * (H.table[5 * b + 4] - H.table[5 * b + 3])));
+  std::vector<int64_t> slot((size_t)maxlen + 2, 0);
+  for (int64_t b = 0; b < nb; ++b) {
+    const int32_t len = (int32_t)(d * (H.table[5 * b + 4] - H.table[5 * b + 3]));
+    slot[(size_t)(maxlen - len) + 1] += H.table[5 * b] == 0 ? 1 : H.rank_after[b];
   }
+  for (size_t i = 1; i < slot.size(); ++i) slot[i] += slot[i - 1];
+  std::vector<MvJob1> jobs((size_t)slot.back());
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t g = bseg[b];
     const int64_t m = H.table[5 * b + 2] - H.table[5 * b + 1];
@@ -210,30 +215,20 @@ int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
     H.leaf_ld[b] = ld;
     H.leaf_moff[b] = moff[g] + colstart[b] * ld;
     const int64_t c0 = H.table[5 * b + 3];
+    int64_t& pos = slot[(size_t)(maxlen - (int32_t)(d * n))];
     if (H.table[5 * b] == 0) {
-      jobs.push_back(MvJob1{0, d * c0, soff[g] + colstart[b], (int32_t)(d * n), 0});
+      jobs[(size_t)pos++] = MvJob1{0, d * c0, soff[g] + colstart[b], (int32_t)(d * n), 0};
       dense_b += 16.0 * ld * d * n;
     } else {
       const int64_t r = H.rank_after[b];
       H.leaf_voff[b] = vo;
       for (int64_t l = 0; l < r; ++l)
-        jobs.push_back(MvJob1{vo + l * d * n, d * c0, soff[g] + colstart[b] + l, (int32_t)(d * n), 1});
+        jobs[(size_t)pos++] = MvJob1{vo + l * d * n, d * c0, soff[g] + colstart[b] + l, (int32_t)(d * n), 1};
       vo += d * n * r;
       lr_b += 16.0 * r * d * (m + n);
     }
   }
   H.v_elems = vo;
-  // longest jobs first (stable counting sort on the job length)
-  {
-    int32_t maxlen = 0;
-    for (const MvJob1& j : jobs) maxlen = std::max(maxlen, j.len);
-    std::vector<int64_t> cnt((size_t)maxlen + 2, 0);
-    for (const MvJob1& j : jobs) cnt[(size_t)(maxlen - j.len) + 1]++;
-    for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
-    std::vector<MvJob1> sorted(jobs.size());
-    for (const MvJob1& j : jobs) sorted[(size_t)cnt[(size_t)(maxlen - j.len)]++] = j;
-    jobs.swap(sorted);
-  }
   std::vector<MvTile2> tiles;
   for (int64_t g = 0; g < ns; ++g) {
     if (ncols[g] == 0) continue;
