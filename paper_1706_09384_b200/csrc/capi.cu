@@ -167,15 +167,22 @@ struct DevBuf {
   explicit DevBuf(Ctx& c) : ctx(&c) {}
   DevBuf(DevBuf&& o) noexcept : ctx(o.ctx), p(std::move(o.p)) { o.p.clear(); }
   DevBuf(const DevBuf&) = delete;
-  ~DevBuf() {
+  ~DevBuf() { release(); }
+  void release() {
     for (void* q : p) dev_free(*ctx, q);
+    p.clear();
   }
   template <class T>
   int alloc(T** out, int64_t count) {
     void* q = nullptr;
     cudaError_t e = dev_alloc(*ctx, &q, sizeof(T) * std::max<int64_t>(count, 1));
     if (e != cudaSuccess) {
-      hmx_set_error("cudaMalloc(%lld bytes): %s", (long long)(sizeof(T) * count), cudaGetErrorString(e));
+      size_t fr = 0, tot = 0;
+      cudaGetLastError();
+      cudaMemGetInfo(&fr, &tot);
+      hmx_set_error("cudaMalloc(%lld bytes): %s (free %.2f GB of %.2f GB, context cache %.2f GB)",
+                    (long long)(sizeof(T) * count), cudaGetErrorString(e), fr / 1e9, tot / 1e9,
+                    ctx->cached_bytes / 1e9);
       return e == cudaErrorMemoryAllocation ? HMX_ENOMEM : HMX_ECUDA;
     }
     p.push_back(q);
@@ -220,8 +227,9 @@ struct OnAux {
 };
 
 struct AcaPass {
-  explicit AcaPass(Ctx& c) : mem(c) {}
-  DevBuf mem;
+  explicit AcaPass(Ctx& c) : mem(c), gmem(c) {}
+  DevBuf mem;   // U, V factor workspaces and the recompression W
+  DevBuf gmem;  // Gram matrices: only needed until the recompression
   double2 *U = nullptr, *V = nullptr, *G = nullptr, *W = nullptr;
   std::vector<int64_t> blocks;  // block ids
   std::vector<AcaDesc> desc;
@@ -480,8 +488,11 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   auto tick = [&](const char* what) {
     if (!verbose) return;
     cudaStreamSynchronize(c.stream);
-    std::fprintf(stderr, "[hmx] %-28s %9.2f ms\n", what,
-                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+    size_t fr = 0, tot = 0;
+    cudaMemGetInfo(&fr, &tot);
+    std::fprintf(stderr, "[hmx] %-28s %9.2f ms   free %7.2f GB  cache %6.2f GB\n", what,
+                 std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count(),
+                 fr / 1e9, c.cached_bytes / 1e9);
   };
   tick("upload");
 
@@ -498,7 +509,10 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   }
   size_t free_b = 0, total_b = 0;
   HMX_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-  const double budget = cfg->mem_budget_gb > 0 ? cfg->mem_budget_gb * 1e9 : 0.4 * (double)free_b;
+  // memory cached by this context counts as free; U, V and the Gram matrices get
+  // 55% (the Grams are released before the final streams are allocated)
+  const double avail = (double)free_b + (double)c.cached_bytes;
+  const double budget = cfg->mem_budget_gb > 0 ? cfg->mem_budget_gb * 1e9 : 0.55 * avail;
   auto round_d = [&](int64_t v) { return std::max<int64_t>(d, (v / d) * d); };
   auto ws_bytes = [&](int64_t b, int64_t kc) {
     return 16.0 * ((double)d * (rows_of(b) + cols_of(b)) * kc + 2.0 * kc * kc);
@@ -520,7 +534,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       return std::sqrt((hi3[0] - lo3[0]) * (hi3[0] - lo3[0]) + (hi3[1] - lo3[1]) * (hi3[1] - lo3[1]) +
                        (hi3[2] - lo3[2]) * (hi3[2] - lo3[2]));
     };
-    const double floor_cols = d == 1 ? 36.0 : 72.0;
+    const double floor_cols = d == 1 ? 36.0 : 60.0;
     for (int64_t b : adm) {
       const double dm = std::max(diam(table[5 * b + 1], table[5 * b + 2]), diam(table[5 * b + 3], table[5 * b + 4]));
       const int64_t est = round_d((int64_t)std::ceil(floor_cols + 2.0 * d * kap * dm) + d - 1);
@@ -569,7 +583,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     tick("aca: descriptors");
     if ((rc = ps.mem.alloc(&ps.U, uo))) return fail(rc);
     if ((rc = ps.mem.alloc(&ps.V, vo))) return fail(rc);
-    if ((rc = ps.mem.alloc(&ps.G, go))) return fail(rc);
+    if ((rc = ps.gmem.alloc(&ps.G, go))) return fail(rc);
     AcaDesc* d_desc;
     AcaOut* d_out;
     int32_t* d_order;
@@ -752,6 +766,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     }
   }
   HMX_CUDA_TRY(cudaEventRecord(ev[2], c.stream));
+  for (AcaPass& ps : passes) ps.gmem.release();  // Gram workspaces back before the streams are allocated
   tick("recompress done");
 
   // ---- 3. layout + matvec plan ----------------------------------------------------------------

@@ -18,7 +18,7 @@ namespace hmx {
 
 namespace {
 
-constexpr int kThreads = 256;  // form_gemm
+
 
 template <int NT>
 HMX_D double block_sum(double v, double* red) {
@@ -723,11 +723,14 @@ __global__ void __launch_bounds__(NT) recompress_core(const RecDesc* __restrict_
 }
 
 // C (rows x r, ldc) = A (rows x K, lda) * W (K x r, ld K); one CTA = 64 x 32 tile.
-constexpr int TM = 64, TN = 32, TK = 16;
-__global__ void __launch_bounds__(kThreads) form_gemm(const FormDesc* __restrict__ desc,
-                                                      const int64_t* __restrict__ tile_start, int64_t nitems,
-                                                      const double2* __restrict__ Abase,
-                                                      const double2* __restrict__ Wbase, double2* __restrict__ Cbase) {
+// 64 x 32 output tile per CTA of 128 threads, 4 x 4 complex outputs per thread
+// (16 DFMA per shared-memory load pair), k-chunks of 16.
+constexpr int TM = 64, TN = 32, TK = 16, kFormThreads = 128;
+__global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __restrict__ desc,
+                                                          const int64_t* __restrict__ tile_start, int64_t nitems,
+                                                          const double2* __restrict__ Abase,
+                                                          const double2* __restrict__ Wbase,
+                                                          double2* __restrict__ Cbase) {
   __shared__ double2 As[TK][TM + 1];
   __shared__ double2 Ws[TK][TN + 1];
   // locate item by binary search over tile_start
@@ -746,42 +749,44 @@ __global__ void __launch_bounds__(kThreads) form_gemm(const FormDesc* __restrict
   const double2* W = Wbase + ds.woff;
   double2* C = Cbase + ds.coff;
   const int tid = threadIdx.x;
-  const int tr = tid % 32, tc = tid / 32;  // thread computes rows tr, tr+32 ; cols tc, tc+8, tc+16, tc+24
-  double2 acc[2][4];
+  const int tr = tid % 16, tc = tid / 16;  // rows tr + 16 a, cols tc + 8 b
+  double2 acc[4][4];
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) acc[a][b] = cmk(0.0, 0.0);
   const int row0 = tm * TM, col0 = tn * TN;
   for (int k0 = 0; k0 < ds.K; k0 += TK) {
-    for (int t = tid; t < TK * TM; t += kThreads) {
+    for (int t = tid; t < TK * TM; t += kFormThreads) {
       const int rr = t % TM, kk = t / TM;
       const int gr = row0 + rr, gk = k0 + kk;
       As[kk][rr] = (gr < ds.rows && gk < ds.K) ? A[gr + (int64_t)gk * ds.lda] : cmk(0.0, 0.0);
     }
-    for (int t = tid; t < TK * TN; t += kThreads) {
+    for (int t = tid; t < TK * TN; t += kFormThreads) {
       const int kk = t % TK, cc = t / TK;
       const int gk = k0 + kk, gc = col0 + cc;
       Ws[kk][cc] = (gk < ds.K && gc < ds.r) ? W[gk + (int64_t)gc * ds.K] : cmk(0.0, 0.0);
     }
     __syncthreads();
-#pragma unroll 4
+#pragma unroll 2
     for (int kk = 0; kk < TK; ++kk) {
-      const double2 a0 = As[kk][tr], a1 = As[kk][tr + 32];
+      double2 av[4], wv[4];
 #pragma unroll
-      for (int b = 0; b < 4; ++b) {
-        const double2 w = Ws[kk][tc + 8 * b];
-        acc[0][b] = cfma(a0, w, acc[0][b]);
-        acc[1][b] = cfma(a1, w, acc[1][b]);
-      }
+      for (int a = 0; a < 4; ++a) av[a] = As[kk][tr + 16 * a];
+#pragma unroll
+      for (int b = 0; b < 4; ++b) wv[b] = Ws[kk][tc + 8 * b];
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] = cfma(av[a], wv[b], acc[a][b]);
     }
     __syncthreads();
   }
 #pragma unroll
-  for (int a = 0; a < 2; ++a)
+  for (int a = 0; a < 4; ++a)
 #pragma unroll
     for (int b = 0; b < 4; ++b) {
-      const int gr = row0 + tr + 32 * a, gc = col0 + tc + 8 * b;
+      const int gr = row0 + tr + 16 * a, gc = col0 + tc + 8 * b;
       if (gr < ds.rows && gc < ds.r) C[gr + (int64_t)gc * ds.ldc] = acc[a][b];
     }
 }
@@ -828,7 +833,7 @@ int launch_recompress_core(Ctx& c, const RecDesc* d_desc, int64_t nblk, int kmax
 int launch_form(Ctx& c, const FormDesc* d_desc, int64_t nitems, int64_t ntiles_total, const int64_t* d_tile_start,
                 const double2* A, const double2* W, double2* C) {
   if (ntiles_total == 0) return HMX_OK;
-  form_gemm<<<(unsigned)ntiles_total, kThreads, 0, c.stream>>>(d_desc, d_tile_start, nitems, A, W, C);
+  form_gemm<<<(unsigned)ntiles_total, kFormThreads, 0, c.stream>>>(d_desc, d_tile_start, nitems, A, W, C);
   HMX_CUDA_TRY(cudaGetLastError());
   return HMX_OK;
 }
