@@ -594,7 +594,9 @@ int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const 
   // slower), kAcaNarrow (128 threads, 4 CTAs per SM: small leaves are latency
   // bound and use few threads per step), >1: cluster of that many CTAs per leaf.
   const int CSv = variant > 1 ? variant : 1;
-  const int nt = variant == kAcaNarrow ? 128 : 512;
+  const char* e_wnt = std::getenv("HMX_ACA_WIDE_NT");
+  const int wide_nt = e_wnt && std::atoi(e_wnt) == 256 ? 256 : 512;
+  const int nt = variant == kAcaNarrow ? 128 : (CSv > 1 ? 512 : wide_nt);
   size_t smem = sizeof(double2) * (CSv > 1 ? 4 : 2) * (size_t)d * kcap_max + (size_t)((m_max + 15) / 16) * 16;
   auto go = [&](auto kern) -> int {
     HMX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -624,6 +626,9 @@ int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const 
   } else if (variant == kAcaNarrow) {
     rc = P.kind == 0 ? go(aca_kernel<1, 0, 128, 4, 1>)
                      : (P.kind == 1 ? go(aca_kernel<3, 1, 128, 4, 1>) : go(aca_kernel<3, 2, 128, 4, 1>));
+  } else if (nt == 256) {
+    rc = P.kind == 0 ? go(aca_kernel<1, 0, 256, 2, 1>)
+                     : (P.kind == 1 ? go(aca_kernel<3, 1, 256, 2, 1>) : go(aca_kernel<3, 2, 256, 2, 1>));
   } else {
     rc = P.kind == 0 ? go(aca_kernel<1, 0, 512, 1, 1>)
                      : (P.kind == 1 ? go(aca_kernel<3, 1, 512, 1, 1>) : go(aca_kernel<3, 2, 512, 1, 1>));

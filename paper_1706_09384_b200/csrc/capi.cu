@@ -14,6 +14,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <cstdlib>
+#include <deque>
 #include <cmath>
 #include <cstring>
 #include <string>
@@ -230,11 +231,11 @@ struct AcaPass {
   explicit AcaPass(Ctx& c) : mem(c), gmem(c) {}
   DevBuf mem;   // U, V factor workspaces and the recompression W
   DevBuf gmem;  // Gram matrices: only needed until the recompression
-  double2 *U = nullptr, *V = nullptr, *G = nullptr, *W = nullptr;
+  double2 *U = nullptr, *V = nullptr, *G = nullptr;
   std::vector<int64_t> blocks;  // block ids
   std::vector<AcaDesc> desc;
   std::vector<AcaOut> out;
-  std::vector<int64_t> woff;
+  std::vector<double2*> wptr;  // per leaf: its W_U | W_V coefficients
   int kcap_max = 0;
 };
 
@@ -495,6 +496,15 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
                  fr / 1e9, c.cached_bytes / 1e9);
   };
   tick("upload");
+  // HMX_VERBOSE: GPU timeline of the launches (events on the issuing stream)
+  std::vector<std::pair<std::string, cudaEvent_t>> tl;
+  auto mark = [&](const std::string& what) {
+    if (!verbose) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, c.stream);
+    tl.emplace_back(what + (c.stream == c.aux ? " [aux]" : " [main]"), e);
+  };
 
   // ---- 1. ACA passes --------------------------------------------------------------------
   std::vector<int64_t> adm;
@@ -548,21 +558,136 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       for (int64_t b : adm) kcap[b] = std::max<int64_t>(d, round_d((int64_t)(kcap[b] * f)));
     }
   }
-  std::vector<AcaPass> passes;
-  passes.reserve(8);
+  std::deque<AcaPass> passes;  // stable addresses (Pending keeps pointers)
   std::vector<int64_t> todo = adm;
-  int64_t m_max_all = 1;
-  for (int64_t b : adm) m_max_all = std::max(m_max_all, rows_of(b));
+  const double s3f = cfg->sigma3_floor > 0 ? cfg->sigma3_floor : 1e-12;
+  const char* e_cs = std::getenv("HMX_ACA_CS");
+  const char* e_min = std::getenv("HMX_ACA_CLUSTER_MIN");
+  const char* e_nm = std::getenv("HMX_ACA_NARROW_MAX");
+  const int cs = e_cs ? std::atoi(e_cs) : 1;  // clusters measured slower
+  const int64_t cmin = e_min ? std::atoll(e_min) : kAcaClusterMin;
+  const int64_t nmax = e_nm ? std::atoll(e_nm) : kAcaNarrowMax;
+  // recompression results read back once at the end
+  struct Pending {
+    AcaPass* ps;
+    std::vector<int64_t> live;  // indices into ps->blocks
+    int32_t* d_rank;
+    int32_t* d_flag;
+  };
+  std::vector<Pending> pending;
+  DevBuf rec_tmp(c);
+  const cudaStream_t main_stream = c.stream;
+  // Recompression of the live leaves [q0, q1) of a pass, on the current c.stream.
+  auto recompress_subset = [&](AcaPass& ps, std::vector<int64_t> live) -> int {
+    if (live.empty()) return HMX_OK;
+    // largest K first, launched in K classes so small leaves do not pay for big shared memory
+    std::sort(live.begin(), live.end(), [&](int64_t x, int64_t y) {
+      return ps.out[x].rank != ps.out[y].rank ? ps.out[x].rank > ps.out[y].rank : x < y;
+    });
+    std::vector<RecDesc> rd(live.size());
+    int64_t wo = 0;
+    for (size_t q = 0; q < live.size(); ++q) {
+      const int K = ps.out[live[q]].rank;
+      rd[q].goff = ps.desc[live[q]].goff;
+      rd[q].woff = wo;
+      rd[q].K = K;
+      rd[q].kcap = ps.desc[live[q]].kcap;
+      wo += 6 * (int64_t)K * K;
+    }
+    double2* W;
+    RecDesc* d_rd;
+    int32_t *d_rank, *d_flag;
+    int e;
+    if ((e = ps.mem.alloc(&W, wo))) return e;
+    if ((e = rec_tmp.alloc(&d_rd, (int64_t)rd.size()))) return e;
+    if ((e = rec_tmp.alloc(&d_rank, (int64_t)rd.size()))) return e;
+    if ((e = rec_tmp.alloc(&d_flag, (int64_t)rd.size()))) return e;
+    for (size_t q = 0; q < live.size(); ++q) ps.wptr[live[q]] = W + rd[q].woff;
+    HMX_CUDA_TRY(cudaMemcpyAsync(d_rd, rd.data(), sizeof(RecDesc) * rd.size(), cudaMemcpyHostToDevice, c.stream));
+    mark("recompress start");
+    // shared-memory size classes (smem ~ 16 K^2 bytes): more CTAs per SM for small K
+    const int classes[] = {kMaxAcaCols, kRecompressSmemMax, 88, 64, 48, 32};
+    const int ncls = 6;
+    size_t q0 = 0;
+    // when issued on the auxiliary stream, only the large-K class stays there;
+    // the shared-memory classes go to the main stream (ordered after this
+    // point by an event) so they overlap the long large-K CTAs
+    const bool on_aux = c.stream == c.aux;
+    bool forked = false;
+    for (int ci = 0; ci < ncls && q0 < rd.size(); ++ci) {
+      const int lim_lo = ci + 1 < ncls ? classes[ci + 1] : 0;
+      size_t q1 = q0;
+      while (q1 < rd.size() && (rd[q1].K > lim_lo || ci == ncls - 1)) ++q1;
+      if (q1 > q0) {
+        const cudaStream_t saved = c.stream;
+        if (on_aux && ci > 0) {
+          if (!forked) {
+            cudaEvent_t ev_f;
+            HMX_CUDA_TRY(cudaEventCreateWithFlags(&ev_f, cudaEventDisableTiming));
+            HMX_CUDA_TRY(cudaEventRecord(ev_f, c.aux));
+            HMX_CUDA_TRY(cudaStreamWaitEvent(main_stream, ev_f, 0));
+            cudaEventDestroy(ev_f);
+            forked = true;
+          }
+          c.stream = main_stream;
+        }
+        e = launch_recompress_core(c, d_rd + q0, (int64_t)(q1 - q0), rd[q0].K, cfg->eps, cfg->trunc_rule, ps.G, W,
+                                   d_rank + q0, d_flag + q0);
+        c.stream = saved;
+        if (e) return e;
+      }
+      q0 = q1;
+    }
+    mark("recompress issued");
+    if (forked) {
+      const cudaStream_t sv = c.stream;
+      c.stream = main_stream;
+      mark("recompress small classes issued");
+      c.stream = sv;
+    }
+    pending.push_back(Pending{&ps, std::move(live), d_rank, d_flag});
+    return HMX_OK;
+  };
+  // ACA outputs of positions [q0, q1) of the pass (already on the host):
+  // bookkeeping, overflow -> next pass, recompression of the rest
+  std::vector<int64_t> next;
+  int64_t nfb = 0;
+  auto consume = [&](AcaPass& ps, size_t q0, size_t q1) -> int {
+    std::vector<int64_t> live;
+    for (size_t i = q0; i < q1; ++i) {
+      const int64_t b = ps.blocks[i];
+      const AcaOut& o = ps.out[i];
+      if (o.status & 4) {
+        if (kcap[b] >= std::min<int64_t>(maxr[b], round_d(kMaxAcaCols))) {
+          hmx_set_error("block %lld: ACA rank exceeds %d columns", (long long)b, kMaxAcaCols);
+          return HMX_ENOMEM;
+        }
+        kcap[b] = std::min<int64_t>(std::min<int64_t>(maxr[b], round_d(kMaxAcaCols)), 2 * kcap[b]);
+        next.push_back(b);
+        ps.out[i].rank = -1;  // superseded
+        continue;
+      }
+      if (o.status & 8) ++nfb;
+      H.steps[b] = o.steps;
+      H.rank_before[b] = o.rank;
+      H.flags[b] = o.status & 0xB;
+      H.pairs_evaluated += (int64_t)o.steps * (rows_of(b) + cols_of(b)) + (int64_t)o.zero_rows * cols_of(b);
+      live.push_back((int64_t)i);
+    }
+    if (nfb) return HMX_OK;
+    return recompress_subset(ps, std::move(live));
+  };
   while (!todo.empty()) {
     passes.emplace_back(c);
     AcaPass& ps = passes.back();
-    std::sort(todo.begin(), todo.end(), [&](int64_t a, int64_t b) {
-      const int64_t ca = rows_of(a) + cols_of(a), cb = rows_of(b) + cols_of(b);
-      return ca != cb ? ca > cb : a < b;
+    std::sort(todo.begin(), todo.end(), [&](int64_t x, int64_t y) {
+      const int64_t ca = rows_of(x) + cols_of(x), cb = rows_of(y) + cols_of(y);
+      return ca != cb ? ca > cb : x < y;
     });
     ps.blocks = todo;
     int64_t uo = 0, vo = 0, go = 0;
     ps.desc.resize(todo.size());
+    ps.wptr.assign(todo.size(), nullptr);
     for (size_t i = 0; i < todo.size(); ++i) {
       const int64_t b = todo[i];
       AcaDesc& D = ps.desc[i];
@@ -587,10 +712,9 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     AcaDesc* d_desc;
     AcaOut* d_out;
     int32_t* d_order;
-    DevBuf tmp(c);
-    if ((rc = tmp.alloc(&d_desc, (int64_t)todo.size()))) return fail(rc);
-    if ((rc = tmp.alloc(&d_out, (int64_t)todo.size()))) return fail(rc);
-    if ((rc = tmp.alloc(&d_order, (int64_t)todo.size()))) return fail(rc);
+    if ((rc = rec_tmp.alloc(&d_desc, (int64_t)todo.size()))) return fail(rc);
+    if ((rc = rec_tmp.alloc(&d_out, (int64_t)todo.size()))) return fail(rc);
+    if ((rc = rec_tmp.alloc(&d_order, (int64_t)todo.size()))) return fail(rc);
     std::vector<int32_t> order(todo.size());
     for (size_t i = 0; i < order.size(); ++i) order[i] = (int32_t)i;
     HMX_CUDA_TRY(cudaMemcpyAsync(d_desc, ps.desc.data(), sizeof(AcaDesc) * todo.size(), cudaMemcpyHostToDevice,
@@ -598,83 +722,64 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     HMX_CUDA_TRY(
         cudaMemcpyAsync(d_order, order.data(), sizeof(int32_t) * todo.size(), cudaMemcpyHostToDevice, c.stream));
     tick("aca: workspace alloc");
+    // large leaves (clusters / wide CTAs, a prefix of the size-sorted list) on
+    // the auxiliary stream, the many small leaves (narrow CTAs) on the main
+    // stream; each side's recompression starts as soon as its own ACA is done
+    size_t nbig = 0, nwide = 0;
+    while (cs > 1 && nbig < todo.size() && rows_of(todo[nbig]) + cols_of(todo[nbig]) >= cmin) ++nbig;
+    nwide = nbig;
+    while (nwide < todo.size() && rows_of(todo[nwide]) + cols_of(todo[nwide]) >= nmax) ++nwide;
+    auto sub_max = [&](size_t q0, size_t q1, int& kc, int& mm) {
+      kc = 1;
+      mm = 1;
+      for (size_t q = q0; q < q1; ++q) {
+        kc = std::max<int>(kc, ps.desc[q].kcap);
+        mm = std::max<int>(mm, ps.desc[q].m);
+      }
+    };
+    cudaEvent_t fork;
+    HMX_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+    HMX_CUDA_TRY(cudaEventRecord(fork, c.stream));
+    HMX_CUDA_TRY(cudaStreamWaitEvent(c.aux, fork, 0));
+    cudaEventDestroy(fork);
+    ps.out.resize(todo.size());
+    int kc, mm;
+    mark("aca start");
     {
-      // large leaves (a prefix of the size-sorted list) on CTA clusters in an
-      // auxiliary stream, concurrently with the one-CTA-per-leaf launch
-      const char* e_cs = std::getenv("HMX_ACA_CS");
-      const char* e_min = std::getenv("HMX_ACA_CLUSTER_MIN");
-      const int cs = e_cs ? std::atoi(e_cs) : 1;  // clusters measured slower
-      const int64_t cmin = e_min ? std::atoll(e_min) : kAcaClusterMin;
-      const char* e_nm = std::getenv("HMX_ACA_NARROW_MAX");
-      const int64_t nmax = e_nm ? std::atoll(e_nm) : kAcaNarrowMax;
-      size_t nbig = 0, nwide = 0;
-      while (cs > 1 && nbig < todo.size() && rows_of(todo[nbig]) + cols_of(todo[nbig]) >= cmin) ++nbig;
-      nwide = nbig;
-      while (nwide < todo.size() && rows_of(todo[nwide]) + cols_of(todo[nwide]) >= nmax) ++nwide;
-      auto sub_max = [&](size_t q0, size_t q1, int& kc, int& mm) {
-        kc = 1;
-        mm = 1;
-        for (size_t q = q0; q < q1; ++q) {
-          kc = std::max<int>(kc, ps.desc[q].kcap);
-          mm = std::max<int>(mm, ps.desc[q].m);
-        }
-      };
-      const double s3f = cfg->sigma3_floor > 0 ? cfg->sigma3_floor : 1e-12;
-      cudaEvent_t fork, join;
-      HMX_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-      HMX_CUDA_TRY(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
-      HMX_CUDA_TRY(cudaEventRecord(fork, c.stream));
-      HMX_CUDA_TRY(cudaStreamWaitEvent(c.aux, fork, 0));
-      int kc, mm;
-      // large leaves (clusters, then wide CTAs) on the auxiliary stream, the
-      // many small leaves (narrow CTAs) concurrently on the main stream
+      OnAux on(c);
+      mark("aca wide start");
       if (nbig) {
         sub_max(0, nbig, kc, mm);
-        if ((rc = [&] { OnAux on(c); return launch_aca(c, d, P, pts.soa, d_desc, d_order, (int64_t)nbig, kc, mm, cfg->eps, s3f, ps.U, ps.V,
-                             ps.G, d_out, cs); }()))
+        if ((rc = launch_aca(c, d, P, pts.soa, d_desc, d_order, (int64_t)nbig, kc, mm, cfg->eps, s3f, ps.U, ps.V,
+                             ps.G, d_out, cs)))
           return fail(rc);
       }
       if (nwide > nbig) {
         sub_max(nbig, nwide, kc, mm);
-        if ((rc = [&] { OnAux on(c); return launch_aca(c, d, P, pts.soa, d_desc, d_order + nbig, (int64_t)(nwide - nbig), kc, mm, cfg->eps,
-                             s3f, ps.U, ps.V, ps.G, d_out, kAcaWide); }()))
+        if ((rc = launch_aca(c, d, P, pts.soa, d_desc, d_order + nbig, (int64_t)(nwide - nbig), kc, mm, cfg->eps,
+                             s3f, ps.U, ps.V, ps.G, d_out, kAcaWide)))
           return fail(rc);
       }
-      if (todo.size() > nwide) {
-        sub_max(nwide, todo.size(), kc, mm);
-        if ((rc = launch_aca(c, d, P, pts.soa, d_desc, d_order + nwide, (int64_t)(todo.size() - nwide), kc, mm,
-                             cfg->eps, s3f, ps.U, ps.V, ps.G, d_out, kAcaNarrow)))
-          return fail(rc);
-      }
-      HMX_CUDA_TRY(cudaEventRecord(join, c.aux));
-      HMX_CUDA_TRY(cudaStreamWaitEvent(c.stream, join, 0));
-      cudaEventDestroy(fork);
-      cudaEventDestroy(join);
+      mark("aca wide done");
+      if (nwide)
+        HMX_CUDA_TRY(
+            cudaMemcpyAsync(ps.out.data(), d_out, sizeof(AcaOut) * nwide, cudaMemcpyDeviceToHost, c.stream));
     }
-    ps.out.resize(todo.size());
-    HMX_CUDA_TRY(
-        cudaMemcpyAsync(ps.out.data(), d_out, sizeof(AcaOut) * todo.size(), cudaMemcpyDeviceToHost, c.stream));
-    HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
-    std::vector<int64_t> next;
-    int64_t nfb = 0;
-    for (size_t i = 0; i < todo.size(); ++i) {
-      const int64_t b = todo[i];
-      const AcaOut& o = ps.out[i];
-      if (o.status & 4) {
-        if (kcap[b] >= std::min<int64_t>(maxr[b], round_d(kMaxAcaCols))) {
-          hmx_set_error("block %lld: ACA rank exceeds %d columns", (long long)b, kMaxAcaCols);
-          return fail(HMX_ENOMEM);
-        }
-        kcap[b] = std::min<int64_t>(std::min<int64_t>(maxr[b], round_d(kMaxAcaCols)), 2 * kcap[b]);
-        next.push_back(b);
-        ps.out[i].rank = -1;  // superseded
-        continue;
-      }
-      if (o.status & 8) ++nfb;
-      H.steps[b] = o.steps;
-      H.rank_before[b] = o.rank;
-      H.flags[b] = o.status & 0xB;
-      H.pairs_evaluated += (int64_t)o.steps * (rows_of(b) + cols_of(b)) + (int64_t)o.zero_rows * cols_of(b);
+    if (todo.size() > nwide) {
+      sub_max(nwide, todo.size(), kc, mm);
+      if ((rc = launch_aca(c, d, P, pts.soa, d_desc, d_order + nwide, (int64_t)(todo.size() - nwide), kc, mm,
+                           cfg->eps, s3f, ps.U, ps.V, ps.G, d_out, kAcaNarrow)))
+        return fail(rc);
+      mark("aca narrow done");
+      HMX_CUDA_TRY(cudaMemcpyAsync(ps.out.data() + nwide, d_out + nwide, sizeof(AcaOut) * (todo.size() - nwide),
+                                   cudaMemcpyDeviceToHost, c.stream));
+      HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));  // small leaves only; the large ones keep running
+      if ((rc = consume(ps, nwide, todo.size()))) return fail(rc);
+    }
+    if (nwide) {
+      HMX_CUDA_TRY(cudaStreamSynchronize(c.aux));
+      OnAux on(c);
+      if ((rc = consume(ps, 0, nwide))) return fail(rc);
     }
     H.aca_passes++;
     if (nfb) {
@@ -684,78 +789,38 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
                     (long long)nfb);
       return fail(HMX_EPIVOT);
     }
+    // join the auxiliary stream before the next pass / the layout
+    cudaEvent_t join;
+    HMX_CUDA_TRY(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    HMX_CUDA_TRY(cudaEventRecord(join, c.aux));
+    HMX_CUDA_TRY(cudaStreamWaitEvent(c.stream, join, 0));
+    cudaEventDestroy(join);
     todo.swap(next);
+    next.clear();
   }
   HMX_CUDA_TRY(cudaEventRecord(ev[1], c.stream));
   tick("aca done");
-
-  // ---- 2. recompression core --------------------------------------------------------------
-  std::vector<int64_t> regularized(nb, 0);
-  for (AcaPass& ps : passes) {
-    std::vector<int64_t> live;
-    for (size_t i = 0; i < ps.blocks.size(); ++i)
-      if (ps.out[i].rank >= 0) live.push_back((int64_t)i);
-    // largest K first, launched in K classes so small leaves do not pay for big shared memory
-    std::sort(live.begin(), live.end(), [&](int64_t a, int64_t b) {
-      return ps.out[a].rank != ps.out[b].rank ? ps.out[a].rank > ps.out[b].rank : a < b;
-    });
-    std::vector<RecDesc> rd(live.size());
-    int64_t wo = 0;
-    ps.woff.assign(ps.blocks.size(), 0);
-    for (size_t q = 0; q < live.size(); ++q) {
-      const int64_t i = live[q];
-      const int K = ps.out[i].rank;
-      rd[q].goff = ps.desc[i].goff;
-      rd[q].woff = wo;
-      rd[q].K = K;
-      rd[q].kcap = ps.desc[i].kcap;
-      ps.woff[i] = wo;
-      wo += 6 * (int64_t)K * K;
+  if (verbose) {
+    cudaDeviceSynchronize();
+    for (auto& kv : tl) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, ev[0], kv.second);
+      std::fprintf(stderr, "[hmx]   gpu %-36s %9.2f ms\n", kv.first.c_str(), ms);
+      cudaEventDestroy(kv.second);
     }
-    if (live.empty()) continue;
-    if ((rc = ps.mem.alloc(&ps.W, wo))) return fail(rc);
-    DevBuf tmp(c);
-    RecDesc* d_rd;
-    int32_t *d_rank, *d_flag;
-    if ((rc = tmp.alloc(&d_rd, (int64_t)rd.size()))) return fail(rc);
-    if ((rc = tmp.alloc(&d_rank, (int64_t)rd.size()))) return fail(rc);
-    if ((rc = tmp.alloc(&d_flag, (int64_t)rd.size()))) return fail(rc);
-    HMX_CUDA_TRY(cudaMemcpyAsync(d_rd, rd.data(), sizeof(RecDesc) * rd.size(), cudaMemcpyHostToDevice, c.stream));
-    // shared-memory size classes (smem ~ 16 K^2 bytes): more CTAs per SM for small K
-    const int classes[] = {kMaxAcaCols, kRecompressSmemMax, 88, 64, 48, 32};
-    const int ncls = 6;
-    size_t q0 = 0;
-    // the large-K class (few long CTAs) runs on the auxiliary stream,
-    // overlapping the many short CTAs of the shared-memory classes
-    cudaEvent_t fork, join;
-    HMX_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
-    HMX_CUDA_TRY(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
-    HMX_CUDA_TRY(cudaEventRecord(fork, c.stream));
-    HMX_CUDA_TRY(cudaStreamWaitEvent(c.aux, fork, 0));
-    for (int ci = 0; ci < ncls && q0 < rd.size(); ++ci) {
-      const int lim_lo = ci + 1 < ncls ? classes[ci + 1] : 0;
-      size_t q1 = q0;
-      while (q1 < rd.size() && (rd[q1].K > lim_lo || ci == ncls - 1)) ++q1;
-      if (q1 > q0) {
-        const cudaStream_t saved = c.stream;
-        if (ci == 0) c.stream = c.aux;
-        rc = launch_recompress_core(c, d_rd + q0, (int64_t)(q1 - q0), rd[q0].K, cfg->eps, cfg->trunc_rule, ps.G,
-                                    ps.W, d_rank + q0, d_flag + q0);
-        c.stream = saved;
-        if (rc) return fail(rc);
-      }
-      q0 = q1;
-    }
-    HMX_CUDA_TRY(cudaEventRecord(join, c.aux));
-    HMX_CUDA_TRY(cudaStreamWaitEvent(c.stream, join, 0));
-    cudaEventDestroy(fork);
-    cudaEventDestroy(join);
-    std::vector<int32_t> hr(rd.size()), hf(rd.size());
-    HMX_CUDA_TRY(cudaMemcpyAsync(hr.data(), d_rank, sizeof(int32_t) * rd.size(), cudaMemcpyDeviceToHost, c.stream));
-    HMX_CUDA_TRY(cudaMemcpyAsync(hf.data(), d_flag, sizeof(int32_t) * rd.size(), cudaMemcpyDeviceToHost, c.stream));
+  }
+  // ---- 2. recompression results (launched per pass above) -------------------------------
+  for (Pending& pd : pending) {
+    std::vector<int32_t> hr(pd.live.size()), hf(pd.live.size());
+    HMX_CUDA_TRY(
+        cudaMemcpyAsync(hr.data(), pd.d_rank, sizeof(int32_t) * hr.size(), cudaMemcpyDeviceToHost, c.stream));
+    HMX_CUDA_TRY(
+        cudaMemcpyAsync(hf.data(), pd.d_flag, sizeof(int32_t) * hf.size(), cudaMemcpyDeviceToHost, c.stream));
     HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
-    for (size_t q = 0; q < live.size(); ++q) {
-      const int64_t b = ps.blocks[live[q]];
+    // pd.live was sorted by K inside recompress_subset: rebuild the same order
+    std::vector<int64_t> lv = pd.live;
+    for (size_t q = 0; q < lv.size(); ++q) {
+      const int64_t b = pd.ps->blocks[lv[q]];
       H.rank_after[b] = hr[q];
       if (hf[q] & 1) {
         H.flags[b] |= 16;
@@ -795,34 +860,35 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   tick("dense leaves");
 
   // ---- 4b. U' = U W_U, V' = V W_V -------------------------------------------------------------
-  for (AcaPass& ps : passes) {
-    if (!ps.W) continue;
-    for (int side = 0; side < 2; ++side) {
-      std::vector<FormDesc> fd;
-      std::vector<int64_t> ts;
-      int64_t ntiles = 0;
-      for (size_t i = 0; i < ps.blocks.size(); ++i) {
-        if (ps.out[i].rank < 0) continue;
-        const int64_t b = ps.blocks[i];
-        const int K = ps.out[i].rank;
-        const int r = (int)H.rank_after[b];
-        if (r == 0 || K == 0) continue;
-        FormDesc f;
-        const int64_t rows = side == 0 ? d * rows_of(b) : d * cols_of(b);
-        f.aoff = side == 0 ? ps.desc[i].uoff : ps.desc[i].voff;
-        f.woff = ps.woff[i] + 4 * (int64_t)K * K + (side == 0 ? 0 : (int64_t)K * r);
-        f.coff = side == 0 ? H.leaf_moff[b] : H.leaf_voff[b];
-        f.rows = (int32_t)rows;
-        f.K = K;
-        f.r = r;
-        f.lda = (int32_t)rows;
-        f.ldc = (int32_t)rows;
-        f.pad = 0;
-        ts.push_back(ntiles);
-        ntiles += hmx_cdiv(rows, 64) * hmx_cdiv(r, 32);
-        fd.push_back(f);
-      }
-      if (fd.empty()) continue;
+  {
+    // one batched launch for every low-rank leaf of every pass, both sides
+    std::vector<FormDesc> fd;
+    std::vector<int64_t> ts;
+    int64_t ntiles = 0;
+    for (AcaPass& ps : passes)
+      for (int side = 0; side < 2; ++side)
+        for (size_t i = 0; i < ps.blocks.size(); ++i) {
+          if (ps.out[i].rank <= 0 || !ps.wptr[i]) continue;
+          const int64_t b = ps.blocks[i];
+          const int K = ps.out[i].rank;
+          const int r = (int)H.rank_after[b];
+          if (r == 0) continue;
+          FormDesc f;
+          const int64_t rows = side == 0 ? d * rows_of(b) : d * cols_of(b);
+          f.A = (side == 0 ? ps.U + ps.desc[i].uoff : ps.V + ps.desc[i].voff);
+          f.W = ps.wptr[i] + 4 * (int64_t)K * K + (side == 0 ? 0 : (int64_t)K * r);
+          f.C = side == 0 ? H.d_row + H.leaf_moff[b] : H.d_v + H.leaf_voff[b];
+          f.rows = (int32_t)rows;
+          f.K = K;
+          f.r = r;
+          f.lda = (int32_t)rows;
+          f.ldc = (int32_t)rows;
+          f.pad = 0;
+          ts.push_back(ntiles);
+          ntiles += hmx_cdiv(rows, 64) * hmx_cdiv(r, 32);
+          fd.push_back(f);
+        }
+    if (!fd.empty()) {
       DevBuf t5(c);
       FormDesc* d_fd;
       int64_t* d_ts;
@@ -830,12 +896,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       if ((rc = t5.alloc(&d_ts, (int64_t)ts.size()))) return fail(rc);
       HMX_CUDA_TRY(cudaMemcpyAsync(d_fd, fd.data(), sizeof(FormDesc) * fd.size(), cudaMemcpyHostToDevice, c.stream));
       HMX_CUDA_TRY(cudaMemcpyAsync(d_ts, ts.data(), sizeof(int64_t) * ts.size(), cudaMemcpyHostToDevice, c.stream));
-      tick(side == 0 ? "form: U descriptors" : "form: V descriptors");
-      if ((rc = launch_form(c, d_fd, (int64_t)fd.size(), ntiles, d_ts, side == 0 ? ps.U : ps.V, ps.W,
-                            side == 0 ? H.d_row : H.d_v)))
-        return fail(rc);
-      HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
-      tick(side == 0 ? "form: U kernel" : "form: V kernel");
+      if ((rc = launch_form(c, d_fd, (int64_t)fd.size(), ntiles, d_ts))) return fail(rc);
     }
   }
   HMX_CUDA_TRY(cudaEventRecord(ev[5], c.stream));

@@ -169,14 +169,13 @@ struct RecDesc {
 int launch_recompress_core(Ctx& c, const RecDesc* d_desc, int64_t nblk, int kmax, double eps, int rule, double2* G,
                            double2* W, int32_t* d_rank, int32_t* d_flags);
 struct FormDesc {
-  int64_t aoff;   // source factor (U or V workspace), ld = lda
-  int64_t woff;   // K x r coefficient matrix in W (ld = K)
-  int64_t coff;   // destination (row stream or V stream)
+  const double2* A;  // source factor (U or V workspace), ld = lda
+  const double2* W;  // K x r coefficient matrix (ld = K)
+  double2* C;        // destination slot in the row stream or V stream, ld = ldc
   int32_t rows, K, r, lda, ldc;
   int32_t pad;
 };
-int launch_form(Ctx& c, const FormDesc* d_desc, int64_t nitems, int64_t ntiles_total, const int64_t* d_tile_start,
-                const double2* A, const double2* W, double2* C);
+int launch_form(Ctx& c, const FormDesc* d_desc, int64_t nitems, int64_t ntiles_total, const int64_t* d_tile_start);
 
 // dense.cu: FP64 peak microbenchmark
 int bench_dfma(Ctx& c, double* tflops);

@@ -12,6 +12,8 @@
 //   U'  = U W_U,  V' = V W_V   (batched tiled complex GEMM, launch_form)
 // so U' V'^H = U V^H Q_V L_r L_r^H Q_V^H: the rank-r truncated SVD of the ACA
 // product, identical to the reference pipeline up to roundoff.
+#include <cstdlib>
+
 #include "hmatrix.h"
 
 namespace hmx {
@@ -63,7 +65,8 @@ constexpr int kGemmTile = 2 * 16 * 33;
 template <int NT, bool ACT, bool BCT>
 __device__ void cta_zgemm(int M, int N, int Kd, const double2* A, int lda, const double2* B, int ldb, double2* C,
                           int ldc, double2* tile) {
-  constexpr int BM = 32, BN = 32, BK = 16, RS = NT / 16, RPT = BM / RS;
+  constexpr int NG = NT > 512 ? 512 : NT;  // threads that own outputs (all threads load tiles)
+  constexpr int BM = 32, BN = 32, BK = 16, RS = NG / 16, RPT = BM / RS;
   double2* As = tile;              // [BK][BM + 1]
   double2* Bs = tile + BK * (BM + 1);  // [BK][BN + 1]
   const int tid = threadIdx.x, tx = tid % 16, ty = tid / 16;
@@ -102,25 +105,29 @@ __device__ void cta_zgemm(int M, int N, int Kd, const double2* A, int lda, const
           Bs[kk * (BN + 1) + jj] = v;
         }
         __syncthreads();
+        if (tid < NG) {
 #pragma unroll 4
-        for (int kk = 0; kk < BK; ++kk) {
-          const double2 b0 = Bs[kk * (BN + 1) + tx], b1 = Bs[kk * (BN + 1) + tx + 16];
+          for (int kk = 0; kk < BK; ++kk) {
+            const double2 b0 = Bs[kk * (BN + 1) + tx], b1 = Bs[kk * (BN + 1) + tx + 16];
 #pragma unroll
-          for (int q = 0; q < RPT; ++q) {
-            const double2 a = As[kk * (BM + 1) + ty + q * RS];
-            acc[q][0] = cfma(a, b0, acc[q][0]);
-            acc[q][1] = cfma(a, b1, acc[q][1]);
+            for (int q = 0; q < RPT; ++q) {
+              const double2 a = As[kk * (BM + 1) + ty + q * RS];
+              acc[q][0] = cfma(a, b0, acc[q][0]);
+              acc[q][1] = cfma(a, b1, acc[q][1]);
+            }
           }
         }
         __syncthreads();
       }
+      if (tid < NG) {
 #pragma unroll
-      for (int q = 0; q < RPT; ++q)
+        for (int q = 0; q < RPT; ++q)
 #pragma unroll
-        for (int h = 0; h < 2; ++h) {
-          const int gi = i0 + ty + q * RS, gj = j0 + tx + 16 * h;
-          if (gi < M && gj < N) C[gi + (int64_t)gj * ldc] = acc[q][h];
-        }
+          for (int h = 0; h < 2; ++h) {
+            const int gi = i0 + ty + q * RS, gj = j0 + tx + 16 * h;
+            if (gi < M && gj < N) C[gi + (int64_t)gj * ldc] = acc[q][h];
+          }
+      }
     }
   __syncthreads();
 }
@@ -727,10 +734,7 @@ __global__ void __launch_bounds__(NT) recompress_core(const RecDesc* __restrict_
 // (16 DFMA per shared-memory load pair), k-chunks of 16.
 constexpr int TM = 64, TN = 32, TK = 16, kFormThreads = 128;
 __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __restrict__ desc,
-                                                          const int64_t* __restrict__ tile_start, int64_t nitems,
-                                                          const double2* __restrict__ Abase,
-                                                          const double2* __restrict__ Wbase,
-                                                          double2* __restrict__ Cbase) {
+                                                          const int64_t* __restrict__ tile_start, int64_t nitems) {
   __shared__ double2 As[TK][TM + 1];
   __shared__ double2 Ws[TK][TN + 1];
   // locate item by binary search over tile_start
@@ -745,9 +749,9 @@ __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __rest
   const int64_t local = tile - tile_start[lo];
   const int ntm = (ds.rows + TM - 1) / TM;
   const int tm = (int)(local % ntm), tn = (int)(local / ntm);
-  const double2* A = Abase + ds.aoff;
-  const double2* W = Wbase + ds.woff;
-  double2* C = Cbase + ds.coff;
+  const double2* A = ds.A;
+  const double2* W = ds.W;
+  double2* C = ds.C;
   const int tid = threadIdx.x;
   const int tr = tid % 16, tc = tid / 16;  // rows tr + 16 a, cols tc + 8 b
   double2 acc[4][4];
@@ -798,6 +802,8 @@ void warm_recompress() {
   cudaFuncGetAttributes(&a, recompress_core<true, 128>);
   cudaFuncGetAttributes(&a, recompress_core<true, 256>);
   cudaFuncGetAttributes(&a, recompress_core<false, 256>);
+  cudaFuncGetAttributes(&a, recompress_core<false, 512>);
+  cudaFuncGetAttributes(&a, recompress_core<false, 1024>);
   cudaFuncGetAttributes(&a, form_gemm);
 }
 
@@ -821,19 +827,31 @@ int launch_recompress_core(Ctx& c, const RecDesc* d_desc, int64_t nblk, int kmax
       recompress_core<true, 256><<<(unsigned)nblk, 256, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
     }
   } else {
+    // large K: few long CTAs whose O(K^3) phases are L2-latency bound -> more warps
     const size_t smem = vec + sizeof(double2) * kGemmTile;
-    HMX_CUDA_TRY(
-        cudaFuncSetAttribute(recompress_core<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    recompress_core<false, 256><<<(unsigned)nblk, 256, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
+    const char* e_nt = std::getenv("HMX_RC_NT");
+    const int nt = e_nt ? std::atoi(e_nt) : 512;
+    if (nt == 1024) {
+      HMX_CUDA_TRY(cudaFuncSetAttribute(recompress_core<false, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                        (int)smem));
+      recompress_core<false, 1024><<<(unsigned)nblk, 1024, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
+    } else if (nt == 256) {
+      HMX_CUDA_TRY(
+          cudaFuncSetAttribute(recompress_core<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      recompress_core<false, 256><<<(unsigned)nblk, 256, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
+    } else {
+      HMX_CUDA_TRY(
+          cudaFuncSetAttribute(recompress_core<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      recompress_core<false, 512><<<(unsigned)nblk, 512, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
+    }
   }
   HMX_CUDA_TRY(cudaGetLastError());
   return HMX_OK;
 }
 
-int launch_form(Ctx& c, const FormDesc* d_desc, int64_t nitems, int64_t ntiles_total, const int64_t* d_tile_start,
-                const double2* A, const double2* W, double2* C) {
+int launch_form(Ctx& c, const FormDesc* d_desc, int64_t nitems, int64_t ntiles_total, const int64_t* d_tile_start) {
   if (ntiles_total == 0) return HMX_OK;
-  form_gemm<<<(unsigned)ntiles_total, kFormThreads, 0, c.stream>>>(d_desc, d_tile_start, nitems, A, W, C);
+  form_gemm<<<(unsigned)ntiles_total, kFormThreads, 0, c.stream>>>(d_desc, d_tile_start, nitems);
   HMX_CUDA_TRY(cudaGetLastError());
   return HMX_OK;
 }
