@@ -43,6 +43,8 @@ def parse():
     ap.add_argument("--impl", default="hmx", choices=["hmx", "reference"])
     ap.add_argument("--config", default="U32k")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-solve", action="store_true", help="skip the T65k time-to-solve run")
+    ap.add_argument("--solve-config", default="T65k")
     return ap.parse_args()
 
 
@@ -208,6 +210,44 @@ def reference_arm(args):
 
 
 # ----------------------------------------------------------------------------------------------
+def time_to_solve(tag, device):
+    """BASELINE config 5: assembly + GMRES(restart 50, tol 1e-4) on the
+    elastodynamic T kernel, seeded complex Gaussian RHS; device-timed phases
+    plus the host tree build."""
+    import torch
+
+    import paper_1706_09384_b200 as hmx
+    from paper_1706_09384_b200.configs import WORKLOADS
+
+    w = WORKLOADS[tag]
+    t0 = time.perf_counter()
+    cloud = hmx.make_geometry("sphere", w.n_points, 1.0, d=w.d)
+    ct = hmx.build_cluster_tree(cloud, w.n_leaf)
+    bt = hmx.build_block_tree(ct, ct, w.eta)
+    t_tree = time.perf_counter() - t0
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    H, rep = hmx.assemble(w.spec(), cloud, ct, bt, hmx.ACAConfig(eps_aca=w.eps), device=device)
+    t_asm = time.perf_counter() - t0
+    st = H.stats()
+    n = w.d * w.n_points
+    rng = np.random.default_rng(SEED)
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    t0 = time.perf_counter()
+    res = hmx.solve_gmres(H, b, hmx.GmresConfig(tol=1e-4, restart=50))
+    t_gm = time.perf_counter() - t0
+    r = b - hmx.matvec(H, res.x)
+    out = {"workload": tag, "n_points": w.n_points, "ks": w.ks, "iterations": res.iters,
+           "converged": res.converged, "true_rel_residual": float(np.linalg.norm(r) / np.linalg.norm(b)),
+           "assembly_ms": st["t_total_ms"], "assembly_wall_s": t_asm, "gmres_s": t_gm, "tree_build_s": t_tree,
+           "time_to_solve_s": st["t_total_ms"] * 1e-3 + t_gm,
+           "time_to_solve_with_tree_s": st["t_total_ms"] * 1e-3 + t_gm + t_tree,
+           "max_rank_before": rep.max_rank_before, "max_rank_after": rep.max_rank_after,
+           "matvec_bytes": st["matvec_bytes"]}
+    del H
+    return out
+
+
 def hmx_arm(args):
     import torch
 
@@ -292,15 +332,19 @@ def hmx_arm(args):
     # ---- roofline of the dominant kernel (phase 2: row-stream GEMV)
     nc = max(int(ncalls.value), 1)
     p1_ms, p2_ms = ph[1] / nc, ph[2] / nc
-    p2_gbs = st["phase2_bytes"] / (p2_ms * 1e-3) / 1e9
-    p1_gbs = st["phase1_bytes"] / (p1_ms * 1e-3) / 1e9
+    fused = p2_ms == 0.0  # phases 1 + 2 in one launch (mv_fused)
+    if fused:
+        dom_kernel, dom_bytes, dom_ms = "mv_fused", st["phase1_bytes"] + st["phase2_bytes"], p1_ms
+    else:
+        dom_kernel, dom_bytes, dom_ms = "mv_phase2", st["phase2_bytes"], p2_ms
+    dom_gbs = dom_bytes / (dom_ms * 1e-3) / 1e9
     hbm_peak = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
         try:
             with open(prof) as f:
-                traffic = json.load(f).get(args.config, {}).get("mv_phase2")
+                traffic = json.load(f).get(args.config, {}).get(dom_kernel)
         except Exception:
             traffic = None
     # ---- assembly roofline (FP64)
@@ -324,15 +368,18 @@ def hmx_arm(args):
         "gpu_launches": 4 * K,
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
                 "ms_per_step": e2e_ms / K},
-        "roofline": {"bound": "hbm", "kernel": "mv_phase2", "achieved": p2_gbs, "peak": hbm_peak,
-                     "unit": "GB/s", "frac": p2_gbs / hbm_peak, "traffic": traffic,
+        "roofline": {"bound": "hbm", "kernel": dom_kernel, "achieved": dom_gbs, "peak": hbm_peak,
+                     "unit": "GB/s", "frac": dom_gbs / hbm_peak, "traffic": traffic,
                      "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
                      else "fallback 6.65 TB/s (B200_PROFILING.md)",
-                     "bytes_per_launch": st["phase2_bytes"], "ms_per_launch": p2_ms,
+                     "bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms,
                      "whole_matvec_frac": (mv_bytes / (ms_max / K * 1e-3) / 1e9) / hbm_peak,
                      "vs_8TBps": (mv_bytes / (ms_max / K * 1e-3) / 1e9) / 8000.0},
-        "matvec_phases": {"gather_ms": ph[0] / nc, "vhx_ms": p1_ms, "vhx_GBps": p1_gbs, "row_gemv_ms": p2_ms,
-                          "row_gemv_GBps": p2_gbs, "finalize_ms": ph[3] / nc, "bytes": mv_bytes},
+        "matvec_phases": ({"gather_ms": ph[0] / nc, "fused_vhx_row_gemv_ms": p1_ms, "fused_GBps": dom_gbs,
+                           "finalize_ms": ph[3] / nc, "bytes": mv_bytes} if fused else
+                          {"gather_ms": ph[0] / nc, "vhx_ms": p1_ms,
+                           "vhx_GBps": st["phase1_bytes"] / (p1_ms * 1e-3) / 1e9, "row_gemv_ms": p2_ms,
+                           "row_gemv_GBps": dom_gbs, "finalize_ms": ph[3] / nc, "bytes": mv_bytes}),
         "assembly": {"ms": st["t_total_ms"], "wall_s": t_asm_wall, "tree_build_s": t_tree,
                      "aca_ms": st["t_aca_ms"], "recompress_ms": st["t_recompress_ms"],
                      "dense_ms": st["t_dense_ms"], "form_ms": st["t_form_ms"],
@@ -344,6 +391,8 @@ def hmx_arm(args):
                      "tau": rep.tau, "aca_passes": st["aca_passes"]},
         "clocks": clocks,
     }
+    if not args.no_solve:
+        line["time_to_solve"] = time_to_solve(args.solve_config, local)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             r = run_cpu(args.config, steps=50, warmup=1, budget_s=15.0)
