@@ -160,6 +160,8 @@ int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const 
 // recompress.cu
 // recompress_core keeps E and the QL eigenvector matrix in shared memory up to this ACA rank
 constexpr int kRecompressSmemMax = 112;
+// ... and R, T / L_r as well (3 K^2 complex) up to this one
+constexpr int kRecompressAllSmemMax = 0;  // measured no faster
 struct RecDesc {
   int64_t goff;      // Gram pair (G_U at goff, G_V at goff + kcap*kcap), ld = kcap
   int64_t woff;      // K x K scratch workspace (2 matrices) offset

@@ -494,11 +494,15 @@ HMX_D void recompress_truncate(const double* lam, const int* ordr, int K, double
 
 // Workspace per leaf, 6 K x K complex slots: 0 R, 1 T then L_r, 2 E (global
 // variant), 3 Z (real, global variant), 4-5 W_U | W_V.
-template <bool SMEM, int NT>
+// MODE 0: E, Z, R, T in L2 (large K); 1: E / Z in shared memory; 2: E / Z, R and
+// T / L_r all in shared memory (small K: the O(K) sequential phases then run
+// at shared-memory instead of L2 latency)
+template <int MODE, int NT>
 __global__ void __launch_bounds__(NT) recompress_core(const RecDesc* __restrict__ desc, double eps, int rule,
                                                             const double2* __restrict__ G, double2* __restrict__ W,
                                                             int32_t* __restrict__ rank_out,
                                                             int32_t* __restrict__ flags_out) {
+  constexpr bool SMEM = MODE >= 1;
   extern __shared__ double2 dyn[];
   __shared__ double red[2 * (NT / 32)];
   __shared__ Scalars S;
@@ -517,9 +521,10 @@ __global__ void __launch_bounds__(NT) recompress_core(const RecDesc* __restrict_
   const double2* GU = G + ds.goff;
   const double2* GV = GU + (int64_t)kcap * kcap;
   const int64_t KK = (int64_t)K * K;
-  double2* A = W + ds.woff;  // R (upper)
-  double2* B = A + KK;       // T, then L_r (K x r)
-  double2* Wuv = A + 4 * KK;
+  double2* gA = W + ds.woff;  // this leaf's L2 workspace
+  double2* A = gA;            // R (upper)
+  double2* B = gA + KK;       // T, then L_r (K x r)
+  double2* Wuv = gA + 4 * KK;
   // shared: 2K complex vectors, K complex tau, then 6K doubles (d, e, lam, dscale, rc, rs), K ints
   double2* vbuf = dyn;
   double2* pbuf = vbuf + K;
@@ -540,6 +545,10 @@ __global__ void __launch_bounds__(NT) recompress_core(const RecDesc* __restrict_
     E = gtile;  // no GEMM tiles in the shared-memory variant
     Z = reinterpret_cast<double*>(E);  // overlays E after the reduction (8 K (K+1) <= 16 K^2 bytes)
     ldz = K + 1;
+    if (MODE == 2) {
+      A = E + KK;
+      B = A + KK;
+    }
   } else {
     E = A + 2 * KK;
     Z = reinterpret_cast<double*>(A + 3 * KK);
@@ -646,7 +655,7 @@ __global__ void __launch_bounds__(NT) recompress_core(const RecDesc* __restrict_
     // near-degenerate eigenvalues: implicit QL with accumulated vectors
     if (SMEM) {
       // reflectors to L2 (workspace slot 2); Z reuses E's shared memory
-      Hv = A + 2 * KK;
+      Hv = gA + 2 * KK;
       for (int t = tid; t < K * K; t += NT) {
         const int i = t % K, j = t / K;
         if (i > j) Hv[t] = E[t];
@@ -799,11 +808,12 @@ __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __rest
 
 void warm_recompress() {
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, recompress_core<true, 128>);
-  cudaFuncGetAttributes(&a, recompress_core<true, 256>);
-  cudaFuncGetAttributes(&a, recompress_core<false, 256>);
-  cudaFuncGetAttributes(&a, recompress_core<false, 512>);
-  cudaFuncGetAttributes(&a, recompress_core<false, 1024>);
+  cudaFuncGetAttributes(&a, recompress_core<2, 128>);
+  cudaFuncGetAttributes(&a, recompress_core<1, 128>);
+  cudaFuncGetAttributes(&a, recompress_core<1, 256>);
+  cudaFuncGetAttributes(&a, recompress_core<0, 256>);
+  cudaFuncGetAttributes(&a, recompress_core<0, 512>);
+  cudaFuncGetAttributes(&a, recompress_core<0, 1024>);
   cudaFuncGetAttributes(&a, form_gemm);
 }
 
@@ -815,16 +825,22 @@ int launch_recompress_core(Ctx& c, const RecDesc* d_desc, int64_t nblk, int kmax
     return HMX_EINVAL;
   }
   const size_t vec = sizeof(double2) * 3 * (size_t)kmax + sizeof(double) * 6 * kmax + sizeof(int) * (kmax + 4) + 32;
-  if (kmax <= kRecompressSmemMax) {
+  const char* e_all = std::getenv("HMX_RC_ALLSMEM_MAX");
+  const int all_max = e_all ? std::atoi(e_all) : kRecompressAllSmemMax;
+  if (kmax <= all_max) {
+    const size_t smem = vec + 3 * sizeof(double2) * (size_t)kmax * kmax;
+    HMX_CUDA_TRY(cudaFuncSetAttribute(recompress_core<2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    recompress_core<2, 128><<<(unsigned)nblk, 128, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
+  } else if (kmax <= kRecompressSmemMax) {
     const size_t smem = vec + sizeof(double2) * (size_t)kmax * kmax;
     if (kmax <= 64) {
       HMX_CUDA_TRY(
-          cudaFuncSetAttribute(recompress_core<true, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      recompress_core<true, 128><<<(unsigned)nblk, 128, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
+          cudaFuncSetAttribute(recompress_core<1, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      recompress_core<1, 128><<<(unsigned)nblk, 128, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
     } else {
       HMX_CUDA_TRY(
-          cudaFuncSetAttribute(recompress_core<true, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      recompress_core<true, 256><<<(unsigned)nblk, 256, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
+          cudaFuncSetAttribute(recompress_core<1, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      recompress_core<1, 256><<<(unsigned)nblk, 256, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
     }
   } else {
     // large K: few long CTAs whose O(K^3) phases are L2-latency bound -> more warps
@@ -832,17 +848,17 @@ int launch_recompress_core(Ctx& c, const RecDesc* d_desc, int64_t nblk, int kmax
     const char* e_nt = std::getenv("HMX_RC_NT");
     const int nt = e_nt ? std::atoi(e_nt) : 512;
     if (nt == 1024) {
-      HMX_CUDA_TRY(cudaFuncSetAttribute(recompress_core<false, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+      HMX_CUDA_TRY(cudaFuncSetAttribute(recompress_core<0, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));
-      recompress_core<false, 1024><<<(unsigned)nblk, 1024, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
+      recompress_core<0, 1024><<<(unsigned)nblk, 1024, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
     } else if (nt == 256) {
       HMX_CUDA_TRY(
-          cudaFuncSetAttribute(recompress_core<false, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      recompress_core<false, 256><<<(unsigned)nblk, 256, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
+          cudaFuncSetAttribute(recompress_core<0, 256>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      recompress_core<0, 256><<<(unsigned)nblk, 256, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
     } else {
       HMX_CUDA_TRY(
-          cudaFuncSetAttribute(recompress_core<false, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      recompress_core<false, 512><<<(unsigned)nblk, 512, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
+          cudaFuncSetAttribute(recompress_core<0, 512>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      recompress_core<0, 512><<<(unsigned)nblk, 512, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
     }
   }
   HMX_CUDA_TRY(cudaGetLastError());
