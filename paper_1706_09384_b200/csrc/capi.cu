@@ -606,8 +606,8 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     HMX_CUDA_TRY(cudaMemcpyAsync(d_rd, rd.data(), sizeof(RecDesc) * rd.size(), cudaMemcpyHostToDevice, c.stream));
     mark("recompress start");
     // shared-memory size classes (smem ~ 16 K^2 bytes): more CTAs per SM for small K
-    const int classes[] = {kMaxAcaCols, kRecompressSmemMax, 88, 64, 48, 32};
-    const int ncls = 6;
+    const int classes[] = {kMaxAcaCols, kRecompressSmemMax, 88, 72, 60, 48, 39, 30, 21};
+    const int ncls = (int)(sizeof(classes) / sizeof(classes[0]));
     size_t q0 = 0;
     // when issued on the auxiliary stream, only the large-K class stays there;
     // the shared-memory classes go to the main stream (ordered after this

@@ -313,16 +313,29 @@ __device__ void tridiag_ql(double* d, double* e, double* Z, int ldz, int K, doub
 // without the RRR machinery), orthonormalised by classical Gram-Schmidt twice
 // in descending-eigenvalue order.  A vector that is mostly in the span of the
 // previous ones (near-degenerate cluster) makes the caller fall back to QL.
-HMX_D int sturm_count(const double* d, const double* e2, int K, double x, double pivmin) {
-  double q = d[0] - x;
-  if (fabs(q) < pivmin) q = -pivmin;
-  int cnt = q < 0.0;
+// three shifts at once (independent recurrences interleave in the pipeline)
+HMX_D void sturm_count3(const double* d, const double* e2, int K, double x1, double x2, double x3, double pivmin,
+                        int& c1, int& c2, int& c3) {
+  double q1 = d[0] - x1, q2 = d[0] - x2, q3 = d[0] - x3;
+  if (fabs(q1) < pivmin) q1 = -pivmin;
+  if (fabs(q2) < pivmin) q2 = -pivmin;
+  if (fabs(q3) < pivmin) q3 = -pivmin;
+  int n1 = q1 < 0.0, n2 = q2 < 0.0, n3 = q3 < 0.0;
   for (int i = 1; i < K; ++i) {
-    q = (d[i] - x) - e2[i - 1] / q;
-    if (fabs(q) < pivmin) q = -pivmin;
-    cnt += q < 0.0;
+    const double di = d[i], ei = e2[i - 1];
+    q1 = (di - x1) - ei / q1;
+    q2 = (di - x2) - ei / q2;
+    q3 = (di - x3) - ei / q3;
+    if (fabs(q1) < pivmin) q1 = -pivmin;
+    if (fabs(q2) < pivmin) q2 = -pivmin;
+    if (fabs(q3) < pivmin) q3 = -pivmin;
+    n1 += q1 < 0.0;
+    n2 += q2 < 0.0;
+    n3 += q3 < 0.0;
   }
-  return cnt;
+  c1 = n1;
+  c2 = n2;
+  c3 = n3;
 }
 
 // lam_asc[j] = j-th smallest eigenvalue
@@ -372,15 +385,30 @@ __device__ void bisect_all(const double* d, const double* e, double* e2, int K, 
   const double span = fmax(fabs(lo), fabs(hi));
   lo -= 2.2e-16 * span * K + pivmin;
   hi += 2.2e-16 * span * K + pivmin;
+  // stop at max(2 ulp ||T||, 2 ulp |lambda|) + pivmin: LAPACK dstebz's default
+  // absolute tolerance (abstol = ulp ||T||), so eigenvalues far below ||T||
+  // (all truncated away) do not iterate down to their own relative precision
+  const double atol = 4.4e-16 * span + pivmin;
+  // multisection: 3 independent Sturm chains per step (ILP) -> 2 bits per step
   for (int j = tid; j < K; j += NT) {
     double a = lo, b = hi;
-    for (int it = 0; it < 80; ++it) {
-      if (b - a <= 4.4e-16 * fmax(fabs(a), fabs(b)) + pivmin) break;
-      const double mid = 0.5 * (a + b);
-      if (sturm_count(d, e2, K, mid, pivmin) > j)
-        b = mid;
-      else
-        a = mid;
+    for (int it = 0; it < 40; ++it) {
+      if (b - a <= fmax(atol, 4.4e-16 * fmax(fabs(a), fabs(b)))) break;
+      const double h = 0.25 * (b - a);
+      const double x1 = a + h, x2 = a + 2.0 * h, x3 = b - h;
+      int c1, c2, c3;
+      sturm_count3(d, e2, K, x1, x2, x3, pivmin, c1, c2, c3);
+      if (c1 > j) {
+        b = x1;
+      } else if (c2 > j) {
+        a = x1;
+        b = x2;
+      } else if (c3 > j) {
+        a = x2;
+        b = x3;
+      } else {
+        a = x3;
+      }
     }
     lam_asc[j] = 0.5 * (a + b);
   }
