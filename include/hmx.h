@@ -137,6 +137,12 @@ int hmx_hmatrix_block_info(const hmx_hmatrix* h, int64_t* steps, int64_t* rank_b
                            int32_t* flags);
 /* copy leaf b out (layouts as in hmx_hmatrix_load) */
 int hmx_hmatrix_get_block(const hmx_hmatrix* h, int64_t b, double* a, double* v);
+/* delta_{H,F} estimator kernel (SPEC.md:507-515 estimate(): "for each AdmissibleLeaf regenerate the
+ * dense block from the kernel, accumulate ||A_block - U V*||_F^2").  Per leaf b:
+ * err2[b] = ||A_b - U_b V_b^H||_F^2 (0 for dense leaves), norm2[b] = ||A_b||_F^2 of the regenerated
+ * block (dense leaves include the self shift).  pts_tree / nrm_tree as in hmx_assemble. */
+int hmx_block_errors(hmx_hmatrix* h, const hmx_kernel* k, const double* pts_tree, const double* nrm_tree,
+                     int64_t n_points, double self_shift, double* err2, double* norm2);
 void hmx_hmatrix_free(hmx_hmatrix* h);
 
 /* ---- H-matvec / GMRES ---------------------------------------------------------- */

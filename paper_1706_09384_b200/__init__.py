@@ -11,7 +11,8 @@ from .errors import (FallbackNeeded, PivotExhaustionError, SingularEvaluationErr
 from .geometry import (AABB, AdmissibleLeaf, BlockTree, ClusterNode, ClusterTree, DenseLeaf,  # noqa: F401
                        PointCloud, Subdivided, build_block_tree, build_cluster_tree, diam_box,
                        dist_box, is_admissible, make_geometry, sparsity_pattern)
-from .hmatrix import HMatrix, StorageReport, assemble, matvec, storage_report  # noqa: F401
+from .estimate import EstimatorReport, estimate  # noqa: F401
+from .hmatrix import HMatrix, StorageReport, assemble, block_errors, matvec, storage_report  # noqa: F401
 from .kernels import (KernelSpec, Material, Wavenumbers, assemble_dense, elasto_t_block,  # noqa: F401
                       elasto_u_block, eval_elasto_t, eval_elasto_u, eval_scalar, scalar_block)
 from .lowrank import ACAConfig, LowRankFactor  # noqa: F401

@@ -66,6 +66,7 @@ SIGNATURES = {
     "hmx_hmatrix_stats": (C.c_int, [P, C.POINTER(HmxStats)]),
     "hmx_hmatrix_block_info": (C.c_int, [P, P, P, P, P]),
     "hmx_hmatrix_get_block": (C.c_int, [P, i64, P, P]),
+    "hmx_block_errors": (C.c_int, [P, P, P, P, i64, C.c_double, P, P]),
     "hmx_hmatrix_free": (None, [P]),
     "hmx_matvec": (C.c_int, [P, P, P, i32]),
     "hmx_matvec_profile": (C.c_int, [P, P, P, C.POINTER(C.c_float)]),

@@ -285,6 +285,7 @@ int hmx_ctx_create(int32_t device, hmx_ctx** out) {
   warm_dense();
   warm_matvec();
   warm_gmres();
+  warm_estimate();
   *out = c;
   return HMX_OK;
 }
@@ -1080,6 +1081,68 @@ int hmx_hmatrix_get_block(const hmx_hmatrix* h, int64_t b, double* a, double* v)
     for (int64_t l = 0; l < r; ++l) A[i * r + l] = tu[l * ld + i];
   for (int64_t i = 0; i < dn; ++i)
     for (int64_t l = 0; l < r; ++l) Vh[i * r + l] = tv[l * dn + i];
+  return HMX_OK;
+}
+
+int hmx_block_errors(hmx_hmatrix* h, const hmx_kernel* k, const double* pts_tree, const double* nrm_tree,
+                     int64_t n_points, double self_shift, double* err2, double* norm2) {
+  if (!h || !k || !pts_tree || !err2 || !norm2) return HMX_EINVAL;
+  DeviceH& H = h->H;
+  Ctx& c = *H.ctx;
+  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  const int d = k->kind == HMX_HELMHOLTZ ? 1 : 3;
+  if (d != H.d || n_points != H.np) {
+    hmx_set_error("hmx_block_errors: kernel / point count do not match the H-matrix");
+    return HMX_EINVAL;
+  }
+  if (k->kind == HMX_ELASTO_T && !nrm_tree) {
+    hmx_set_error("hmx_block_errors: elasto T needs normals");
+    return HMX_EINVAL;
+  }
+  const GreenParams P = make_params(k, 1, self_shift);
+  DevPoints pts;
+  int rc;
+  if ((rc = pts.upload(c, pts_tree, k->kind == HMX_ELASTO_T ? nrm_tree : nullptr, n_points))) return rc;
+  const int64_t nb = H.nb;
+  std::vector<ErrDesc> desc((size_t)nb);
+  std::vector<int64_t> tile_start((size_t)nb);
+  int64_t nt = 0;
+  for (int64_t b = 0; b < nb; ++b) {
+    ErrDesc& e = desc[b];
+    e.r0 = H.table[5 * b + 1];
+    e.c0 = H.table[5 * b + 3];
+    e.m = (int32_t)(H.table[5 * b + 2] - H.table[5 * b + 1]);
+    e.n = (int32_t)(H.table[5 * b + 4] - H.table[5 * b + 3]);
+    e.pad = 0;
+    const bool lowrank = H.table[5 * b] != 0;
+    e.r = lowrank ? (int32_t)H.rank_after[b] : 0;
+    e.U = lowrank ? H.d_row + H.leaf_moff[b] : nullptr;
+    e.V = lowrank ? H.d_v + H.leaf_voff[b] : nullptr;
+    e.ldu = H.leaf_ld[b];
+    tile_start[b] = nt;
+    nt += err_tiles_of(e.m, e.n);
+  }
+  if (nt >= (int64_t)INT32_MAX) {
+    hmx_set_error("hmx_block_errors: %lld tiles exceed one grid", (long long)nt);
+    return HMX_EINVAL;
+  }
+  DevBuf mem(c);
+  ErrDesc* d_desc;
+  int64_t* d_ts;
+  double2 *d_part, *d_out;
+  if ((rc = mem.alloc(&d_desc, nb)) || (rc = mem.alloc(&d_ts, nb)) || (rc = mem.alloc(&d_part, nt)) ||
+      (rc = mem.alloc(&d_out, nb)))
+    return rc;
+  HMX_CUDA_TRY(cudaMemcpyAsync(d_desc, desc.data(), sizeof(ErrDesc) * nb, cudaMemcpyHostToDevice, c.stream));
+  HMX_CUDA_TRY(cudaMemcpyAsync(d_ts, tile_start.data(), sizeof(int64_t) * nb, cudaMemcpyHostToDevice, c.stream));
+  if ((rc = launch_block_errors(c, d, P, pts.soa, d_desc, d_ts, nb, nt, d_part, d_out))) return rc;
+  std::vector<double2> out((size_t)nb);
+  HMX_CUDA_TRY(cudaMemcpyAsync(out.data(), d_out, sizeof(double2) * nb, cudaMemcpyDeviceToHost, c.stream));
+  HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  for (int64_t b = 0; b < nb; ++b) {
+    err2[b] = H.table[5 * b] != 0 ? out[b].x : 0.0;  // dense leaves are stored exactly
+    norm2[b] = out[b].y;
+  }
   return HMX_OK;
 }
 

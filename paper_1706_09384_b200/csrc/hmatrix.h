@@ -120,6 +120,7 @@ void warm_recompress();
 void warm_dense();
 void warm_matvec();
 void warm_gmres();
+void warm_estimate();
 
 // matvec.cu
 int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& seg_level);
@@ -178,6 +179,19 @@ struct FormDesc {
   int32_t pad;
 };
 int launch_form(Ctx& c, const FormDesc* d_desc, int64_t nitems, int64_t ntiles_total, const int64_t* d_tile_start);
+
+// estimate.cu: per-leaf ||A_b - U V^H||_F^2 and ||A_b||_F^2 by regeneration
+struct ErrDesc {
+  int64_t r0, c0;        // first row / column point (tree order)
+  int32_t m, n, r, pad;  // points, rank (0: dense leaf -> norm only)
+  const double2* U;      // d m x r, ld = ldu
+  const double2* V;      // d n x r, ld = d n
+  int64_t ldu;
+};
+int launch_block_errors(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const ErrDesc* d_desc,
+                        const int64_t* d_tile_start, int64_t nleaves, int64_t ntiles, double2* d_part,
+                        double2* d_out);
+int64_t err_tiles_of(int64_t m, int64_t n);
 
 // dense.cu: FP64 peak microbenchmark
 int bench_dfma(Ctx& c, double* tflops);

@@ -43,6 +43,7 @@ class HMatrix:
         self.spec = spec
         self.table = table
         self.device = device
+        self.self_shift = None
 
     def __del__(self):
         try:
@@ -154,7 +155,34 @@ def assemble(spec, cloud, ct, bt, cfg=ACAConfig(), self_shift=None, device=0):
                                        pts.shape[0], _lib.ptr(perm), _lib.ptr(table), len(table), C.byref(c),
                                        shift, C.byref(h)), "hmx_assemble")
     H = HMatrix(h, spec.d, pts.shape[0], block_tree=bt, perm=perm, spec=spec, table=bt.table, device=device)
+    H.self_shift = shift
     return H, storage_report(H)
+
+
+def block_errors(h, spec, cloud, self_shift=None):
+    """Per-leaf ||A_b - U_b V_b^H||_F^2 and ||A_b||_F^2 by regenerating every
+    leaf on the device (``hmx_block_errors``; the blockwise accumulation of
+    SPEC.md:510).  Dense leaves report error 0.  Returns (err2, norm2), one
+    entry per leaf in ``h.table`` order."""
+    if h.perm is None:
+        raise ValueError("block_errors needs the tree permutation of the H-matrix")
+    if spec.d != h.d:
+        raise ValueError("kernel dimension does not match the H-matrix")
+    pts = np.ascontiguousarray(np.asarray(cloud.points, dtype=np.float64)[h.perm])
+    nrm = None
+    if spec.variant == "elasto_t":
+        if cloud.normals is None:
+            raise ValueError("ElastoT requires normals on the cloud")
+        nrm = np.ascontiguousarray(np.asarray(cloud.normals, dtype=np.float64)[h.perm])
+    if self_shift is None:
+        self_shift = h.self_shift if h.self_shift is not None else float(cloud.size)
+    nb = len(h.table)
+    err2 = np.empty(nb, np.float64)
+    norm2 = np.empty(nb, np.float64)
+    kern = _spec_kernel(spec)
+    _lib.check(_lib.lib().hmx_block_errors(h.handle, C.byref(kern), _lib.ptr(pts), _lib.ptr(nrm), pts.shape[0],
+                                           float(self_shift), _lib.ptr(err2), _lib.ptr(norm2)), "hmx_block_errors")
+    return err2, norm2
 
 
 def storage_report(h):
