@@ -16,4 +16,5 @@ from .hmatrix import HMatrix, StorageReport, assemble, block_errors, matvec, sto
 from .kernels import (KernelSpec, Material, Wavenumbers, assemble_dense, elasto_t_block,  # noqa: F401
                       elasto_u_block, eval_elasto_t, eval_elasto_u, eval_scalar, scalar_block)
 from .lowrank import ACAConfig, LowRankFactor  # noqa: F401
+from .snapfile import snapshot  # noqa: F401
 from .solve import GmresConfig, solve_gmres  # noqa: F401

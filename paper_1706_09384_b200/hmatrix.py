@@ -85,7 +85,9 @@ class HMatrix:
             a = np.empty((dm, dn), np.complex128)
             _lib.check(_lib.lib().hmx_hmatrix_get_block(self._h, b, _lib.ptr(a), None), "get_block")
             return a
-        r = int(self.block_info()["rank_after"][b])
+        if getattr(self, "_ranks", None) is None:  # immutable H: cache the rank table
+            self._ranks = self.block_info()["rank_after"]
+        r = int(self._ranks[b])
         u = np.empty((dm, r), np.complex128)
         v = np.empty((dn, r), np.complex128)
         if r:

@@ -1,0 +1,138 @@
+"""H-matrix snapshots (SPEC.md:563-571 ``snapshot(save|load, path)``; SURVEY
+8(f) row 3): a versioned, checksummed binary image of an assembled H-matrix.
+
+Layout (little endian)::
+
+    b"HMXSNAP\\0" | u32 version | u64 header length | header (JSON)
+    | arrays: perm, table (nb x 5), steps, rank_before, rank_after, flags
+    | payload: every leaf in leaves() order -- dense (d m) x (d n), or
+      U (d m) x r then V (d n) x r, complex128 row-major
+    | SHA-256 of everything before it (32 bytes)
+
+``load`` rebuilds the device H-matrix through ``hmx_hmatrix_load`` with the
+same leaf table and ranks, so the streams, the matvec plan and therefore the
+matvec output are bitwise identical to the saved H-matrix's.  Errors
+(``errors.py:23-32``): wrong magic / version -> ``SnapshotVersionError``,
+checksum or size mismatch -> ``SnapshotCorruptError``.
+"""
+
+import hashlib
+import io
+import json
+import struct
+
+import numpy as np
+
+from .errors import SnapshotCorruptError, SnapshotVersionError
+from .hmatrix import HMatrix
+from .kernels import KernelSpec, Material
+
+MAGIC = b"HMXSNAP\0"
+VERSION = 1
+_ARRAYS = ("perm", "table", "steps", "rank_before", "rank_after", "flags")
+
+
+def _spec_json(spec):
+    if spec is None:
+        return None
+    m = spec.material
+    return {"variant": spec.variant, "kappa": spec.kappa,
+            "material": None if m is None else {"rho": m.rho, "mu": m.mu, "nu": m.nu, "omega": m.omega}}
+
+
+def _spec_from(js):
+    if js is None:
+        return None
+    m = js["material"]
+    return KernelSpec(js["variant"], js["kappa"], None if m is None else Material(**m))
+
+
+class _HashWriter:
+    def __init__(self, f):
+        self.f = f
+        self.h = hashlib.sha256()
+
+    def write(self, b):
+        b = memoryview(b).cast("B")
+        self.h.update(b)
+        self.f.write(b)
+
+
+def save(h, path):
+    """Write ``h`` to ``path``."""
+    info = h.block_info()
+    table = np.ascontiguousarray(np.asarray(h.table)[:, :5], dtype=np.int64)
+    perm = np.ascontiguousarray(h.perm, dtype=np.int64)
+    arrays = {"perm": perm, "table": table, "steps": info["steps"], "rank_before": info["rank_before"],
+              "rank_after": info["rank_after"], "flags": info["flags"]}
+    header = {"d": h.d, "n_points": h.n_points, "n_blocks": len(table), "self_shift": h.self_shift,
+              "spec": _spec_json(h.spec),
+              "arrays": {k: {"dtype": str(v.dtype), "shape": list(v.shape)} for k, v in arrays.items()}}
+    hb = json.dumps(header, sort_keys=True).encode()
+    with open(path, "wb") as f:
+        w = _HashWriter(f)
+        w.write(MAGIC)
+        w.write(struct.pack("<IQ", VERSION, len(hb)))
+        w.write(hb)
+        for k in _ARRAYS:
+            w.write(np.ascontiguousarray(arrays[k]).tobytes())
+        for b in range(len(table)):
+            p = h.block(b)
+            if table[b, 0] == 0:
+                w.write(np.ascontiguousarray(p).tobytes())
+            else:
+                w.write(np.ascontiguousarray(p.u).tobytes())
+                w.write(np.ascontiguousarray(p.v).tobytes())
+        f.write(w.h.digest())
+
+
+def load(path, device=0):
+    """Read a snapshot written by :func:`save` back onto ``device``."""
+    with open(path, "rb") as f:
+        raw = f.read()
+    if len(raw) < len(MAGIC) + 12 + 32 or raw[:len(MAGIC)] != MAGIC:
+        raise SnapshotVersionError("not an hmx snapshot")
+    version, hlen = struct.unpack_from("<IQ", raw, len(MAGIC))
+    if version != VERSION:
+        raise SnapshotVersionError(f"snapshot version {version}, this build reads {VERSION}")
+    body, digest = raw[:-32], raw[-32:]
+    if hashlib.sha256(body).digest() != digest:
+        raise SnapshotCorruptError("snapshot checksum mismatch")
+    buf = io.BytesIO(body)
+    buf.seek(len(MAGIC) + 12)
+    header = json.loads(buf.read(hlen))
+    arrays = {}
+    for k in _ARRAYS:
+        meta = header["arrays"][k]
+        dt = np.dtype(meta["dtype"])
+        n = int(np.prod(meta["shape"])) if meta["shape"] else 1
+        arrays[k] = np.frombuffer(buf.read(n * dt.itemsize), dtype=dt).reshape(meta["shape"])
+    d, table, ranks = header["d"], arrays["table"], arrays["rank_after"]
+    payload = []
+    for b in range(len(table)):
+        dm, dn = d * int(table[b, 2] - table[b, 1]), d * int(table[b, 4] - table[b, 3])
+        if table[b, 0] == 0:
+            payload.append(np.frombuffer(buf.read(16 * dm * dn), np.complex128).reshape(dm, dn))
+        else:
+            r = int(ranks[b])
+            u = np.frombuffer(buf.read(16 * dm * r), np.complex128).reshape(dm, r)
+            v = np.frombuffer(buf.read(16 * dn * r), np.complex128).reshape(dn, r)
+            payload.append((u, v))
+    if buf.tell() != len(body):
+        raise SnapshotCorruptError("snapshot payload size mismatch")
+    H = HMatrix.from_factors(d, header["n_points"], arrays["perm"], table, payload, device=device)
+    H.spec = _spec_from(header["spec"])
+    H.self_shift = header["self_shift"]
+    return H
+
+
+def snapshot(op, path, h=None, device=0):
+    """SPEC.md:563 ``snapshot(save|load, path)``."""
+    if op == "save":
+        if h is None:
+            raise ValueError("snapshot('save', path, h): no H-matrix given")
+        save(h, path)
+        return h
+    if op == "load":
+        return load(path, device=device)
+    raise ValueError(f"unknown snapshot op {op!r}")
