@@ -44,6 +44,7 @@ def parse():
     ap.add_argument("--config", default="U32k")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true", help="skip the T65k time-to-solve run")
+    ap.add_argument("--no-estimate", action="store_true", help="skip the delta_{H,F} estimator timing")
     ap.add_argument("--solve-config", default="T65k")
     return ap.parse_args()
 
@@ -391,6 +392,26 @@ def hmx_arm(args):
                      "tau": rep.tau, "aca_passes": st["aca_passes"]},
         "clocks": clocks,
     }
+    if not args.no_estimate:
+        # delta_{H,F} estimator: every leaf regenerated on the device
+        from paper_1706_09384_b200.hmatrix import block_errors
+
+        ra = H.block_info()["rank_after"].astype(np.float64)
+        tb = np.asarray(bt.leaf_table)
+        mn = ((tb[:, 2] - tb[:, 1]) * (tb[:, 4] - tb[:, 3])).astype(np.float64)
+        est_flops = float(np.sum(mn * (8.0 * w.d * w.d * ra + PAIR_FLOPS[w.kind])))
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        err2, norm2 = block_errors(H, spec, cloud)
+        t_est = time.perf_counter() - t0
+        adm = tb[:, 0] == 1
+        ratio = np.sqrt(err2[adm] / norm2[adm]) / w.eps
+        line["estimator"] = {"wall_s": t_est, "pairs": float(mn.sum()), "fp64_flops": est_flops,
+                             "fp64_tflops": est_flops / t_est / 1e12,
+                             "fp64_frac": est_flops / t_est / 1e12 / dfma.value,
+                             "delta_h_frob_rel": float(np.sqrt(err2.sum() / norm2.sum())),
+                             "worst_leaf_eps": float(ratio.max()), "leaves_above_eps": int((ratio > 1).sum()),
+                             "leaves_above_3eps": int((ratio > 3).sum())}
     if not args.no_solve:
         line["time_to_solve"] = time_to_solve(args.solve_config, local)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
