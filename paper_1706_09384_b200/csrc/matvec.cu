@@ -2,7 +2,7 @@
 //
 // One pass over the packed HBM streams (layout in hmatrix.h):
 //   gather    x_tree[d k + a] = x[d perm[k] + a]                      (tree order)
-//   phase 1   warp per job: s[slot] = V_b(:, l)^H x_tree(cols of b)   (low-rank)
+//   phase 1   warp per job: s[slot..+4] = V_b(:, l..l+4)^H x_tree(cols of b)   (low-rank)
 //             or s[slot..] = x_tree(cols of b)                        (dense)
 //   phase 2   CTA per (row segment, 256-row tile): y_lev[level][rows] =
 //             M_g(rows, :) s_g -- column-major M_g, lanes over rows so each
@@ -36,6 +36,11 @@ __global__ void mv_gather(const double2* __restrict__ x, const int64_t* __restri
   }
 }
 
+// Phase-1 job: kind 0 copies x pieces of a dense leaf into its slots; kind
+// k = 1..4 computes k consecutive columns t_c = V(:, l + c)^H x of a low-rank
+// leaf (x loaded once for the k columns, 2 k + 2 loads in flight per lane), then
+// one butterfly reduce-scatter of the 2 x 4 partial sums over the warp.
+constexpr int kColsPerJob = 4;
 __global__ void __launch_bounds__(kThreads) mv_phase1(const MvJob1* __restrict__ jobs, int64_t njobs,
                                                          const double2* __restrict__ V,
                                                          const double2* __restrict__ xt, double2* __restrict__ s) {
@@ -50,20 +55,62 @@ __global__ void __launch_bounds__(kThreads) mv_phase1(const MvJob1* __restrict__
       continue;
     }
     const double2* vp = V + J.voff;
-    double2 a0 = cmk(0, 0), a1 = cmk(0, 0);
+    const int64_t len = J.len;
+    const int nc = J.kind;
+    double2 acc[kColsPerJob];
+#pragma unroll
+    for (int c = 0; c < kColsPerJob; ++c) acc[c] = cmk(0, 0);
     int q = lane;
-    // 4 independent 16-byte loads of V in flight per lane
-    for (; q + 96 < J.len; q += 128) {
-      const double2 v0 = __ldcs(vp + q), v1 = __ldcs(vp + q + 32), v2 = __ldcs(vp + q + 64),
-                    v3 = __ldcs(vp + q + 96);
-      a0 = cfma_ca(v0, xp[q], a0);
-      a1 = cfma_ca(v1, xp[q + 32], a1);
-      a0 = cfma_ca(v2, xp[q + 64], a0);
-      a1 = cfma_ca(v3, xp[q + 96], a1);
+    if (nc == kColsPerJob) {
+      for (; q + 32 < J.len; q += 64) {
+        const double2 x0 = xp[q], x1 = xp[q + 32];
+        double2 v0[kColsPerJob], v1[kColsPerJob];
+#pragma unroll
+        for (int c = 0; c < kColsPerJob; ++c) {
+          v0[c] = __ldcs(vp + c * len + q);
+          v1[c] = __ldcs(vp + c * len + q + 32);
+        }
+#pragma unroll
+        for (int c = 0; c < kColsPerJob; ++c) acc[c] = cfma_ca(v1[c], x1, cfma_ca(v0[c], x0, acc[c]));
+      }
+      for (; q < J.len; q += 32) {
+        const double2 x0 = xp[q];
+#pragma unroll
+        for (int c = 0; c < kColsPerJob; ++c) acc[c] = cfma_ca(__ldcs(vp + c * len + q), x0, acc[c]);
+      }
+    } else {
+      for (; q < J.len; q += 32) {
+        const double2 x0 = xp[q];
+#pragma unroll
+        for (int c = 0; c < kColsPerJob; ++c)
+          if (c < nc) acc[c] = cfma_ca(__ldcs(vp + c * len + q), x0, acc[c]);
+      }
     }
-    for (; q < J.len; q += 32) a0 = cfma_ca(__ldcs(vp + q), xp[q], a0);
-    double2 acc = warp_sum(cadd(a0, a1));
-    if (lane == 0) s[J.soff] = acc;
+    // reduce-scatter of v[ri * 4 + c] over the 32 lanes (stages 16, 8, 4 halve
+    // the vector, 2 and 1 finish the sum): lane 4 t holds (ri, c) = (t >> 2, t & 3)
+    double v[2 * kColsPerJob];
+#pragma unroll
+    for (int c = 0; c < kColsPerJob; ++c) {
+      v[c] = acc[c].x;
+      v[kColsPerJob + c] = acc[c].y;
+    }
+#pragma unroll
+    for (int st = 0; st < 3; ++st) {
+      const int mask = 16 >> st, half = kColsPerJob >> st;
+      const bool hi = (lane & mask) != 0;
+#pragma unroll
+      for (int i = 0; i < half; ++i) {
+        const double send = hi ? v[i] : v[i + half];
+        const double keep = hi ? v[i + half] : v[i];
+        v[i] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+      }
+    }
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
+    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
+    if ((lane & 3) == 0) {
+      const int ri = (lane >> 4) & 1, c = ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+      if (c < nc) reinterpret_cast<double*>(s + J.soff + c)[ri] = v[0];
+    }
   }
 }
 
@@ -203,7 +250,7 @@ int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
   std::vector<int64_t> slot((size_t)maxlen + 2, 0);
   for (int64_t b = 0; b < nb; ++b) {
     const int32_t len = (int32_t)(d * (H.table[5 * b + 4] - H.table[5 * b + 3]));
-    slot[(size_t)(maxlen - len) + 1] += H.table[5 * b] == 0 ? 1 : H.rank_after[b];
+    slot[(size_t)(maxlen - len) + 1] += H.table[5 * b] == 0 ? 1 : hmx_cdiv(H.rank_after[b], kColsPerJob);
   }
   for (size_t i = 1; i < slot.size(); ++i) slot[i] += slot[i - 1];
   std::vector<MvJob1> jobs((size_t)slot.back());
@@ -222,8 +269,9 @@ int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
     } else {
       const int64_t r = H.rank_after[b];
       H.leaf_voff[b] = vo;
-      for (int64_t l = 0; l < r; ++l)
-        jobs[(size_t)pos++] = MvJob1{vo + l * d * n, d * c0, soff[g] + colstart[b] + l, (int32_t)(d * n), 1};
+      for (int64_t l = 0; l < r; l += kColsPerJob)
+        jobs[(size_t)pos++] = MvJob1{vo + l * d * n, d * c0, soff[g] + colstart[b] + l, (int32_t)(d * n),
+                                     (int32_t)std::min<int64_t>(kColsPerJob, r - l)};
       vo += d * n * r;
       lr_b += 16.0 * r * d * (m + n);
     }
