@@ -40,7 +40,7 @@ __global__ void mv_gather(const double2* __restrict__ x, const int64_t* __restri
 // k = 1..4 computes k consecutive columns t_c = V(:, l + c)^H x of a low-rank
 // leaf (x loaded once for the k columns, 2 k + 2 loads in flight per lane), then
 // one butterfly reduce-scatter of the 2 x 4 partial sums over the warp.
-constexpr int kColsPerJob = 4;
+constexpr int kColsPerJob = 4;  // 8 measured 13% slower (fewer, longer jobs)
 __global__ void __launch_bounds__(kThreads) mv_phase1(const MvJob1* __restrict__ jobs, int64_t njobs,
                                                          const double2* __restrict__ V,
                                                          const double2* __restrict__ xt, double2* __restrict__ s) {
@@ -86,17 +86,21 @@ __global__ void __launch_bounds__(kThreads) mv_phase1(const MvJob1* __restrict__
           if (c < nc) acc[c] = cfma_ca(__ldcs(vp + c * len + q), x0, acc[c]);
       }
     }
-    // reduce-scatter of v[ri * 4 + c] over the 32 lanes (stages 16, 8, 4 halve
-    // the vector, 2 and 1 finish the sum): lane 4 t holds (ri, c) = (t >> 2, t & 3)
-    double v[2 * kColsPerJob];
+    // reduce-scatter of v[ri * C + c] over the 32 lanes: the first log2(2C)
+    // xor stages halve the vector each lane carries, the rest finish the sum;
+    // lane (q << kFin) holds value q = (ri, c) in bit-reversed-free order
+    constexpr int NV = 2 * kColsPerJob;
+    constexpr int kHalv = NV == 8 ? 3 : (NV == 16 ? 4 : 5);
+    constexpr int kFin = 5 - kHalv;
+    double v[NV];
 #pragma unroll
     for (int c = 0; c < kColsPerJob; ++c) {
       v[c] = acc[c].x;
       v[kColsPerJob + c] = acc[c].y;
     }
 #pragma unroll
-    for (int st = 0; st < 3; ++st) {
-      const int mask = 16 >> st, half = kColsPerJob >> st;
+    for (int st = 0; st < kHalv; ++st) {
+      const int mask = 16 >> st, half = (NV / 2) >> st;
       const bool hi = (lane & mask) != 0;
 #pragma unroll
       for (int i = 0; i < half; ++i) {
@@ -105,10 +109,11 @@ __global__ void __launch_bounds__(kThreads) mv_phase1(const MvJob1* __restrict__
         v[i] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
       }
     }
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 2);
-    v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1);
-    if ((lane & 3) == 0) {
-      const int ri = (lane >> 4) & 1, c = ((lane >> 3) & 1) * 2 + ((lane >> 2) & 1);
+#pragma unroll
+    for (int st = 0; st < kFin; ++st) v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1 << st);
+    if ((lane & ((1 << kFin) - 1)) == 0) {
+      const int q = lane >> kFin;  // bits of q (MSB first) = the halving choices
+      const int ri = q / kColsPerJob, c = q % kColsPerJob;
       if (c < nc) reinterpret_cast<double*>(s + J.soff + c)[ri] = v[0];
     }
   }
