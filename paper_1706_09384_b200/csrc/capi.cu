@@ -18,6 +18,7 @@
 #include <cmath>
 #include <cstring>
 #include <string>
+#include <map>
 #include <vector>
 
 #include "../../include/hmx.h"
@@ -546,8 +547,18 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
                        (hi3[2] - lo3[2]) * (hi3[2] - lo3[2]));
     };
     const double floor_cols = d == 1 ? 36.0 : 60.0;
+    // clusters are shared by many leaves: one box per distinct (start, stop)
+    std::map<std::pair<int64_t, int64_t>, double> dcache;
+    auto diam_c = [&](int64_t a0, int64_t a1) {
+      auto it = dcache.find({a0, a1});
+      if (it != dcache.end()) return it->second;
+      const double v = diam(a0, a1);
+      dcache.emplace(std::make_pair(a0, a1), v);
+      return v;
+    };
     for (int64_t b : adm) {
-      const double dm = std::max(diam(table[5 * b + 1], table[5 * b + 2]), diam(table[5 * b + 3], table[5 * b + 4]));
+      const double dm =
+          std::max(diam_c(table[5 * b + 1], table[5 * b + 2]), diam_c(table[5 * b + 3], table[5 * b + 4]));
       const int64_t est = round_d((int64_t)std::ceil(floor_cols + 2.0 * d * kap * dm) + d - 1);
       kcap[b] = std::min<int64_t>(maxr[b], std::min<int64_t>(est, round_d(kMaxAcaCols)));
     }
