@@ -19,7 +19,7 @@ HEADERS = ["hmx_common.cuh", "green.cuh", "hmatrix.h", "hmx_host.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-ffp-contract=off",
-         "-diag-suppress", "128,550"]
+         "-diag-suppress", "128,550"] + os.environ.get("HMX_NVCC_EXTRA", "").split()
 
 
 def _newest_dep():

@@ -6,8 +6,8 @@
 // this kernel implement the same step sequence, so pivots agree except on
 // roundoff-level near-ties (ranks compared +/-1 in tests/test_gpu_parity.py).
 //
-// Mapping: one CTA (256 threads) per admissible block, blocks taken in LPT
-// order (largest first).  Per step:
+// Mapping: one CTA per admissible block (512 threads for large blocks, 128 for
+// small ones), blocks taken in LPT order (largest first).  Per step:
 //   row pass   thread per column point j: Green's d x d block of (i_piv, j)
 //              minus U(i_piv,:) V(j,:)^H  -> written conjugated as the new V
 //              columns (v_k = R_row^H), sigma_1 / sigma_3 per sub-block,
@@ -15,29 +15,40 @@
 //   pivot      gamma = R(i_piv, j_piv)^{-1}
 //   col pass   thread per row point i: (i, j_piv) block minus U(i,:) V(j_piv,:)^H,
 //              sigma_3 over unvisited rows -> next row pivot, u_k = R_col gamma
-//   Gram pass  warp per 4 factor columns: G_U(:, K:K+d) = U^H u_k and
-//              G_V(:, K:K+d) = V^H v_k (these Gram matrices are reused by the
-//              recompression, so the exact ||B_k||_F update of SPEC.md:338
-//              costs no extra pass over the factors)
-//   decision   thread 0: ||B_k||^2 update, stop test ||u|| ||v|| <= eps ||B_k||.
+//   Gram pass  G_U(:, new) = U^H u_new, G_V(:, new) = V^H v_new, warp per
+//              kGramGroup factor columns, lanes over rows (these Gram matrices
+//              give the exact ||B_k||_F update of SPEC.md:338 and are reused by
+//              the recompression)
+//   decision   ||B_k||^2 update, stop test ||u|| ||v|| <= eps ||B_k||.
+// The Gram pass re-streams both factor panels from HBM (they do not fit in a
+// CTA's share of L2), so it is run once per kGramBatch steps for all their new
+// columns together: the stop decisions of the batched steps are then taken in
+// order, and a step after the one that stops is discarded (it was speculative:
+// nothing the decision reads depends on it).  Where a step cannot run (column
+// capacity, max rank, no unvisited row, zero residual row, sigma_3 fallback)
+// the pending steps are resolved first, so every outcome is the one the
+// sequential algorithm produces.
 // The residual strips are written straight into the factor storage; U/V are
 // column-major with ld = d m / d n, the U(i_piv,:) and V(j_piv,:) rows are
 // staged in shared memory.
 #include <cstdio>
 #include <cstdlib>
 
-#include <cooperative_groups.h>
-
 #include "green.cuh"
 #include "hmatrix.h"
-
-namespace cg = cooperative_groups;
 
 namespace hmx {
 
 namespace {
 
-constexpr int kGramGroup = 4;
+#ifndef HMX_GRAM_GROUP
+#define HMX_GRAM_GROUP 4
+#endif
+constexpr int kGramGroup = HMX_GRAM_GROUP;  // factor columns per warp in the Gram pass
+#ifndef HMX_GRAM_BATCH
+#define HMX_GRAM_BATCH 1
+#endif
+constexpr int kGramBatch = HMX_GRAM_BATCH;  // steps per Gram pass (max; HMX_ACA_GRAM_BATCH lowers it)
 
 // sigma_1 and sigma_3 of a 3x3 complex matrix from the characteristic
 // polynomial of R^H R: c2 = ||R||_F^2, c1 = sum |2x2 minors|^2 (Cauchy-Binet),
@@ -135,8 +146,8 @@ HMX_D void inverse(const double2* P, double2* G) {
 
 constexpr int kMaxWarps = 32;
 struct Shared {
-  int ipiv, jpiv, K, steps, state, zero_rows, verdict;
-  double normB2, s1max;
+  int ipiv, jpiv, K, steps, state, zero_rows, verdict, npend, rowout, nextrow, stop, bbi, kfinal, sfinal;
+  double normB2, s1max, bbv;
   double2 gamma[9];
   double red_v[kMaxWarps];
   int red_i[kMaxWarps];
@@ -144,48 +155,147 @@ struct Shared {
   double red_a[kMaxWarps];
 };
 
-// What each CTA of a cluster publishes for the cluster-wide reductions
-// (read by the other CTAs through distributed shared memory).
-struct Pub {
-  double row_v, row_s1, col_v, cross;
-  int row_i, col_i;
-};
-
-// state codes
+// state codes / row-pass outcomes
 constexpr int kRun = 0, kZeroRow = 1, kDone = 2;
+constexpr int kRowPivot = 0, kRowZero = 1, kRowFallback = 2;
 
-template <int CS>
-HMX_D void cluster_sync() {
-  if constexpr (CS > 1) cg::this_cluster().sync();
+// Gram columns G(:, Kc:Kc+NC) = F^H F(:, Kc:Kc+NC) for NC new columns, rows
+// l < Kc + NC, both factor panels; warp per kGramGroup columns l, lanes over
+// factor rows (contiguous 512 B per load instruction).
+template <int NC, int NT>
+HMX_D void gram_columns(const double2* __restrict__ Ub, const double2* __restrict__ Vb, int64_t ldu, int64_t ldv,
+                        double2* __restrict__ GU, double2* __restrict__ GV, int kcap, int Kc) {
+  constexpr int NW = NT / 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int Kn = Kc + NC;
+  const int ngroups = (Kn + kGramGroup - 1) / kGramGroup;
+  for (int side = 0; side < 2; ++side) {
+    const double2* F = side == 0 ? Ub : Vb;
+    const int64_t ld = side == 0 ? ldu : ldv;
+    double2* Gm = side == 0 ? GU : GV;
+    for (int grp = warp; grp < ngroups; grp += NW) {
+      double2 acc[kGramGroup][NC];
+#pragma unroll
+      for (int t = 0; t < kGramGroup; ++t)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[t][c] = cmk(0.0, 0.0);
+      const int l0 = grp * kGramGroup;
+#pragma unroll 2
+      for (int64_t q = lane; q < ld; q += 32) {
+        double2 nf[NC];
+#pragma unroll
+        for (int c = 0; c < NC; ++c) nf[c] = F[q + (int64_t)(Kc + c) * ld];
+#pragma unroll
+        for (int t = 0; t < kGramGroup; ++t) {
+          if (l0 + t < Kn) {
+            const double2 fl = F[q + (int64_t)(l0 + t) * ld];
+#pragma unroll
+            for (int c = 0; c < NC; ++c) acc[t][c] = cfma_ca(fl, nf[c], acc[t][c]);
+          }
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < kGramGroup; ++t)
+#pragma unroll
+        for (int c = 0; c < NC; ++c) acc[t][c] = warp_sum(acc[t][c]);
+      if (lane == 0) {
+#pragma unroll
+        for (int t = 0; t < kGramGroup; ++t) {
+          const int l = l0 + t;
+          if (l >= Kn) continue;
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            const int col = Kc + c;
+            if (l < Kc || l < col) {
+              Gm[l + (int64_t)col * kcap] = acc[t][c];
+              Gm[col + (int64_t)l * kcap] = cconj(acc[t][c]);
+            } else if (l == col) {
+              Gm[l + (int64_t)col * kcap] = cmk(acc[t][c].x, 0.0);
+            }
+          }
+        }
+      }
+    }
+  }
 }
 
-template <int CS, class T>
-HMX_D T* peer(T* p, int r) {
-  if constexpr (CS > 1) return cg::this_cluster().map_shared_rank(p, r);
-  return p;
+// ||B||_F^2 update with the Gram columns Ks..Ks+D-1 and the stop test
+// (oracle/lowrank.py decisions 4-5); result in sh.stop.
+template <int D, int NT>
+HMX_D void decide_step(const double2* __restrict__ GU, const double2* __restrict__ GV, int kcap, int Ks, double eps,
+                       Shared& sh) {
+  constexpr int NW = NT / 32;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double cross = 0.0;
+  for (int t = tid; t < Ks * D; t += NT) {
+    const int l = t / D, c = t - l * D;
+    const double2 gu = GU[l + (int64_t)(Ks + c) * kcap];
+    const double2 gv = GV[l + (int64_t)(Ks + c) * kcap];
+    cross += gu.x * gv.x + gu.y * gv.y;
+  }
+  cross = warp_sum(cross);
+  if (lane == 0) sh.red_a[warp] = cross;
+  __syncthreads();
+  if (tid == 0) {
+    double crs = 0.0;
+    for (int w = 0; w < NW; ++w) crs += sh.red_a[w];
+    double diag = 0.0, nu = 0.0, nv = 0.0;
+    for (int c = 0; c < D; ++c) {
+      nu += GU[(Ks + c) + (int64_t)(Ks + c) * kcap].x;
+      nv += GV[(Ks + c) + (int64_t)(Ks + c) * kcap].x;
+      for (int q = 0; q < D; ++q) {
+        const double2 a = GU[(Ks + c) + (int64_t)(Ks + q) * kcap];
+        const double2 bq = GV[(Ks + q) + (int64_t)(Ks + c) * kcap];
+        diag += a.x * bq.x - a.y * bq.y;
+      }
+    }
+    sh.normB2 = sh.normB2 + 2.0 * crs + diag;
+    sh.stop = sqrt(nu) * sqrt(nv) <= eps * sqrt(fmax(sh.normB2, 0.0));
+  }
+  __syncthreads();
 }
 
-// CS CTAs (a thread-block cluster, distributed shared memory for the
-// reductions) cooperate on one admissible leaf; CS = 1 is one CTA per leaf.
-// Every CTA keeps an identical copy of the ACA state (all decisions are made
-// from the same reduced values in the same order -> deterministic).
-// CTA rank cr owns column points [n cr/CS, n (cr+1)/CS) in the row pass and
-// row points [m cr/CS, ...) in the column pass; its Gram partial sums run over
-// exactly the factor rows it wrote, so no barrier is needed before the Gram pass.
-template <int D, int KIND, int NT, int MINB, int CS>
+// Gram columns of the npend pending steps (one pass) and their stop decisions
+// in order.  sh.kfinal / sh.sfinal = rank / step count at the first step that
+// stops (sh.stop = 1), else the whole batch is accepted (sh.stop = 0).
+template <int D, int NT, int BMAX>
+HMX_D void resolve_pending(const double2* __restrict__ Ub, const double2* __restrict__ Vb, int64_t ldu, int64_t ldv,
+                           double2* __restrict__ GU, double2* __restrict__ GV, int kcap, double eps, Shared& sh) {
+  const int npend = sh.npend;
+  const int K = sh.K;
+  const int Kc = K - npend * D;
+  if (BMAX == 1 || npend == 1)
+    gram_columns<D, NT>(Ub, Vb, ldu, ldv, GU, GV, kcap, Kc);
+  else
+    gram_columns<D * (BMAX > 1 ? 2 : 1), NT>(Ub, Vb, ldu, ldv, GU, GV, kcap, Kc);
+  __syncthreads();
+  int stop = 0;
+  for (int p = 0; p < npend && !stop; ++p) {
+    decide_step<D, NT>(GU, GV, kcap, Kc + p * D, eps, sh);
+    stop = sh.stop;
+    if (stop && threadIdx.x == 0) {
+      sh.kfinal = Kc + (p + 1) * D;
+      sh.sfinal = sh.steps - (npend - 1 - p);
+    }
+  }
+  if (threadIdx.x == 0) {
+    sh.stop = stop;
+    sh.npend = 0;
+  }
+  __syncthreads();
+}
+
+template <int D, int KIND, int NT, int MINB, int BMAX>
 __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA pts, const AcaDesc* __restrict__ desc,
                                                        const int32_t* __restrict__ order, double eps, double floor,
                                                        double2* __restrict__ U, double2* __restrict__ V,
                                                        double2* __restrict__ G, AcaOut* __restrict__ out,
-                                                       int kcap_max) {
+                                                       int kcap_max, int batch) {
   extern __shared__ double2 dyn[];
   __shared__ Shared sh;
-  __shared__ Pub pub;
   constexpr int NW = NT / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  int cr = 0;
-  if constexpr (CS > 1) cr = (int)cg::this_cluster().block_rank();
-  const int b = order[blockIdx.x / CS];
+  const int b = order[blockIdx.x];
   const AcaDesc ds = desc[b];
   const int m = ds.m, n = ds.n, kcap = ds.kcap;
   const int64_t ldu = (int64_t)D * m, ldv = (int64_t)D * n;
@@ -193,12 +303,11 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
   double2* __restrict__ Vb = V + ds.voff;
   double2* __restrict__ GU = G + ds.goff;
   double2* __restrict__ GV = GU + (int64_t)kcap * kcap;
-  const int j0 = (int)((int64_t)n * cr / CS), j1 = (int)((int64_t)n * (cr + 1) / CS);
-  const int i0 = (int)((int64_t)m * cr / CS), i1 = (int)((int64_t)m * (cr + 1) / CS);
   double2* Urow = dyn;                 // D x kcap_max
   double2* Vrow = dyn + D * kcap_max;  // D x kcap_max
-  double2* pubG = Vrow + D * kcap_max; // (CS > 1) 2 x D x kcap_max partial Gram columns
-  unsigned char* visited = reinterpret_cast<unsigned char*>(pubG + (CS > 1 ? 2 * D * kcap_max : 0));
+  unsigned char* visited = reinterpret_cast<unsigned char*>(Vrow + D * kcap_max);
+  if (batch < 1) batch = 1;
+  if (batch > BMAX) batch = BMAX;
 
   for (int i = tid; i < m; i += NT) visited[i] = 0;
   if (tid == 0) {
@@ -209,6 +318,8 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
     sh.zero_rows = 0;
     sh.normB2 = 0.0;
     sh.s1max = 0.0;
+    sh.npend = 0;
+    sh.stop = 0;
   }
   __syncthreads();
   int status = 0;
@@ -217,6 +328,13 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
     const int ipiv = sh.ipiv;
     const int K = sh.K;
     if (K + D > kcap) {
+      if (sh.npend > 0) {  // the pending steps may already have converged
+        resolve_pending<D, NT, BMAX>(Ub, Vb, ldu, ldv, GU, GV, kcap, eps, sh);
+        if (sh.stop) {
+          status = 1;
+          break;
+        }
+      }
       status = 4;  // capacity overflow -> host reruns with a larger capacity
       break;
     }
@@ -227,10 +345,10 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
     }
     __syncthreads();
 
-    // ---- row pass (own column points) -----------------------------------------
+    // ---- row pass -----------------------------------------------------------------
     ArgMax best{-1.0, 0x7fffffff};
     double rs1 = 0.0;
-    for (int j = j0 + tid; j < j1; j += NT) {
+    for (int j = tid; j < n; j += NT) {
       double2 acc[D * D];
 #pragma unroll
       for (int t = 0; t < D * D; ++t) acc[t] = cmk(0.0, 0.0);
@@ -295,56 +413,55 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
         bb = argmax_pick(bb, ArgMax{sh.red_v[w], sh.red_i[w]});
         r1 = fmax(r1, sh.red_s[w]);
       }
-      pub.row_v = bb.v;
-      pub.row_i = bb.i;
-      pub.row_s1 = r1;
-    }
-    cluster_sync<CS>();  // row-pass results (and the new V columns) visible cluster-wide
-    if (tid == 0) {
-      ArgMax bb{-1.0, 0x7fffffff};
-      double r1 = 0.0;
-      for (int r = 0; r < CS; ++r) {
-        const Pub* q = peer<CS>(&pub, r);
-        bb = argmax_pick(bb, ArgMax{q->row_v, q->row_i});
-        r1 = fmax(r1, q->row_s1);
-      }
       sh.s1max = fmax(sh.s1max, r1);
       if (r1 <= floor * sh.s1max || sh.s1max == 0.0) {
-        // zero residual row: lowest unvisited row, no rank added
-        sh.zero_rows++;
+        sh.rowout = kRowZero;  // zero residual row: lowest unvisited row, no rank added
         int nxt = -1;
         for (int i = 0; i < m; ++i)
           if (!visited[i]) {
             nxt = i;
             break;
           }
-        if (nxt < 0) {
-          sh.state = kDone;
-          sh.verdict = 1;  // converged flag
-        } else {
-          sh.state = kZeroRow;
-          sh.ipiv = nxt;
-        }
+        sh.nextrow = nxt;
       } else if (bb.v <= floor * sh.s1max) {
-        sh.state = kDone;
-        sh.verdict = 8;  // fallback needed
+        sh.rowout = kRowFallback;
       } else {
+        sh.rowout = kRowPivot;
         sh.jpiv = bb.i;
         double2 Pv[D * D];
         for (int a = 0; a < D; ++a)
           for (int c = 0; c < D; ++c) Pv[a * D + c] = cconj(Vb[(int64_t)(D * bb.i + c) + (int64_t)(K + a) * ldv]);
         inverse<D>(Pv, sh.gamma);
-        sh.state = kRun;
       }
     }
     __syncthreads();
-    if (sh.state == kZeroRow) {
-      cluster_sync<CS>();  // everyone has read pub.row_* before it is rewritten
+    if (sh.rowout != kRowPivot) {
+      if (sh.npend > 0) {  // this step cannot complete: settle the pending ones first
+        resolve_pending<D, NT, BMAX>(Ub, Vb, ldu, ldv, GU, GV, kcap, eps, sh);
+        if (sh.stop) {
+          status = 1;
+          break;
+        }
+      }
+      if (sh.rowout == kRowFallback) {
+        status = 8;  // fallback needed
+        break;
+      }
+      if (tid == 0) {
+        sh.zero_rows++;
+        if (sh.nextrow < 0) {
+          sh.state = kDone;
+          sh.verdict = 1;  // converged flag
+        } else {
+          sh.ipiv = sh.nextrow;
+        }
+      }
+      __syncthreads();
+      if (sh.state == kDone) {
+        status = sh.verdict;
+        break;
+      }
       continue;
-    }
-    if (sh.state == kDone) {
-      status = sh.verdict;
-      break;
     }
     const int jpiv = sh.jpiv;
     for (int t = tid; t < D * K; t += NT) {
@@ -356,9 +473,9 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
     for (int t = 0; t < D * D; ++t) gam[t] = sh.gamma[t];
     __syncthreads();
 
-    // ---- column pass (own row points) -------------------------------------------
+    // ---- column pass ------------------------------------------------------------------
     best = ArgMax{-1.0, 0x7fffffff};
-    for (int i = i0 + tid; i < i1; i += NT) {
+    for (int i = tid; i < m; i += NT) {
       double2 acc[D * D];
 #pragma unroll
       for (int t = 0; t < D * D; ++t) acc[t] = cmk(0.0, 0.0);
@@ -406,10 +523,10 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
       for (int a = 0; a < D; ++a)
 #pragma unroll
         for (int c = 0; c < D; ++c) {
-          double2 s = cmk(0.0, 0.0);
+          double2 sacc = cmk(0.0, 0.0);
 #pragma unroll
-          for (int q = 0; q < D; ++q) s = cfma(C[a * D + q], gam[q * D + c], s);
-          Ub[(int64_t)(D * i + a) + (int64_t)(K + c) * ldu] = s;
+          for (int q = 0; q < D; ++q) sacc = cfma(C[a * D + q], gam[q * D + c], sacc);
+          Ub[(int64_t)(D * i + a) + (int64_t)(K + c) * ldu] = sacc;
         }
     }
     best = warp_argmax(best);
@@ -421,152 +538,42 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
     if (tid == 0) {
       ArgMax bb{sh.red_v[0], sh.red_i[0]};
       for (int w = 1; w < NW; ++w) bb = argmax_pick(bb, ArgMax{sh.red_v[w], sh.red_i[w]});
-      pub.col_v = bb.v;
-      pub.col_i = bb.i;
-    }
-
-    // ---- Gram pass: G(:, K:K+D) = F^H f_new over this CTA's factor rows -----------
-    const int Kn = K + D;
-    const int ngroups = (Kn + kGramGroup - 1) / kGramGroup;
-    for (int side = 0; side < 2; ++side) {
-      const double2* F = side == 0 ? Ub : Vb;
-      const int64_t ld = side == 0 ? ldu : ldv;
-      const int64_t q0 = (int64_t)D * (side == 0 ? i0 : j0), q1 = (int64_t)D * (side == 0 ? i1 : j1);
-      double2* Gm = side == 0 ? GU : GV;
-      for (int grp = warp; grp < ngroups; grp += NW) {
-        double2 acc[kGramGroup][D];
-#pragma unroll
-        for (int t = 0; t < kGramGroup; ++t)
-#pragma unroll
-          for (int c = 0; c < D; ++c) acc[t][c] = cmk(0.0, 0.0);
-        const int l0 = grp * kGramGroup;
-#pragma unroll 2
-        for (int64_t q = q0 + lane; q < q1; q += 32) {
-          double2 nf[D];
-#pragma unroll
-          for (int c = 0; c < D; ++c) nf[c] = F[q + (int64_t)(K + c) * ld];
-#pragma unroll
-          for (int t = 0; t < kGramGroup; ++t) {
-            if (l0 + t < Kn) {
-              const double2 fl = F[q + (int64_t)(l0 + t) * ld];
-#pragma unroll
-              for (int c = 0; c < D; ++c) acc[t][c] = cfma_ca(fl, nf[c], acc[t][c]);
-            }
-          }
-        }
-#pragma unroll
-        for (int t = 0; t < kGramGroup; ++t)
-#pragma unroll
-          for (int c = 0; c < D; ++c) acc[t][c] = warp_sum(acc[t][c]);
-        if (lane == 0) {
-#pragma unroll
-          for (int t = 0; t < kGramGroup; ++t) {
-            const int l = l0 + t;
-            if (l >= Kn) continue;
-#pragma unroll
-            for (int c = 0; c < D; ++c) {
-              if constexpr (CS > 1) {
-                pubG[(side * D + c) * kcap_max + l] = acc[t][c];
-              } else {
-                const int col = K + c;
-                if (l < K || l < col) {
-                  Gm[l + (int64_t)col * kcap] = acc[t][c];
-                  Gm[col + (int64_t)l * kcap] = cconj(acc[t][c]);
-                } else if (l == col) {
-                  Gm[l + (int64_t)col * kcap] = cmk(acc[t][c].x, 0.0);
-                }
-              }
-            }
-          }
-        }
-      }
-    }
-    if constexpr (CS > 1) {
-      // combine the CS partial Gram columns (fixed rank order); CTA cr finalises
-      // the entries l = cr, cr + CS, ... and writes them to global G
-      cluster_sync<CS>();
-      for (int t = tid; t < 2 * D * Kn; t += NT) {
-        const int l = t % Kn, sc = t / Kn;  // sc = side * D + c
-        if (l % CS != cr) continue;
-        double2 v = cmk(0.0, 0.0);
-        for (int r = 0; r < CS; ++r) v = cadd(v, peer<CS>(pubG, r)[sc * kcap_max + l]);
-        const int side = sc / D, c = sc - side * D, col = K + c;
-        double2* Gm = side == 0 ? GU : GV;
-        if (l < K || l < col) {
-          Gm[l + (int64_t)col * kcap] = v;
-          Gm[col + (int64_t)l * kcap] = cconj(v);
-        } else if (l == col) {
-          Gm[l + (int64_t)col * kcap] = cmk(v.x, 0.0);
-        }
-      }
-    }
-    __syncthreads();
-
-    // ---- ||B_k||_F update: cross = Re sum_{l<K,c} G_U(l,K+c) conj(G_V(l,K+c)) ----------
-    double cross = 0.0;
-    for (int t = tid; t < K * D; t += NT) {
-      const int l = t / D, c = t - l * D;
-      if (l % CS != cr) continue;  // this CTA's finalised entries
-      const double2 gu = GU[l + (int64_t)(K + c) * kcap];
-      const double2 gv = GV[l + (int64_t)(K + c) * kcap];
-      cross += gu.x * gv.x + gu.y * gv.y;
-    }
-    cross = warp_sum(cross);
-    if (lane == 0) sh.red_a[warp] = cross;
-    __syncthreads();
-    if (tid == 0) {
-      double cr_sum = 0.0;
-      for (int w = 0; w < NW; ++w) cr_sum += sh.red_a[w];
-      pub.cross = cr_sum;
-    }
-    cluster_sync<CS>();  // cross partials, column argmax and G entries visible
-    if (tid == 0) {
-      double crs = 0.0;
-      ArgMax bb{-1.0, 0x7fffffff};
-      for (int r = 0; r < CS; ++r) {
-        const Pub* q = peer<CS>(&pub, r);
-        crs += q->cross;
-        bb = argmax_pick(bb, ArgMax{q->col_v, q->col_i});
-      }
-      double diag = 0.0, nu = 0.0, nv = 0.0;
-      for (int c = 0; c < D; ++c) {
-        nu += GU[(K + c) + (int64_t)(K + c) * kcap].x;
-        nv += GV[(K + c) + (int64_t)(K + c) * kcap].x;
-        for (int q = 0; q < D; ++q) {
-          const double2 a = GU[(K + c) + (int64_t)(K + q) * kcap];
-          const double2 bq = GV[(K + q) + (int64_t)(K + c) * kcap];
-          diag += a.x * bq.x - a.y * bq.y;
-        }
-      }
-      sh.normB2 = sh.normB2 + 2.0 * crs + diag;
-      sh.K = Kn;
+      sh.bbv = bb.v;
+      sh.bbi = bb.i;
+      // this step joins the pending batch
+      sh.K = K + D;
       sh.steps += 1;
-      const int dmin = D * (m < n ? m : n);
-      if (sqrt(nu) * sqrt(nv) <= eps * sqrt(fmax(sh.normB2, 0.0))) {
-        sh.state = kDone;
-        sh.verdict = 1;
-      } else if (Kn >= ds.max_rank) {
-        sh.state = kDone;
-        sh.verdict = 2 | (Kn >= dmin ? 1 : 0);
-      } else if (bb.v < 0.0) {  // no unvisited row left
-        sh.state = kDone;
-        sh.verdict = 1;
-      } else {
-        sh.state = kRun;
-        sh.ipiv = bb.i;
-      }
+      sh.npend += 1;
     }
     __syncthreads();
-    cluster_sync<CS>();  // all peers done reading pub before the next step rewrites it
-    if (sh.state == kDone) {
-      status = sh.verdict;
-      break;
+    const int Kn = K + D;
+    const bool no_row = sh.bbv < 0.0;  // no unvisited row left
+    const bool at_max = Kn >= ds.max_rank;
+    if (at_max || no_row || sh.npend >= batch) {
+      resolve_pending<D, NT, BMAX>(Ub, Vb, ldu, ldv, GU, GV, kcap, eps, sh);
+      if (sh.stop) {
+        status = 1;
+        break;
+      }
+      if (at_max) {
+        const int dmin = D * (m < n ? m : n);
+        status = 2 | (Kn >= dmin ? 1 : 0);
+        break;
+      }
+      if (no_row) {
+        status = 1;
+        break;
+      }
     }
+    if (tid == 0) sh.ipiv = sh.bbi;
+    __syncthreads();
   }
-  if (tid == 0 && cr == 0) {
+  __syncthreads();
+  if (tid == 0) {
     AcaOut o;
-    o.steps = sh.steps;
-    o.rank = sh.K;
+    const bool truncated = status == 1 && sh.stop;  // a batched step converged
+    o.steps = truncated ? sh.sfinal : sh.steps;
+    o.rank = truncated ? sh.kfinal : sh.K;
     o.status = status;
     o.zero_rows = sh.zero_rows;
     out[b] = o;
@@ -577,61 +584,40 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
 
 void warm_aca() {
   cudaFuncAttributes a;
-  cudaFuncGetAttributes(&a, aca_kernel<1, 0, 512, 1, 1>);
-  cudaFuncGetAttributes(&a, aca_kernel<3, 1, 512, 1, 1>);
-  cudaFuncGetAttributes(&a, aca_kernel<3, 2, 512, 1, 1>);
-  cudaFuncGetAttributes(&a, aca_kernel<1, 0, 128, 4, 1>);
-  cudaFuncGetAttributes(&a, aca_kernel<3, 1, 128, 4, 1>);
-  cudaFuncGetAttributes(&a, aca_kernel<3, 2, 128, 4, 1>);
+  cudaFuncGetAttributes(&a, aca_kernel<1, 0, 512, 1, kGramBatch>);
+  cudaFuncGetAttributes(&a, aca_kernel<3, 1, 512, 1, kGramBatch>);
+  cudaFuncGetAttributes(&a, aca_kernel<3, 2, 512, 1, kGramBatch>);
+  cudaFuncGetAttributes(&a, aca_kernel<1, 0, 128, 4, kGramBatch>);
+  cudaFuncGetAttributes(&a, aca_kernel<3, 1, 128, 4, kGramBatch>);
+  cudaFuncGetAttributes(&a, aca_kernel<3, 2, 128, 4, kGramBatch>);
 }
 
 int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const AcaDesc* d_desc, const int32_t* d_order,
                int64_t nblk, int kcap_max, int m_max, double eps, double sigma3_floor, double2* U, double2* V,
                double2* G, AcaOut* d_out, int variant) {
   if (nblk == 0) return HMX_OK;
-  // variant: kAcaWide (512 threads, one CTA per SM: the factors of large
-  // leaves stay hot in L1 / the SM's L2 share; 2-3 CTAs/SM measured 1.4-1.8x
-  // slower), kAcaNarrow (128 threads, 4 CTAs per SM: small leaves are latency
-  // bound and use few threads per step), >1: cluster of that many CTAs per leaf.
-  const int CSv = variant > 1 ? variant : 1;
-  const char* e_wnt = std::getenv("HMX_ACA_WIDE_NT");
-  const int wide_nt = e_wnt && std::atoi(e_wnt) == 256 ? 256 : 512;
-  const int nt = variant == kAcaNarrow ? 128 : (CSv > 1 ? 512 : wide_nt);
-  size_t smem = sizeof(double2) * (CSv > 1 ? 4 : 2) * (size_t)d * kcap_max + (size_t)((m_max + 15) / 16) * 16;
+  // variant: kAcaWide (512 threads, one CTA per SM: 2-3 CTAs/SM measured
+  // 1.4-1.8x slower), kAcaNarrow (128 threads, 4 CTAs per SM: small leaves
+  // are latency bound and use few threads per step).
+  const int nt = variant == kAcaNarrow ? 128 : 512;
+  const char* e_b = std::getenv("HMX_ACA_GRAM_BATCH");
+  const int batch = e_b ? std::atoi(e_b) : kGramBatch;
+  const size_t smem = sizeof(double2) * 2 * (size_t)d * kcap_max + (size_t)((m_max + 15) / 16) * 16;
   auto go = [&](auto kern) -> int {
     HMX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)(nblk * CSv));
-    cfg.blockDim = dim3(nt);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = c.stream;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = CSv;
-    attr[0].val.clusterDim.y = 1;
-    attr[0].val.clusterDim.z = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    HMX_CUDA_TRY(cudaLaunchKernelEx(&cfg, kern, P, pts, d_desc, d_order, eps, sigma3_floor, U, V, G, d_out,
-                                    kcap_max));
+    kern<<<(unsigned)nblk, nt, smem, c.stream>>>(P, pts, d_desc, d_order, eps, sigma3_floor, U, V, G, d_out,
+                                                 kcap_max, batch);
     return HMX_OK;
   };
   int rc;
-  if (CSv == 8) {
-    rc = P.kind == 0 ? go(aca_kernel<1, 0, 512, 1, 8>)
-                     : (P.kind == 1 ? go(aca_kernel<3, 1, 512, 1, 8>) : go(aca_kernel<3, 2, 512, 1, 8>));
-  } else if (CSv == 4) {
-    rc = P.kind == 0 ? go(aca_kernel<1, 0, 512, 1, 4>)
-                     : (P.kind == 1 ? go(aca_kernel<3, 1, 512, 1, 4>) : go(aca_kernel<3, 2, 512, 1, 4>));
-  } else if (variant == kAcaNarrow) {
-    rc = P.kind == 0 ? go(aca_kernel<1, 0, 128, 4, 1>)
-                     : (P.kind == 1 ? go(aca_kernel<3, 1, 128, 4, 1>) : go(aca_kernel<3, 2, 128, 4, 1>));
-  } else if (nt == 256) {
-    rc = P.kind == 0 ? go(aca_kernel<1, 0, 256, 2, 1>)
-                     : (P.kind == 1 ? go(aca_kernel<3, 1, 256, 2, 1>) : go(aca_kernel<3, 2, 256, 2, 1>));
+  if (variant == kAcaNarrow) {
+    rc = P.kind == 0 ? go(aca_kernel<1, 0, 128, 4, kGramBatch>)
+                     : (P.kind == 1 ? go(aca_kernel<3, 1, 128, 4, kGramBatch>)
+                                    : go(aca_kernel<3, 2, 128, 4, kGramBatch>));
   } else {
-    rc = P.kind == 0 ? go(aca_kernel<1, 0, 512, 1, 1>)
-                     : (P.kind == 1 ? go(aca_kernel<3, 1, 512, 1, 1>) : go(aca_kernel<3, 2, 512, 1, 1>));
+    rc = P.kind == 0 ? go(aca_kernel<1, 0, 512, 1, kGramBatch>)
+                     : (P.kind == 1 ? go(aca_kernel<3, 1, 512, 1, kGramBatch>)
+                                    : go(aca_kernel<3, 2, 512, 1, kGramBatch>));
   }
   if (rc) return rc;
   HMX_CUDA_TRY(cudaGetLastError());

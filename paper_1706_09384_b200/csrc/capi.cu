@@ -573,11 +573,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   std::deque<AcaPass> passes;  // stable addresses (Pending keeps pointers)
   std::vector<int64_t> todo = adm;
   const double s3f = cfg->sigma3_floor > 0 ? cfg->sigma3_floor : 1e-12;
-  const char* e_cs = std::getenv("HMX_ACA_CS");
-  const char* e_min = std::getenv("HMX_ACA_CLUSTER_MIN");
   const char* e_nm = std::getenv("HMX_ACA_NARROW_MAX");
-  const int cs = e_cs ? std::atoi(e_cs) : 1;  // clusters measured slower
-  const int64_t cmin = e_min ? std::atoll(e_min) : kAcaClusterMin;
   const int64_t nmax = e_nm ? std::atoll(e_nm) : kAcaNarrowMax;
   // recompression results read back once at the end
   struct Pending {
@@ -734,12 +730,10 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     HMX_CUDA_TRY(
         cudaMemcpyAsync(d_order, order.data(), sizeof(int32_t) * todo.size(), cudaMemcpyHostToDevice, c.stream));
     tick("aca: workspace alloc");
-    // large leaves (clusters / wide CTAs, a prefix of the size-sorted list) on
-    // the auxiliary stream, the many small leaves (narrow CTAs) on the main
+    // large leaves (wide CTAs, a prefix of the size-sorted list) on the
+    // auxiliary stream, the many small leaves (narrow CTAs) on the main
     // stream; each side's recompression starts as soon as its own ACA is done
-    size_t nbig = 0, nwide = 0;
-    while (cs > 1 && nbig < todo.size() && rows_of(todo[nbig]) + cols_of(todo[nbig]) >= cmin) ++nbig;
-    nwide = nbig;
+    size_t nwide = 0;
     while (nwide < todo.size() && rows_of(todo[nwide]) + cols_of(todo[nwide]) >= nmax) ++nwide;
     auto sub_max = [&](size_t q0, size_t q1, int& kc, int& mm) {
       kc = 1;
@@ -760,16 +754,10 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     {
       OnAux on(c);
       mark("aca wide start");
-      if (nbig) {
-        sub_max(0, nbig, kc, mm);
-        if ((rc = launch_aca(c, d, P, pts.soa, d_desc, d_order, (int64_t)nbig, kc, mm, cfg->eps, s3f, ps.U, ps.V,
-                             ps.G, d_out, cs)))
-          return fail(rc);
-      }
-      if (nwide > nbig) {
-        sub_max(nbig, nwide, kc, mm);
-        if ((rc = launch_aca(c, d, P, pts.soa, d_desc, d_order + nbig, (int64_t)(nwide - nbig), kc, mm, cfg->eps,
-                             s3f, ps.U, ps.V, ps.G, d_out, kAcaWide)))
+      if (nwide) {
+        sub_max(0, nwide, kc, mm);
+        if ((rc = launch_aca(c, d, P, pts.soa, d_desc, d_order, (int64_t)nwide, kc, mm, cfg->eps, s3f, ps.U, ps.V,
+                             ps.G, d_out, kAcaWide)))
           return fail(rc);
       }
       mark("aca wide done");

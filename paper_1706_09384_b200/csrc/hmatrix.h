@@ -148,12 +148,10 @@ struct AcaOut {
   int32_t zero_rows;
 };
 // launch variants of the ACA kernel; leaves with m + n < kAcaNarrowMax points use
-// the narrow variant, optionally m + n >= kAcaClusterMin a cluster of CTAs
+// the narrow variant (128 threads, 4 CTAs / SM), the others the wide one (512)
 constexpr int kAcaWide = 0;
 constexpr int kAcaNarrow = 1;
 constexpr int kAcaNarrowMax = 320;
-constexpr int kAcaCluster = 8;
-constexpr int kAcaClusterMin = 1024;
 int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const AcaDesc* d_desc, const int32_t* d_order,
                int64_t nblk, int kcap_max, int m_max, double eps, double sigma3_floor, double2* U, double2* V,
                double2* G, AcaOut* d_out, int variant);
