@@ -766,14 +766,37 @@ __global__ void __launch_bounds__(NT) recompress_core(const RecDesc* __restrict_
   for (int t = tid; t < K * r; t += NT) Wv[t] = cscale(Wv[t], sqrt(sqrt(lam[ordr[t / K]])));
 }
 
-// C (rows x r, ldc) = A (rows x K, lda) * W (K x r, ld K); one CTA = 64 x 32 tile.
-// 64 x 32 output tile per CTA of 128 threads, 4 x 4 complex outputs per thread
-// (16 DFMA per shared-memory load pair), k-chunks of 16.
-constexpr int TM = 64, TN = 32, TK = 16, kFormThreads = 128;
+// C (rows x r, ldc) = A (rows x K, lda) * W (K x r, ld K) on the FP64 tensor
+// cores (mma.sync m8n8k4 f64: 37 TF/s measured vs 34 for DFMA, and one
+// instruction per 256 FMAs).  Complex product with two real MMAs per 8 x 4
+// block: B = [W_re | W_im] (4 complex columns as 8 real ones), C1 = A_re B,
+// C2 = A_im B -> C_re = C1[:, :4] - C2[:, 4:], C_im = C1[:, 4:] + C2[:, :4].
+// CTA tile 64 rows x 32 complex columns, 8 warps of 32 rows x 8 columns, k
+// chunks of 16 staged in shared memory.  Fragment layout (checked by
+// tools/micro/dmma_layout.cu): A[r][k] at lane 4 r + k, B[k][n] at lane
+// 4 n + k, C[r][2 t + i] at lane 4 r + t.
+constexpr int TM = 64, TN = 32, TK = 16, kFormThreads = 256, kFormStages = 3;
+HMX_D void dmma_8x8x4(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+// 16-byte asynchronous global -> shared copy, zero-filled when !valid
+HMX_D void cp_async16(void* smem, const void* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  const int n = valid ? 16 : 0;
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(valid ? gmem : smem), "r"(n));
+}
+HMX_D void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
+template <int N>
+HMX_D void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N));
+}
 __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __restrict__ desc,
                                                           const int64_t* __restrict__ tile_start, int64_t nitems) {
-  __shared__ double2 As[TK][TM + 1];
-  __shared__ double2 Ws[TK][TN + 1];
+  extern __shared__ double2 fsm[];
+  double2(*As)[TK][TM + 2] = reinterpret_cast<double2(*)[TK][TM + 2]>(fsm);
+  double2(*Ws)[TK][TN + 2] = reinterpret_cast<double2(*)[TK][TN + 2]>(fsm + kFormStages * TK * (TM + 2));
   // locate item by binary search over tile_start
   const int64_t tile = blockIdx.x;
   int64_t lo = 0, hi = nitems - 1;
@@ -789,48 +812,82 @@ __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __rest
   const double2* A = ds.A;
   const double2* W = ds.W;
   double2* C = ds.C;
-  const int tid = threadIdx.x;
-  const int tr = tid % 16, tc = tid / 16;  // rows tr + 16 a, cols tc + 8 b
-  double2 acc[4][4];
-#pragma unroll
-  for (int a = 0; a < 4; ++a)
-#pragma unroll
-    for (int b = 0; b < 4; ++b) acc[a][b] = cmk(0.0, 0.0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;  // warp tile: rows wm*32 + [0,32), cols wn*8 + [0,8)
+  const int fr = lane >> 2, fk = lane & 3;  // fragment row / k (A), column group lane / k (B)
   const int row0 = tm * TM, col0 = tn * TN;
-  for (int k0 = 0; k0 < ds.K; k0 += TK) {
+  const int nk = (ds.K + TK - 1) / TK;
+  auto stage = [&](int kc, int buf) {
+    const int k0 = kc * TK;
     for (int t = tid; t < TK * TM; t += kFormThreads) {
       const int rr = t % TM, kk = t / TM;
       const int gr = row0 + rr, gk = k0 + kk;
-      As[kk][rr] = (gr < ds.rows && gk < ds.K) ? A[gr + (int64_t)gk * ds.lda] : cmk(0.0, 0.0);
+      const bool v = gr < ds.rows && gk < ds.K;
+      cp_async16(&As[buf][kk][rr], A + (v ? gr + (int64_t)gk * ds.lda : 0), v);
     }
     for (int t = tid; t < TK * TN; t += kFormThreads) {
       const int kk = t % TK, cc = t / TK;
       const int gk = k0 + kk, gc = col0 + cc;
-      Ws[kk][cc] = (gk < ds.K && gc < ds.r) ? W[gk + (int64_t)gc * ds.K] : cmk(0.0, 0.0);
+      const bool v = gk < ds.K && gc < ds.r;
+      cp_async16(&Ws[buf][kk][cc], W + (v ? gk + (int64_t)gc * ds.K : 0), v);
     }
-    __syncthreads();
-#pragma unroll 2
-    for (int kk = 0; kk < TK; ++kk) {
-      double2 av[4], wv[4];
+  };
+  double c1[4][2][2], c2[4][2][2];  // [row octet][column group][2]
 #pragma unroll
-      for (int a = 0; a < 4; ++a) av[a] = As[kk][tr + 16 * a];
+  for (int o = 0; o < 4; ++o)
 #pragma unroll
-      for (int b = 0; b < 4; ++b) wv[b] = Ws[kk][tc + 8 * b];
+    for (int g = 0; g < 2; ++g) c1[o][g][0] = c1[o][g][1] = c2[o][g][0] = c2[o][g][1] = 0.0;
 #pragma unroll
-      for (int a = 0; a < 4; ++a)
-#pragma unroll
-        for (int b = 0; b < 4; ++b) acc[a][b] = cfma(av[a], wv[b], acc[a][b]);
-    }
-    __syncthreads();
+  for (int sidx = 0; sidx < kFormStages - 1; ++sidx) {
+    if (sidx < nk) stage(sidx, sidx);
+    cp_async_commit();
   }
+  for (int kc = 0; kc < nk; ++kc) {
+    cp_async_wait<kFormStages - 2>();
+    __syncthreads();  // chunk kc landed; every warp is done with chunk kc - 1
+    if (kc + kFormStages - 1 < nk) stage(kc + kFormStages - 1, (kc + kFormStages - 1) % kFormStages);
+    cp_async_commit();
+    const int buf = kc % kFormStages;
 #pragma unroll
-  for (int a = 0; a < 4; ++a)
+    for (int ks = 0; ks < TK; ks += 4) {
+      double2 av[4];
 #pragma unroll
-    for (int b = 0; b < 4; ++b) {
-      const int gr = row0 + tr + 16 * a, gc = col0 + tc + 8 * b;
-      if (gr < ds.rows && gc < ds.r) C[gr + (int64_t)gc * ds.ldc] = acc[a][b];
+      for (int o = 0; o < 4; ++o) av[o] = As[buf][ks + fk][wm * 32 + o * 8 + fr];
+      double bv[2];
+#pragma unroll
+      for (int g = 0; g < 2; ++g) {
+        // B[k][n], n = fr: n < 4 -> W_re(k, 4 g + n), else W_im(k, 4 g + n - 4)
+        const double2 w = Ws[buf][ks + fk][wn * 8 + g * 4 + (fr & 3)];
+        bv[g] = fr < 4 ? w.x : w.y;
+      }
+#pragma unroll
+      for (int o = 0; o < 4; ++o)
+#pragma unroll
+        for (int g = 0; g < 2; ++g) {
+          dmma_8x8x4(c1[o][g][0], c1[o][g][1], av[o].x, bv[g]);
+          dmma_8x8x4(c2[o][g][0], c2[o][g][1], av[o].y, bv[g]);
+        }
     }
+  }
+  cp_async_wait<0>();
+  // lane (r, t): t < 2 holds re*re / im*re parts of columns 2t, 2t+1; the
+  // partner lane t + 2 the re*im / im*im parts of the same columns
+  const int t = lane & 3;
+#pragma unroll
+  for (int o = 0; o < 4; ++o)
+#pragma unroll
+    for (int g = 0; g < 2; ++g)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const double p1 = __shfl_xor_sync(0xffffffffu, c1[o][g][i], 2);
+        const double p2 = __shfl_xor_sync(0xffffffffu, c2[o][g][i], 2);
+        if (t < 2) {
+          const int gr = row0 + wm * 32 + o * 8 + fr, gc = col0 + wn * 8 + g * 4 + 2 * t + i;
+          if (gr < ds.rows && gc < ds.r) C[gr + (int64_t)gc * ds.ldc] = cmk(c1[o][g][i] - p2, p1 + c2[o][g][i]);
+        }
+      }
 }
+constexpr size_t kFormSmem = sizeof(double2) * kFormStages * TK * ((TM + 2) + (TN + 2));
 
 }  // namespace
 
@@ -895,7 +952,8 @@ int launch_recompress_core(Ctx& c, const RecDesc* d_desc, int64_t nblk, int kmax
 
 int launch_form(Ctx& c, const FormDesc* d_desc, int64_t nitems, int64_t ntiles_total, const int64_t* d_tile_start) {
   if (ntiles_total == 0) return HMX_OK;
-  form_gemm<<<(unsigned)ntiles_total, kFormThreads, 0, c.stream>>>(d_desc, d_tile_start, nitems);
+  HMX_CUDA_TRY(cudaFuncSetAttribute(form_gemm, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kFormSmem));
+  form_gemm<<<(unsigned)ntiles_total, kFormThreads, kFormSmem, c.stream>>>(d_desc, d_tile_start, nitems);
   HMX_CUDA_TRY(cudaGetLastError());
   return HMX_OK;
 }
