@@ -164,12 +164,13 @@ constexpr int kRowPivot = 0, kRowZero = 1, kRowFallback = 2;
 // factor rows (contiguous 512 B per load instruction).
 template <int NC, int NT>
 HMX_D void gram_columns(const double2* __restrict__ Ub, const double2* __restrict__ Vb, int64_t ldu, int64_t ldv,
-                        double2* __restrict__ GU, double2* __restrict__ GV, int kcap, int Kc) {
+                        double2* __restrict__ GU, double2* __restrict__ GV, int kcap, int Kc, int sides = 3) {
   constexpr int NW = NT / 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int Kn = Kc + NC;
   const int ngroups = (Kn + kGramGroup - 1) / kGramGroup;
   for (int side = 0; side < 2; ++side) {
+    if (!((sides >> side) & 1)) continue;
     const double2* F = side == 0 ? Ub : Vb;
     const int64_t ld = side == 0 ? ldu : ldv;
     double2* Gm = side == 0 ? GU : GV;
@@ -580,6 +581,436 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
   }
 }
 
+// ===================================================================================
+// Tensor-core ACA for large leaves (d = 3): every pass streams its factor panel
+// F (rows x K, column-major) ONCE and feeds the same fragments to two FP64 MMA
+// contractions (mma.sync m8n8k4 f64, 37 TF/s measured, 256 FMAs / instruction):
+//   residual   res(q, a) = sum_l F(q, l)^(*) piv(a, l)   (m = rows, k = columns)
+//   Gram       G(l, a')  = sum_q conj F(q, l) F(q, P + a') of the PENDING step's
+//              columns P..P+2                        (m = columns, k = rows)
+// so the separate Gram pass of aca_kernel (which re-streamed both panels from
+// HBM every step) disappears.  The Gram columns of step s are therefore
+// produced by step s+1's passes and step s's stop decision is taken then; if it
+// says stop, step s+1 is discarded (speculative).  Where step s+1 cannot run the
+// pending columns come from the standalone gram_columns first -- the decision
+// sequence is exactly the sequential algorithm's (aca_kernel, oracle/lowrank.py).
+//
+// Complex products as two real MMAs with B = [X_re | X_im] (3 + 3 of 8 columns):
+// C1 = F_re B, C2 = F_im B.  Warp w owns row blocks of kTcRows rows (16 points),
+// loops over all column octets; Gram partials of its rows go to a per-warp
+// scratch slice in global memory (L2) and are summed in fixed warp order.
+constexpr int kTcRows = 48, kTcOct = kTcRows / 8, kTcKs = kTcRows / 4;
+constexpr int kTcThreads = 512, kTcWarps = kTcThreads / 32;
+
+HMX_D void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+
+// B fragment of a pivot row piv (3 x lds complex) for column l: n < 3 real,
+// 3 <= n < 6 imaginary part of piv(n mod 3, l), else 0
+HMX_D double piv_frag(const double2* piv, int lds, int l, int n) {
+  if (n >= 6) return 0.0;
+  const double2 v = piv[(n < 3 ? n : n - 3) * lds + l];
+  return n < 3 ? v.x : v.y;
+}
+
+// Fused pass over panel F (rows = 3 npts, ld = rows, K columns) for the row
+// blocks of this warp.  Residual fragments of each row block are left in
+// resb (kTcRows x 12 doubles: C1 n = 0..5, C2 n = 0..5) and `epi(rb_row0)` is
+// called by the whole warp; with pend, the Gram partials of the pending
+// columns [Pc, Pc + 3) go to scr (this warp's slice: noct x 32 lanes x 4).
+template <class Epi>
+HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const double2* piv, int lds, bool pend,
+                   int Pc, double* __restrict__ scr, int noct, double* resb, double* bnf, Epi&& epi) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int fr = lane >> 2, fk = lane & 3;
+  bool first = true;
+  for (int64_t r0 = (int64_t)warp * kTcRows; r0 < rows; r0 += (int64_t)kTcWarps * kTcRows) {
+    // Gram B fragments (rows r0 + 4 j + fk, pending column / part fr) in this warp's smem slice
+#pragma unroll
+    for (int j = 0; j < kTcKs; ++j) {
+      const int64_t q = r0 + 4 * j + fk;
+      double v = 0.0;
+      if (pend && fr < 6 && q < rows) {
+        const double2 x = F[q + (int64_t)(Pc + (fr < 3 ? fr : fr - 3)) * rows];
+        v = fr < 3 ? x.x : x.y;
+      }
+      bnf[j * 32 + lane] = v;
+    }
+    __syncwarp();
+    double c1[kTcOct][2], c2[kTcOct][2];
+#pragma unroll
+    for (int o = 0; o < kTcOct; ++o) c1[o][0] = c1[o][1] = c2[o][0] = c2[o][1] = 0.0;
+    for (int co = 0; co < noct; ++co) {
+      const int l0 = co * 8;
+      // residual: two k-steps of 4 columns (all fragment loads issued first)
+      double2 ar[2][kTcOct];
+      double br[2];
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int l = l0 + 4 * h + fk;
+        br[h] = l < K ? piv_frag(piv, lds, l, fr) : 0.0;
+#pragma unroll
+        for (int o = 0; o < kTcOct; ++o) {
+          const int64_t q = r0 + 8 * o + fr;
+          ar[h][o] = (q < rows && l < K) ? F[q + (int64_t)l * rows] : cmk(0.0, 0.0);
+        }
+      }
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+#pragma unroll
+        for (int o = 0; o < kTcOct; ++o) {
+          dmma(c1[o][0], c1[o][1], ar[h][o].x, br[h]);
+          dmma(c2[o][0], c2[o][1], ar[h][o].y, br[h]);
+        }
+      if (pend) {
+        double* d = scr + ((int64_t)co * 32 + lane) * 4;
+        double g3[2] = {0.0, 0.0}, g4[2] = {0.0, 0.0};
+        if (!first) {  // accumulate onto this warp's earlier row blocks (loads issued early)
+          g3[0] = d[0];
+          g3[1] = d[1];
+          g4[0] = d[2];
+          g4[1] = d[3];
+        }
+        const int l = l0 + fr;  // A' = F^T: m = column l0 + fr, k = row r0 + 4 j + fk
+        double2 ag[kTcKs];
+#pragma unroll
+        for (int j = 0; j < kTcKs; ++j) {
+          const int64_t q = r0 + 4 * j + fk;
+          ag[j] = (q < rows && l < K) ? F[q + (int64_t)l * rows] : cmk(0.0, 0.0);
+        }
+#pragma unroll
+        for (int j = 0; j < kTcKs; ++j) {
+          const double bj = bnf[j * 32 + lane];
+          dmma(g3[0], g3[1], ag[j].x, bj);
+          dmma(g4[0], g4[1], ag[j].y, bj);
+        }
+        d[0] = g3[0];
+        d[1] = g3[1];
+        d[2] = g4[0];
+        d[3] = g4[1];
+      }
+    }
+    // residual fragments -> shared memory (rows of this block)
+#pragma unroll
+    for (int o = 0; o < kTcOct; ++o)
+#pragma unroll
+      for (int i = 0; i < 2; ++i) {
+        const int nn = 2 * fk + i;
+        if (nn < 6) {
+          resb[(8 * o + fr) * 12 + nn] = c1[o][i];
+          resb[(8 * o + fr) * 12 + 6 + nn] = c2[o][i];
+        }
+      }
+    __syncwarp();
+    epi(r0);
+    __syncwarp();
+    first = false;
+  }
+}
+
+// Sum the warp slices (fixed order) into G(:, Pc:Pc+3), rows l < Kend.
+HMX_D void tc_gram_finalize(const double* __restrict__ scr, int noct, int nwork, double2* __restrict__ Gm, int kcap,
+                            int Pc, int Kend) {
+  for (int t = threadIdx.x; t < Kend * 3; t += kTcThreads) {
+    const int l = t / 3, a = t - l * 3;
+    const int co = l >> 3, r = l & 7;
+    // C3[r][n] / C4[r][n] live at lane 4 r + n / 2, element n % 2 (+ 2 for C4)
+    auto at = [&](int w, int nn, int e) {
+      return scr[(((int64_t)w * noct + co) * 32 + 4 * r + nn / 2) * 4 + e + (nn & 1)];
+    };
+    double re = 0.0, im = 0.0;
+    for (int w = 0; w < nwork; ++w) {
+      re += at(w, a, 0) + at(w, 3 + a, 2);
+      im += at(w, 3 + a, 0) - at(w, a, 2);
+    }
+    const double2 v = cmk(re, im);
+    const int col = Pc + a;
+    if (l < Pc || l < col) {
+      Gm[l + (int64_t)col * kcap] = v;
+      Gm[col + (int64_t)l * kcap] = cconj(v);
+    } else if (l == col) {
+      Gm[l + (int64_t)col * kcap] = cmk(v.x, 0.0);
+    }
+  }
+}
+
+template <int KIND>
+__global__ void __launch_bounds__(kTcThreads, 1)
+    aca_tc_kernel(GreenParams P, PointsSoA pts, const AcaDesc* __restrict__ desc, const int32_t* __restrict__ order,
+                  double eps, double floor, double2* __restrict__ U, double2* __restrict__ V,
+                  double2* __restrict__ G, AcaOut* __restrict__ out, int kcap_max) {
+  constexpr int D = 3, NT = kTcThreads, NW = kTcWarps;
+  extern __shared__ double2 dyn[];
+  __shared__ Shared sh;
+  __shared__ int s_pend;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b = order[blockIdx.x];
+  const AcaDesc ds = desc[b];
+  const int m = ds.m, n = ds.n, kcap = ds.kcap;
+  const int64_t ldu = (int64_t)D * m, ldv = (int64_t)D * n;
+  double2* __restrict__ Ub = U + ds.uoff;
+  double2* __restrict__ Vb = V + ds.voff;
+  double2* __restrict__ GU = G + ds.goff;
+  double2* __restrict__ GV = GU + (int64_t)kcap * kcap;
+  const int noct_cap = (kcap + 7) / 8;
+  double* __restrict__ scr = reinterpret_cast<double*>(GV + (int64_t)kcap * kcap);  // NW x noct_cap x 32 x 4
+  double* __restrict__ wscr = scr + (int64_t)warp * noct_cap * 128;
+  const int lds = kcap_max + 8;
+  double2* Urow = dyn;                 // 3 x lds
+  double2* Vrow = dyn + D * lds;       // 3 x lds
+  double* resb_all = reinterpret_cast<double*>(Vrow + D * lds);  // NW x kTcRows x 12
+  double* resb = resb_all + warp * kTcRows * 12;
+  double* bnfw = resb_all + NW * kTcRows * 12 + warp * kTcKs * 32;  // NW x kTcKs x 32
+  unsigned char* visited = reinterpret_cast<unsigned char*>(resb_all + NW * kTcRows * 12 + NW * kTcKs * 32);
+  const int nwork_v = min(NW, (int)((ldv + kTcRows - 1) / kTcRows));
+  const int nwork_u = min(NW, (int)((ldu + kTcRows - 1) / kTcRows));
+
+  for (int i = tid; i < m; i += NT) visited[i] = 0;
+  if (tid == 0) {
+    sh.ipiv = 0;
+    sh.K = 0;
+    sh.steps = 0;
+    sh.state = kRun;
+    sh.zero_rows = 0;
+    sh.normB2 = 0.0;
+    sh.s1max = 0.0;
+    sh.stop = 0;
+    s_pend = 0;
+  }
+  __syncthreads();
+  int status = 0;
+
+  for (;;) {
+    const int ipiv = sh.ipiv;
+    const int K = sh.K;
+    const bool pend = s_pend != 0;
+    const int Pc = K - D;
+    const int noct = (K + 7) / 8;
+    if (K + D > kcap) {
+      if (pend) {
+        gram_columns<D, NT>(Ub, Vb, ldu, ldv, GU, GV, kcap, Pc);
+        __syncthreads();
+        decide_step<D, NT>(GU, GV, kcap, Pc, eps, sh);
+        if (sh.stop) {
+          status = 1;
+          break;
+        }
+      }
+      status = 4;
+      break;
+    }
+    if (tid == 0) visited[ipiv] = 1;
+    for (int t = tid; t < D * lds; t += NT) {
+      const int a = t / lds, l = t - a * lds;
+      Urow[t] = l < K ? Ub[(int64_t)(D * ipiv + a) + (int64_t)l * ldu] : cmk(0.0, 0.0);
+    }
+    __syncthreads();
+
+    // ---- row pass over V ----------------------------------------------------------------
+    ArgMax best{-1.0, 0x7fffffff};
+    double rs1 = 0.0;
+    tc_pass(Vb, ldv, K, Urow, lds, pend, Pc, wscr, noct, resb, bnfw, [&](int64_t r0) {
+      // lanes 0..15: point j = r0 / 3 + lane, rows 3 lane + c of the block
+      const int p = lane;
+      const int j = (int)(r0 / 3) + p;
+      if (p < kTcRows / 3 && j < n) {
+        double2 R[9];
+        green_xy_k<KIND>(P, pts, ds.r0 + ipiv, pts, ds.c0 + j, R);
+#pragma unroll
+        for (int c = 0; c < 3; ++c) {
+          const double* rr = resb + (3 * p + c) * 12;  // V row 3 j + c
+#pragma unroll
+          for (int a = 0; a < 3; ++a) {
+            // sum_l Urow(a, l) conj V(q, l): re = C1[a] + C2[3 + a], im = C1[3 + a] - C2[a]
+            const double2 acc = cmk(rr[a] + rr[6 + 3 + a], rr[3 + a] - rr[6 + a]);
+            R[a * 3 + c] = csub(R[a * 3 + c], acc);
+          }
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) Vb[(int64_t)(3 * j + c) + (int64_t)(K + a) * ldv] = cconj(R[a * 3 + c]);
+        double s1, s3;
+        svals3(R, s1, s3);
+        rs1 = fmax(rs1, s1);
+        best = argmax_pick(best, ArgMax{s3, j});
+      }
+    });
+    best = warp_argmax(best);
+    rs1 = warp_max(rs1);
+    if (lane == 0) {
+      sh.red_v[warp] = best.v;
+      sh.red_i[warp] = best.i;
+      sh.red_s[warp] = rs1;
+    }
+    __syncthreads();
+    if (pend) tc_gram_finalize(scr, noct_cap, nwork_v, GV, kcap, Pc, K);
+    if (tid == 0) {
+      ArgMax bb{sh.red_v[0], sh.red_i[0]};
+      double r1 = sh.red_s[0];
+      for (int w = 1; w < NW; ++w) {
+        bb = argmax_pick(bb, ArgMax{sh.red_v[w], sh.red_i[w]});
+        r1 = fmax(r1, sh.red_s[w]);
+      }
+      sh.s1max = fmax(sh.s1max, r1);
+      if (r1 <= floor * sh.s1max || sh.s1max == 0.0) {
+        sh.rowout = kRowZero;
+        int nxt = -1;
+        for (int i = 0; i < m; ++i)
+          if (!visited[i]) {
+            nxt = i;
+            break;
+          }
+        sh.nextrow = nxt;
+      } else if (bb.v <= floor * sh.s1max) {
+        sh.rowout = kRowFallback;
+      } else {
+        sh.rowout = kRowPivot;
+        sh.jpiv = bb.i;
+        double2 Pv[9];
+        for (int a = 0; a < 3; ++a)
+          for (int c = 0; c < 3; ++c) Pv[a * 3 + c] = cconj(Vb[(int64_t)(3 * bb.i + c) + (int64_t)(K + a) * ldv]);
+        inverse<3>(Pv, sh.gamma);
+      }
+    }
+    __syncthreads();
+    if (sh.rowout != kRowPivot) {
+      if (pend) {  // settle the pending step from a standalone G_U column first
+        gram_columns<D, NT>(Ub, Vb, ldu, ldv, GU, GV, kcap, Pc, 1);
+        __syncthreads();
+        decide_step<D, NT>(GU, GV, kcap, Pc, eps, sh);
+        if (sh.stop) {
+          status = 1;
+          break;
+        }
+        if (tid == 0) s_pend = 0;
+      }
+      if (sh.rowout == kRowFallback) {
+        status = 8;
+        break;
+      }
+      if (tid == 0) {
+        sh.zero_rows++;
+        if (sh.nextrow < 0) {
+          sh.state = kDone;
+          sh.verdict = 1;
+        } else {
+          sh.ipiv = sh.nextrow;
+        }
+      }
+      __syncthreads();
+      if (sh.state == kDone) {
+        status = sh.verdict;
+        break;
+      }
+      continue;
+    }
+    const int jpiv = sh.jpiv;
+    for (int t = tid; t < D * lds; t += NT) {
+      const int c = t / lds, l = t - c * lds;
+      Vrow[t] = l < K ? Vb[(int64_t)(D * jpiv + c) + (int64_t)l * ldv] : cmk(0.0, 0.0);
+    }
+    double2 gam[9];
+#pragma unroll
+    for (int t = 0; t < 9; ++t) gam[t] = sh.gamma[t];
+    __syncthreads();
+
+    // ---- column pass over U ---------------------------------------------------------------
+    best = ArgMax{-1.0, 0x7fffffff};
+    tc_pass(Ub, ldu, K, Vrow, lds, pend, Pc, wscr, noct, resb, bnfw, [&](int64_t r0) {
+      const int p = lane;
+      const int i = (int)(r0 / 3) + p;
+      if (p < kTcRows / 3 && i < m) {
+        double2 C[9];
+        green_xy_k<KIND>(P, pts, ds.r0 + i, pts, ds.c0 + jpiv, C);
+#pragma unroll
+        for (int a = 0; a < 3; ++a) {
+          const double* rr = resb + (3 * p + a) * 12;  // U row 3 i + a
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            // sum_l U(q, l) conj Vrow(c, l): re = C1[c] + C2[3 + c], im = C2[c] - C1[3 + c]
+            const double2 acc = cmk(rr[c] + rr[6 + 3 + c], rr[6 + c] - rr[3 + c]);
+            C[a * 3 + c] = csub(C[a * 3 + c], acc);
+          }
+        }
+        if (!visited[i]) {
+          double s1, s3;
+          svals3(C, s1, s3);
+          best = argmax_pick(best, ArgMax{s3, i});
+        }
+#pragma unroll
+        for (int a = 0; a < 3; ++a)
+#pragma unroll
+          for (int c = 0; c < 3; ++c) {
+            double2 sacc = cmk(0.0, 0.0);
+#pragma unroll
+            for (int q = 0; q < 3; ++q) sacc = cfma(C[a * 3 + q], gam[q * 3 + c], sacc);
+            Ub[(int64_t)(3 * i + a) + (int64_t)(K + c) * ldu] = sacc;
+          }
+      }
+    });
+    best = warp_argmax(best);
+    if (lane == 0) {
+      sh.red_v[warp] = best.v;
+      sh.red_i[warp] = best.i;
+    }
+    __syncthreads();
+    if (pend) tc_gram_finalize(scr, noct_cap, nwork_u, GU, kcap, Pc, K);
+    if (tid == 0) {
+      ArgMax bb{sh.red_v[0], sh.red_i[0]};
+      for (int w = 1; w < NW; ++w) bb = argmax_pick(bb, ArgMax{sh.red_v[w], sh.red_i[w]});
+      sh.bbv = bb.v;
+      sh.bbi = bb.i;
+    }
+    __syncthreads();
+    if (pend) {
+      decide_step<D, NT>(GU, GV, kcap, Pc, eps, sh);
+      if (sh.stop) {  // the pending step converged: this one is discarded
+        status = 1;
+        break;
+      }
+    }
+    const int Kn = K + D;
+    const bool no_row = sh.bbv < 0.0;
+    if (Kn >= ds.max_rank || no_row) {
+      gram_columns<D, NT>(Ub, Vb, ldu, ldv, GU, GV, kcap, K);
+      __syncthreads();
+      decide_step<D, NT>(GU, GV, kcap, K, eps, sh);
+      if (tid == 0) {
+        sh.K = Kn;
+        sh.steps += 1;
+      }
+      const int dmin = D * (m < n ? m : n);
+      status = sh.stop ? 1 : (Kn >= ds.max_rank ? (2 | (Kn >= dmin ? 1 : 0)) : 1);
+      break;
+    }
+    if (tid == 0) {
+      sh.K = Kn;
+      sh.steps += 1;
+      s_pend = 1;
+      sh.ipiv = sh.bbi;
+    }
+    __syncthreads();
+  }
+  __syncthreads();
+  if (tid == 0) {
+    AcaOut o;
+    o.steps = sh.steps;
+    o.rank = sh.K;
+    o.status = status;
+    o.zero_rows = sh.zero_rows;
+    out[b] = o;
+  }
+}
+
+size_t aca_tc_smem(int kcap_max, int m_max) {
+  return sizeof(double2) * 2 * 3 * (size_t)(kcap_max + 8) + sizeof(double) * kTcWarps * (kTcRows * 12 + kTcKs * 32) +
+         (size_t)((m_max + 15) / 16) * 16;
+}
+
 }  // namespace
 
 void warm_aca() {
@@ -590,6 +1021,8 @@ void warm_aca() {
   cudaFuncGetAttributes(&a, aca_kernel<1, 0, 128, 4, kGramBatch>);
   cudaFuncGetAttributes(&a, aca_kernel<3, 1, 128, 4, kGramBatch>);
   cudaFuncGetAttributes(&a, aca_kernel<3, 2, 128, 4, kGramBatch>);
+  cudaFuncGetAttributes(&a, aca_tc_kernel<1>);
+  cudaFuncGetAttributes(&a, aca_tc_kernel<2>);
 }
 
 int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const AcaDesc* d_desc, const int32_t* d_order,
@@ -602,6 +1035,19 @@ int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const 
   const int nt = variant == kAcaNarrow ? 128 : 512;
   const char* e_b = std::getenv("HMX_ACA_GRAM_BATCH");
   const int batch = e_b ? std::atoi(e_b) : kGramBatch;
+  if (variant == kAcaTensor) {
+    const size_t smem_tc = aca_tc_smem(kcap_max, m_max);
+    auto go_tc = [&](auto kern) -> int {
+      HMX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tc));
+      kern<<<(unsigned)nblk, kTcThreads, smem_tc, c.stream>>>(P, pts, d_desc, d_order, eps, sigma3_floor, U, V, G,
+                                                               d_out, kcap_max);
+      return HMX_OK;
+    };
+    const int rc = P.kind == 1 ? go_tc(aca_tc_kernel<1>) : go_tc(aca_tc_kernel<2>);
+    if (rc) return rc;
+    HMX_CUDA_TRY(cudaGetLastError());
+    return HMX_OK;
+  }
   const size_t smem = sizeof(double2) * 2 * (size_t)d * kcap_max + (size_t)((m_max + 15) / 16) * 16;
   auto go = [&](auto kern) -> int {
     HMX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -526,8 +526,15 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   const double avail = (double)free_b + (double)c.cached_bytes;
   const double budget = cfg->mem_budget_gb > 0 ? cfg->mem_budget_gb * 1e9 : 0.55 * avail;
   auto round_d = [&](int64_t v) { return std::max<int64_t>(d, (v / d) * d); };
+  const char* e_nm0 = std::getenv("HMX_ACA_NARROW_MAX");
+  const int64_t nmax0 = e_nm0 ? std::atoll(e_nm0) : kAcaNarrowMax;
+  const char* e_tc = std::getenv("HMX_ACA_TC");
+  // tensor-core ACA for the wide d = 3 leaves (default; HMX_ACA_TC=0 selects the CUDA-core kernel)
+  const bool use_tc = d == 3 && !(e_tc && std::atoi(e_tc) == 0);
+  auto is_tc = [&](int64_t b) { return use_tc && rows_of(b) + cols_of(b) >= nmax0; };
   auto ws_bytes = [&](int64_t b, int64_t kc) {
-    return 16.0 * ((double)d * (rows_of(b) + cols_of(b)) * kc + 2.0 * kc * kc);
+    return 16.0 * ((double)d * (rows_of(b) + cols_of(b)) * kc + 2.0 * kc * kc +
+                   (is_tc(b) ? (double)aca_tc_scratch(kc) : 0.0));
   };
   {
     // Column capacity per leaf from a geometric rank model: ACA ranks of these
@@ -710,7 +717,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       D.goff = go;
       uo += (int64_t)d * D.m * D.kcap;
       vo += (int64_t)d * D.n * D.kcap;
-      go += 2 * (int64_t)D.kcap * D.kcap;
+      go += 2 * (int64_t)D.kcap * D.kcap + (is_tc(b) ? aca_tc_scratch(D.kcap) : 0);
       ps.kcap_max = std::max<int>(ps.kcap_max, D.kcap);
     }
     tick("aca: descriptors");
@@ -757,7 +764,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       if (nwide) {
         sub_max(0, nwide, kc, mm);
         if ((rc = launch_aca(c, d, P, pts.soa, d_desc, d_order, (int64_t)nwide, kc, mm, cfg->eps, s3f, ps.U, ps.V,
-                             ps.G, d_out, kAcaWide)))
+                             ps.G, d_out, use_tc ? kAcaTensor : kAcaWide)))
           return fail(rc);
       }
       mark("aca wide done");

@@ -152,6 +152,10 @@ struct AcaOut {
 constexpr int kAcaWide = 0;
 constexpr int kAcaNarrow = 1;
 constexpr int kAcaNarrowMax = 320;
+// tensor-core variant for large d = 3 leaves (default; HMX_ACA_TC=0 disables); its
+// per-warp Gram scratch sits behind the leaf's Gram pair: aca_tc_scratch(kcap) complex
+constexpr int kAcaTensor = 2;
+inline int64_t aca_tc_scratch(int64_t kcap) { return 16 * ((kcap + 7) / 8) * 64; }
 int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const AcaDesc* d_desc, const int32_t* d_order,
                int64_t nblk, int kcap_max, int m_max, double eps, double sigma3_floor, double2* U, double2* V,
                double2* G, AcaOut* d_out, int variant);
