@@ -599,8 +599,18 @@ __global__ void __launch_bounds__(NT, MINB) aca_kernel(GreenParams P, PointsSoA 
 // C1 = F_re B, C2 = F_im B.  Warp w owns row blocks of kTcRows rows (16 points),
 // loops over all column octets; Gram partials of its rows go to a per-warp
 // scratch slice in global memory (L2) and are summed in fixed warp order.
-constexpr int kTcRows = 48, kTcOct = kTcRows / 8, kTcKs = kTcRows / 4;
-constexpr int kTcThreads = 512, kTcWarps = kTcThreads / 32;
+#ifndef HMX_TC_ROWS
+#define HMX_TC_ROWS 48
+#endif
+constexpr int kTcRows = HMX_TC_ROWS, kTcOct = kTcRows / 8, kTcKs = kTcRows / 4;
+#ifndef HMX_TC_WARPS
+#define HMX_TC_WARPS 8
+#endif
+constexpr int kTcWarps = HMX_TC_WARPS, kTcThreads = 32 * kTcWarps;
+// per-warp cp.async ring: 2 stages of one column octet x kTcRows rows, columns
+// padded to kTcCol rows (the Gram fragments read 8 columns x 4 rows: the pad
+// spreads the 8 columns over all banks)
+constexpr int kTcCol = kTcRows + 4, kTcStage = 8 * kTcCol, kTcRing = 2 * kTcStage;  // double2 units
 
 HMX_D void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -616,84 +626,105 @@ HMX_D double piv_frag(const double2* piv, int lds, int l, int n) {
   return n < 3 ? v.x : v.y;
 }
 
+// 16-byte asynchronous global -> shared copy (zero fill when !valid)
+HMX_D void tc_cp16(double2* smem, const double2* gmem, bool valid) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0));
+}
+
 // Fused pass over panel F (rows = 3 npts, ld = rows, K columns) for the row
-// blocks of this warp.  Residual fragments of each row block are left in
-// resb (kTcRows x 12 doubles: C1 n = 0..5, C2 n = 0..5) and `epi(rb_row0)` is
-// called by the whole warp; with pend, the Gram partials of the pending
-// columns [Pc, Pc + 3) go to scr (this warp's slice: noct x 32 lanes x 4).
+// blocks of this warp.  Each column octet of a row block is brought into the
+// warp's shared-memory ring with cp.async one octet ahead (no registers held by
+// loads in flight), then feeds both contractions from shared memory.  Residual
+// fragments of each row block are left in resb (aliases the ring: kTcRows x 12
+// doubles, C1 n = 0..5 then C2 n = 0..5) and `epi(rb_row0)` is called by the
+// whole warp; with pend, the Gram partials of the pending columns [Pc, Pc + 3)
+// go to scr (this warp's slice: noct x 32 lanes x 4).
 template <class Epi>
 HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const double2* piv, int lds, bool pend,
-                   int Pc, double* __restrict__ scr, int noct, double* resb, double* bnf, Epi&& epi) {
+                   int Pc, double* __restrict__ scr, int noct, double2* ring, double2* nfs, Epi&& epi) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int fr = lane >> 2, fk = lane & 3;
+  double* resb = reinterpret_cast<double*>(ring);
   bool first = true;
   for (int64_t r0 = (int64_t)warp * kTcRows; r0 < rows; r0 += (int64_t)kTcWarps * kTcRows) {
-    // Gram B fragments (rows r0 + 4 j + fk, pending column / part fr) in this warp's smem slice
+    auto stage = [&](int co, int buf) {
 #pragma unroll
-    for (int j = 0; j < kTcKs; ++j) {
-      const int64_t q = r0 + 4 * j + fk;
-      double v = 0.0;
-      if (pend && fr < 6 && q < rows) {
-        const double2 x = F[q + (int64_t)(Pc + (fr < 3 ? fr : fr - 3)) * rows];
-        v = fr < 3 ? x.x : x.y;
+      for (int i = 0; i < (8 * kTcRows) / 32; ++i) {
+        const int e = lane + 32 * i;
+        const int col = e / kTcRows, row = e - col * kTcRows;
+        const int64_t q = r0 + row;
+        const int l = co * 8 + col;
+        const bool v = q < rows && l < K;
+        tc_cp16(ring + buf * kTcStage + col * kTcCol + row, F + (v ? q + (int64_t)l * rows : 0), v);
       }
-      bnf[j * 32 + lane] = v;
+      asm volatile("cp.async.commit_group;");
+    };
+    // pending columns of this row block (Gram B operand) ride along with stage 0
+    if (pend) {
+      for (int e = lane; e < 3 * kTcRows; e += 32) {
+        const int c = e / kTcRows, row = e - c * kTcRows;
+        const int64_t q = r0 + row;
+        const bool v = q < rows;
+        tc_cp16(nfs + c * kTcRows + row, F + (v ? q + (int64_t)(Pc + c) * rows : 0), v);
+      }
     }
-    __syncwarp();
+    stage(0, 0);
     double c1[kTcOct][2], c2[kTcOct][2];
 #pragma unroll
     for (int o = 0; o < kTcOct; ++o) c1[o][0] = c1[o][1] = c2[o][0] = c2[o][1] = 0.0;
     for (int co = 0; co < noct; ++co) {
+      if (co + 1 < noct) stage(co + 1, (co + 1) & 1);
+      else asm volatile("cp.async.commit_group;");
+      // this warp's Gram partials of the earlier row blocks (latency overlaps the residual MMAs)
+      double* d = scr + ((int64_t)co * 32 + lane) * 4;
+      double g3[2] = {0.0, 0.0}, g4[2] = {0.0, 0.0};
+      if (pend && !first) {
+        g3[0] = d[0];
+        g3[1] = d[1];
+        g4[0] = d[2];
+        g4[1] = d[3];
+      }
+      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      __syncwarp();
+      const double2* T = ring + (co & 1) * kTcStage;  // T[col * kTcCol + row]
       const int l0 = co * 8;
-      // residual: two k-steps of 4 columns (all fragment loads issued first)
-      double2 ar[2][kTcOct];
-      double br[2];
+      // residual: two k-steps of 4 columns
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
         const int l = l0 + 4 * h + fk;
-        br[h] = l < K ? piv_frag(piv, lds, l, fr) : 0.0;
+        const double b = l < K ? piv_frag(piv, lds, l, fr) : 0.0;
 #pragma unroll
         for (int o = 0; o < kTcOct; ++o) {
-          const int64_t q = r0 + 8 * o + fr;
-          ar[h][o] = (q < rows && l < K) ? F[q + (int64_t)l * rows] : cmk(0.0, 0.0);
+          const double2 a = T[(4 * h + fk) * kTcCol + 8 * o + fr];
+          dmma(c1[o][0], c1[o][1], a.x, b);
+          dmma(c2[o][0], c2[o][1], a.y, b);
         }
       }
-#pragma unroll
-      for (int h = 0; h < 2; ++h)
-#pragma unroll
-        for (int o = 0; o < kTcOct; ++o) {
-          dmma(c1[o][0], c1[o][1], ar[h][o].x, br[h]);
-          dmma(c2[o][0], c2[o][1], ar[h][o].y, br[h]);
-        }
       if (pend) {
-        double* d = scr + ((int64_t)co * 32 + lane) * 4;
-        double g3[2] = {0.0, 0.0}, g4[2] = {0.0, 0.0};
-        if (!first) {  // accumulate onto this warp's earlier row blocks (loads issued early)
-          g3[0] = d[0];
-          g3[1] = d[1];
-          g4[0] = d[2];
-          g4[1] = d[3];
-        }
-        const int l = l0 + fr;  // A' = F^T: m = column l0 + fr, k = row r0 + 4 j + fk
-        double2 ag[kTcKs];
+        // A' = F^T: m = column l0 + fr, k = row r0 + 4 j + fk
 #pragma unroll
         for (int j = 0; j < kTcKs; ++j) {
-          const int64_t q = r0 + 4 * j + fk;
-          ag[j] = (q < rows && l < K) ? F[q + (int64_t)l * rows] : cmk(0.0, 0.0);
-        }
-#pragma unroll
-        for (int j = 0; j < kTcKs; ++j) {
-          const double bj = bnf[j * 32 + lane];
-          dmma(g3[0], g3[1], ag[j].x, bj);
-          dmma(g4[0], g4[1], ag[j].y, bj);
+          const double2 a = T[fr * kTcCol + 4 * j + fk];
+          // B'[k][n] = pending column n mod 3 (re for n < 3, im for 3 <= n < 6) at row 4 j + k
+          double bj = 0.0;
+          if (fr < 6) {
+            const double2 x = nfs[(fr < 3 ? fr : fr - 3) * kTcRows + 4 * j + fk];
+            bj = fr < 3 ? x.x : x.y;
+          }
+          dmma(g3[0], g3[1], a.x, bj);
+          dmma(g4[0], g4[1], a.y, bj);
         }
         d[0] = g3[0];
         d[1] = g3[1];
         d[2] = g4[0];
         d[3] = g4[1];
       }
+      __syncwarp();  // this buffer is refilled by the next iteration's prefetch
     }
-    // residual fragments -> shared memory (rows of this block)
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncwarp();
+    // residual fragments -> shared memory (rows of this block; the ring is idle now)
 #pragma unroll
     for (int o = 0; o < kTcOct; ++o)
 #pragma unroll
@@ -761,10 +792,9 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int lds = kcap_max + 8;
   double2* Urow = dyn;                 // 3 x lds
   double2* Vrow = dyn + D * lds;       // 3 x lds
-  double* resb_all = reinterpret_cast<double*>(Vrow + D * lds);  // NW x kTcRows x 12
-  double* resb = resb_all + warp * kTcRows * 12;
-  double* bnfw = resb_all + NW * kTcRows * 12 + warp * kTcKs * 32;  // NW x kTcKs x 32
-  unsigned char* visited = reinterpret_cast<unsigned char*>(resb_all + NW * kTcRows * 12 + NW * kTcKs * 32);
+  double2* ring = Vrow + D * lds + warp * kTcRing;  // NW x kTcRing (residual buffer aliased)
+  double2* nfw = Vrow + D * lds + NW * kTcRing + warp * 3 * kTcRows;  // NW x 3 x kTcRows pending columns
+  unsigned char* visited = reinterpret_cast<unsigned char*>(Vrow + D * lds + NW * kTcRing + NW * 3 * kTcRows);
   const int nwork_v = min(NW, (int)((ldv + kTcRows - 1) / kTcRows));
   const int nwork_u = min(NW, (int)((ldu + kTcRows - 1) / kTcRows));
 
@@ -812,7 +842,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ---- row pass over V ----------------------------------------------------------------
     ArgMax best{-1.0, 0x7fffffff};
     double rs1 = 0.0;
-    tc_pass(Vb, ldv, K, Urow, lds, pend, Pc, wscr, noct, resb, bnfw, [&](int64_t r0) {
+    tc_pass(Vb, ldv, K, Urow, lds, pend, Pc, wscr, noct, ring, nfw, [&](int64_t r0) {
       // lanes 0..15: point j = r0 / 3 + lane, rows 3 lane + c of the block
       const int p = lane;
       const int j = (int)(r0 / 3) + p;
@@ -821,7 +851,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         green_xy_k<KIND>(P, pts, ds.r0 + ipiv, pts, ds.c0 + j, R);
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
-          const double* rr = resb + (3 * p + c) * 12;  // V row 3 j + c
+          const double* rr = reinterpret_cast<const double*>(ring) + (3 * p + c) * 12;  // V row 3 j + c
 #pragma unroll
           for (int a = 0; a < 3; ++a) {
             // sum_l Urow(a, l) conj V(q, l): re = C1[a] + C2[3 + a], im = C1[3 + a] - C2[a]
@@ -920,7 +950,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
     // ---- column pass over U ---------------------------------------------------------------
     best = ArgMax{-1.0, 0x7fffffff};
-    tc_pass(Ub, ldu, K, Vrow, lds, pend, Pc, wscr, noct, resb, bnfw, [&](int64_t r0) {
+    tc_pass(Ub, ldu, K, Vrow, lds, pend, Pc, wscr, noct, ring, nfw, [&](int64_t r0) {
       const int p = lane;
       const int i = (int)(r0 / 3) + p;
       if (p < kTcRows / 3 && i < m) {
@@ -928,7 +958,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
         green_xy_k<KIND>(P, pts, ds.r0 + i, pts, ds.c0 + jpiv, C);
 #pragma unroll
         for (int a = 0; a < 3; ++a) {
-          const double* rr = resb + (3 * p + a) * 12;  // U row 3 i + a
+          const double* rr = reinterpret_cast<const double*>(ring) + (3 * p + a) * 12;  // U row 3 i + a
 #pragma unroll
           for (int c = 0; c < 3; ++c) {
             // sum_l U(q, l) conj Vrow(c, l): re = C1[c] + C2[3 + c], im = C2[c] - C1[3 + c]
@@ -1007,7 +1037,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 }
 
 size_t aca_tc_smem(int kcap_max, int m_max) {
-  return sizeof(double2) * 2 * 3 * (size_t)(kcap_max + 8) + sizeof(double) * kTcWarps * (kTcRows * 12 + kTcKs * 32) +
+  return sizeof(double2) * (2 * 3 * (size_t)(kcap_max + 8) + (size_t)kTcWarps * (kTcRing + 3 * kTcRows)) +
          (size_t)((m_max + 15) / 16) * 16;
 }
 
