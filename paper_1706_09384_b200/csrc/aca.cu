@@ -610,7 +610,11 @@ constexpr int kTcWarps = HMX_TC_WARPS, kTcThreads = 32 * kTcWarps;
 // per-warp cp.async ring: 2 stages of one column octet x kTcRows rows, columns
 // padded to kTcCol rows (the Gram fragments read 8 columns x 4 rows: the pad
 // spreads the 8 columns over all banks)
-constexpr int kTcCol = kTcRows + 4, kTcStage = 8 * kTcCol, kTcRing = 2 * kTcStage;  // double2 units
+#ifndef HMX_TC_STAGES
+#define HMX_TC_STAGES 3
+#endif
+constexpr int kTcStages = HMX_TC_STAGES;
+constexpr int kTcCol = kTcRows + 4, kTcStage = 8 * kTcCol, kTcRing = kTcStages * kTcStage;  // double2 units
 
 HMX_D void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -669,12 +673,16 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
         tc_cp16(nfs + c * kTcRows + row, F + (v ? q + (int64_t)(Pc + c) * rows : 0), v);
       }
     }
-    stage(0, 0);
+#pragma unroll
+    for (int sidx = 0; sidx < kTcStages - 1; ++sidx) {
+      if (sidx < noct) stage(sidx, sidx);
+      else asm volatile("cp.async.commit_group;");
+    }
     double c1[kTcOct][2], c2[kTcOct][2];
 #pragma unroll
     for (int o = 0; o < kTcOct; ++o) c1[o][0] = c1[o][1] = c2[o][0] = c2[o][1] = 0.0;
     for (int co = 0; co < noct; ++co) {
-      if (co + 1 < noct) stage(co + 1, (co + 1) & 1);
+      if (co + kTcStages - 1 < noct) stage(co + kTcStages - 1, (co + kTcStages - 1) % kTcStages);
       else asm volatile("cp.async.commit_group;");
       // this warp's Gram partials of the earlier row blocks (latency overlaps the residual MMAs)
       double* d = scr + ((int64_t)co * 32 + lane) * 4;
@@ -685,9 +693,9 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
         g4[0] = d[2];
         g4[1] = d[3];
       }
-      asm volatile("cp.async.wait_group 1;" ::: "memory");
+      asm volatile("cp.async.wait_group %0;" ::"n"(kTcStages - 1) : "memory");
       __syncwarp();
-      const double2* T = ring + (co & 1) * kTcStage;  // T[col * kTcCol + row]
+      const double2* T = ring + (co % kTcStages) * kTcStage;  // T[col * kTcCol + row]
       const int l0 = co * 8;
       // residual: two k-steps of 4 columns
 #pragma unroll
@@ -702,7 +710,10 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
         }
       }
       if (pend) {
-        // A' = F^T: m = column l0 + fr, k = row r0 + 4 j + fk
+        // A' = F^T: m = column l0 + fr, k = row r0 + 4 j + fk; 3 independent
+        // accumulator chains (a single chain serialises on the MMA latency)
+        double h3[3][2] = {{g3[0], g3[1]}, {0.0, 0.0}, {0.0, 0.0}};
+        double h4[3][2] = {{g4[0], g4[1]}, {0.0, 0.0}, {0.0, 0.0}};
 #pragma unroll
         for (int j = 0; j < kTcKs; ++j) {
           const double2 a = T[fr * kTcCol + 4 * j + fk];
@@ -712,9 +723,13 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
             const double2 x = nfs[(fr < 3 ? fr : fr - 3) * kTcRows + 4 * j + fk];
             bj = fr < 3 ? x.x : x.y;
           }
-          dmma(g3[0], g3[1], a.x, bj);
-          dmma(g4[0], g4[1], a.y, bj);
+          dmma(h3[j % 3][0], h3[j % 3][1], a.x, bj);
+          dmma(h4[j % 3][0], h4[j % 3][1], a.y, bj);
         }
+        g3[0] = (h3[0][0] + h3[1][0]) + h3[2][0];
+        g3[1] = (h3[0][1] + h3[1][1]) + h3[2][1];
+        g4[0] = (h4[0][0] + h4[1][0]) + h4[2][0];
+        g4[1] = (h4[0][1] + h4[1][1]) + h4[2][1];
         d[0] = g3[0];
         d[1] = g3[1];
         d[2] = g4[0];
