@@ -610,11 +610,7 @@ constexpr int kTcWarps = HMX_TC_WARPS, kTcThreads = 32 * kTcWarps;
 // per-warp cp.async ring: 2 stages of one column octet x kTcRows rows, columns
 // padded to kTcCol rows (the Gram fragments read 8 columns x 4 rows: the pad
 // spreads the 8 columns over all banks)
-#ifndef HMX_TC_STAGES
-#define HMX_TC_STAGES 3
-#endif
-constexpr int kTcStages = HMX_TC_STAGES;
-constexpr int kTcCol = kTcRows + 4, kTcStage = 8 * kTcCol, kTcRing = kTcStages * kTcStage;  // double2 units
+constexpr int kTcCol = kTcRows + 4, kTcStage = 8 * kTcCol;  // double2 units; ring = STAGES x kTcStage
 
 HMX_D void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -644,7 +640,7 @@ HMX_D void tc_cp16(double2* smem, const double2* gmem, bool valid) {
 // doubles, C1 n = 0..5 then C2 n = 0..5) and `epi(rb_row0)` is called by the
 // whole warp; with pend, the Gram partials of the pending columns [Pc, Pc + 3)
 // go to scr (this warp's slice: noct x 32 lanes x 4).
-template <class Epi>
+template <int kTcStages, class Epi>
 HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const double2* piv, int lds, bool pend,
                    int Pc, double* __restrict__ scr, int noct, double2* ring, double2* nfs, Epi&& epi) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -783,7 +779,7 @@ HMX_D void tc_gram_finalize(const double* __restrict__ scr, int noct, int nwork,
   }
 }
 
-template <int KIND>
+template <int KIND, int STAGES>
 __global__ void __launch_bounds__(kTcThreads, 1)
     aca_tc_kernel(GreenParams P, PointsSoA pts, const AcaDesc* __restrict__ desc, const int32_t* __restrict__ order,
                   double eps, double floor, double2* __restrict__ U, double2* __restrict__ V,
@@ -807,6 +803,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   const int lds = kcap_max + 8;
   double2* Urow = dyn;                 // 3 x lds
   double2* Vrow = dyn + D * lds;       // 3 x lds
+  constexpr int kTcRing = STAGES * kTcStage;
   double2* ring = Vrow + D * lds + warp * kTcRing;  // NW x kTcRing (residual buffer aliased)
   double2* nfw = Vrow + D * lds + NW * kTcRing + warp * 3 * kTcRows;  // NW x 3 x kTcRows pending columns
   unsigned char* visited = reinterpret_cast<unsigned char*>(Vrow + D * lds + NW * kTcRing + NW * 3 * kTcRows);
@@ -857,7 +854,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
     // ---- row pass over V ----------------------------------------------------------------
     ArgMax best{-1.0, 0x7fffffff};
     double rs1 = 0.0;
-    tc_pass(Vb, ldv, K, Urow, lds, pend, Pc, wscr, noct, ring, nfw, [&](int64_t r0) {
+    tc_pass<STAGES>(Vb, ldv, K, Urow, lds, pend, Pc, wscr, noct, ring, nfw, [&](int64_t r0) {
       // lanes 0..15: point j = r0 / 3 + lane, rows 3 lane + c of the block
       const int p = lane;
       const int j = (int)(r0 / 3) + p;
@@ -965,7 +962,7 @@ __global__ void __launch_bounds__(kTcThreads, 1)
 
     // ---- column pass over U ---------------------------------------------------------------
     best = ArgMax{-1.0, 0x7fffffff};
-    tc_pass(Ub, ldu, K, Vrow, lds, pend, Pc, wscr, noct, ring, nfw, [&](int64_t r0) {
+    tc_pass<STAGES>(Ub, ldu, K, Vrow, lds, pend, Pc, wscr, noct, ring, nfw, [&](int64_t r0) {
       const int p = lane;
       const int i = (int)(r0 / 3) + p;
       if (p < kTcRows / 3 && i < m) {
@@ -1051,8 +1048,8 @@ __global__ void __launch_bounds__(kTcThreads, 1)
   }
 }
 
-size_t aca_tc_smem(int kcap_max, int m_max) {
-  return sizeof(double2) * (2 * 3 * (size_t)(kcap_max + 8) + (size_t)kTcWarps * (kTcRing + 3 * kTcRows)) +
+size_t aca_tc_smem(int kcap_max, int m_max, int stages) {
+  return sizeof(double2) * (2 * 3 * (size_t)(kcap_max + 8) + (size_t)kTcWarps * (stages * kTcStage + 3 * kTcRows)) +
          (size_t)((m_max + 15) / 16) * 16;
 }
 
@@ -1066,8 +1063,10 @@ void warm_aca() {
   cudaFuncGetAttributes(&a, aca_kernel<1, 0, 128, 4, kGramBatch>);
   cudaFuncGetAttributes(&a, aca_kernel<3, 1, 128, 4, kGramBatch>);
   cudaFuncGetAttributes(&a, aca_kernel<3, 2, 128, 4, kGramBatch>);
-  cudaFuncGetAttributes(&a, aca_tc_kernel<1>);
-  cudaFuncGetAttributes(&a, aca_tc_kernel<2>);
+  cudaFuncGetAttributes(&a, aca_tc_kernel<1, 3>);
+  cudaFuncGetAttributes(&a, aca_tc_kernel<2, 3>);
+  cudaFuncGetAttributes(&a, aca_tc_kernel<1, 2>);
+  cudaFuncGetAttributes(&a, aca_tc_kernel<2, 2>);
 }
 
 int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const AcaDesc* d_desc, const int32_t* d_order,
@@ -1081,17 +1080,27 @@ int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const 
   const char* e_b = std::getenv("HMX_ACA_GRAM_BATCH");
   const int batch = e_b ? std::atoi(e_b) : kGramBatch;
   if (variant == kAcaTensor) {
-    const size_t smem_tc = aca_tc_smem(kcap_max, m_max);
-    auto go_tc = [&](auto kern) -> int {
-      HMX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tc));
-      kern<<<(unsigned)nblk, kTcThreads, smem_tc, c.stream>>>(P, pts, d_desc, d_order, eps, sigma3_floor, U, V, G,
-                                                               d_out, kcap_max);
+    // 3-stage ring when it fits in shared memory, else 2 stages, else the CUDA-core kernel
+    int smem_max = 0;
+    HMX_CUDA_TRY(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+    const int stages = aca_tc_smem(kcap_max, m_max, 3) <= (size_t)smem_max   ? 3
+                       : aca_tc_smem(kcap_max, m_max, 2) <= (size_t)smem_max ? 2
+                                                                               : 0;
+    if (stages) {
+      const size_t smem_tc = aca_tc_smem(kcap_max, m_max, stages);
+      auto go_tc = [&](auto kern) -> int {
+        HMX_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_tc));
+        kern<<<(unsigned)nblk, kTcThreads, smem_tc, c.stream>>>(P, pts, d_desc, d_order, eps, sigma3_floor, U, V,
+                                                                 G, d_out, kcap_max);
+        return HMX_OK;
+      };
+      const int rc = stages == 3 ? (P.kind == 1 ? go_tc(aca_tc_kernel<1, 3>) : go_tc(aca_tc_kernel<2, 3>))
+                                 : (P.kind == 1 ? go_tc(aca_tc_kernel<1, 2>) : go_tc(aca_tc_kernel<2, 2>));
+      if (rc) return rc;
+      HMX_CUDA_TRY(cudaGetLastError());
       return HMX_OK;
-    };
-    const int rc = P.kind == 1 ? go_tc(aca_tc_kernel<1>) : go_tc(aca_tc_kernel<2>);
-    if (rc) return rc;
-    HMX_CUDA_TRY(cudaGetLastError());
-    return HMX_OK;
+    }
+    variant = kAcaWide;
   }
   const size_t smem = sizeof(double2) * 2 * (size_t)d * kcap_max + (size_t)((m_max + 15) / 16) * 16;
   auto go = [&](auto kern) -> int {
