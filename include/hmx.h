@@ -73,7 +73,7 @@ typedef struct {
   double sigma3_floor;   /* relative sigma_3 floor, default 1e-12 */
   int32_t trunc_rule;    /* HMX_TRUNC_* */
   int32_t pad;
-  double mem_budget_gb;  /* ACA workspace budget; <= 0: 55% of free (+ cached) device memory */
+  double mem_budget_gb;  /* ACA workspace budget; <= 0: 70% of free (+ cached) device memory */
 } hmx_aca_cfg;
 
 typedef struct {

@@ -110,6 +110,9 @@ namespace {
 using namespace hmx;
 
 constexpr int kMaxAcaCols = 1020;  // per-leaf ACA column limit (recompress.cu vector sizes)
+// share of (free + cached) HBM for the ACA workspaces U, V, G: the Grams are released
+// before the final streams are allocated, so U + V + streams stay well inside 180 GB
+constexpr double kAcaBudgetFrac = 0.7;
 
 GreenParams make_params(const hmx_kernel* k, int has_shift, double shift) {
   GreenParams P;
@@ -522,9 +525,9 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   size_t free_b = 0, total_b = 0;
   HMX_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
   // memory cached by this context counts as free; U, V and the Gram matrices get
-  // 55% (the Grams are released before the final streams are allocated)
-  const double avail = (double)free_b + (double)c.cached_bytes;
-  const double budget = cfg->mem_budget_gb > 0 ? cfg->mem_budget_gb * 1e9 : 0.55 * avail;
+  // kAcaBudgetFrac of it (the Grams are released before the final streams are allocated)
+  double avail = (double)free_b + (double)c.cached_bytes;
+  double budget = cfg->mem_budget_gb > 0 ? cfg->mem_budget_gb * 1e9 : kAcaBudgetFrac * avail;
   auto round_d = [&](int64_t v) { return std::max<int64_t>(d, (v / d) * d); };
   const char* e_nm0 = std::getenv("HMX_ACA_NARROW_MAX");
   const int64_t nmax0 = e_nm0 ? std::atoll(e_nm0) : kAcaNarrowMax;
@@ -572,6 +575,17 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     // fit the budget: scale the model down uniformly if needed
     double need = 0;
     for (int64_t b : adm) need += ws_bytes(b, kcap[b]);
+    if (need > budget && c.cached_bytes > 0 && cfg->mem_budget_gb <= 0) {
+      // blocks cached for other sizes may not be reusable: hand them back and
+      // size the budget from what is really free (a scaled-down capacity model
+      // turns into expensive overflow reruns)
+      release_cache(c);
+      HMX_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+      avail = (double)free_b;
+      budget = kAcaBudgetFrac * avail;
+    }
+    if (verbose)
+      std::fprintf(stderr, "[hmx] ACA workspace model %.2f GB, budget %.2f GB\n", need / 1e9, budget / 1e9);
     if (need > budget) {
       const double f = budget / need;
       for (int64_t b : adm) kcap[b] = std::max<int64_t>(d, round_d((int64_t)(kcap[b] * f)));
