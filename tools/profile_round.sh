@@ -9,7 +9,7 @@ python bench.py --steps 100 --warmup 5 > gpurun_out/bench.json 2> gpurun_out/ben
 python tools/ncu_target.py U32k 3 > gpurun_out/plain.log 2>&1 || exit 1
 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/launches_U32k.csv \
     python tools/ncu_target.py U32k 3 > gpurun_out/ncu_launch.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:aca_kernel -c 2 -o gpurun_out/prof_aca \
+ncu --set full --import-source on --clock-control none -k regex:"aca_(tc_)?kernel" -c 2 -o gpurun_out/prof_aca \
     python tools/ncu_target.py U32k 1 > gpurun_out/ncu_aca.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:mv_phase -c 2 -o gpurun_out/prof_mv \
     python tools/ncu_target.py U32k 1 > gpurun_out/ncu_mv.log 2>&1
