@@ -677,17 +677,26 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
     double c1[kTcOct][2], c2[kTcOct][2];
 #pragma unroll
     for (int o = 0; o < kTcOct; ++o) c1[o][0] = c1[o][1] = c2[o][0] = c2[o][1] = 0.0;
+    double nx[4] = {0.0, 0.0, 0.0, 0.0};  // scratch partials of the next octet (prefetched)
+    if (pend && !first) {
+      const double* d0 = scr + (int64_t)lane * 4;
+      nx[0] = d0[0];
+      nx[1] = d0[1];
+      nx[2] = d0[2];
+      nx[3] = d0[3];
+    }
     for (int co = 0; co < noct; ++co) {
       if (co + kTcStages - 1 < noct) stage(co + kTcStages - 1, (co + kTcStages - 1) % kTcStages);
       else asm volatile("cp.async.commit_group;");
-      // this warp's Gram partials of the earlier row blocks (latency overlaps the residual MMAs)
+      // this warp's Gram partials of the earlier row blocks: loaded one octet ahead
       double* d = scr + ((int64_t)co * 32 + lane) * 4;
-      double g3[2] = {0.0, 0.0}, g4[2] = {0.0, 0.0};
-      if (pend && !first) {
-        g3[0] = d[0];
-        g3[1] = d[1];
-        g4[0] = d[2];
-        g4[1] = d[3];
+      double g3[2] = {nx[0], nx[1]}, g4[2] = {nx[2], nx[3]};
+      if (pend && !first && co + 1 < noct) {
+        const double* dn = d + 128;
+        nx[0] = dn[0];
+        nx[1] = dn[1];
+        nx[2] = dn[2];
+        nx[3] = dn[3];
       }
       asm volatile("cp.async.wait_group %0;" ::"n"(kTcStages - 1) : "memory");
       __syncwarp();
@@ -706,10 +715,15 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
         }
       }
       if (pend) {
-        // A' = F^T: m = column l0 + fr, k = row r0 + 4 j + fk; 3 independent
-        // accumulator chains (a single chain serialises on the MMA latency)
-        double h3[3][2] = {{g3[0], g3[1]}, {0.0, 0.0}, {0.0, 0.0}};
-        double h4[3][2] = {{g4[0], g4[1]}, {0.0, 0.0}, {0.0, 0.0}};
+        // A' = F^T: m = column l0 + fr, k = row r0 + 4 j + fk; 6 independent
+        // accumulator chains (a short chain serialises on the MMA latency)
+        double h3[6][2], h4[6][2];
+#pragma unroll
+        for (int cidx = 0; cidx < 6; ++cidx) h3[cidx][0] = h3[cidx][1] = h4[cidx][0] = h4[cidx][1] = 0.0;
+        h3[0][0] = g3[0];
+        h3[0][1] = g3[1];
+        h4[0][0] = g4[0];
+        h4[0][1] = g4[1];
 #pragma unroll
         for (int j = 0; j < kTcKs; ++j) {
           const double2 a = T[fr * kTcCol + 4 * j + fk];
@@ -719,13 +733,13 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
             const double2 x = nfs[(fr < 3 ? fr : fr - 3) * kTcRows + 4 * j + fk];
             bj = fr < 3 ? x.x : x.y;
           }
-          dmma(h3[j % 3][0], h3[j % 3][1], a.x, bj);
-          dmma(h4[j % 3][0], h4[j % 3][1], a.y, bj);
+          dmma(h3[j % 6][0], h3[j % 6][1], a.x, bj);
+          dmma(h4[j % 6][0], h4[j % 6][1], a.y, bj);
         }
-        g3[0] = (h3[0][0] + h3[1][0]) + h3[2][0];
-        g3[1] = (h3[0][1] + h3[1][1]) + h3[2][1];
-        g4[0] = (h4[0][0] + h4[1][0]) + h4[2][0];
-        g4[1] = (h4[0][1] + h4[1][1]) + h4[2][1];
+        g3[0] = ((h3[0][0] + h3[1][0]) + (h3[2][0] + h3[3][0])) + (h3[4][0] + h3[5][0]);
+        g3[1] = ((h3[0][1] + h3[1][1]) + (h3[2][1] + h3[3][1])) + (h3[4][1] + h3[5][1]);
+        g4[0] = ((h4[0][0] + h4[1][0]) + (h4[2][0] + h4[3][0])) + (h4[4][0] + h4[5][0]);
+        g4[1] = ((h4[0][1] + h4[1][1]) + (h4[2][1] + h4[3][1])) + (h4[4][1] + h4[5][1]);
         d[0] = g3[0];
         d[1] = g3[1];
         d[2] = g4[0];
