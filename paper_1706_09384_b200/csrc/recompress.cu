@@ -16,6 +16,9 @@
 
 #include "hmatrix.h"
 
+#ifndef HMX_RC_MINB
+#define HMX_RC_MINB 1
+#endif
 namespace hmx {
 
 namespace {
@@ -526,7 +529,7 @@ HMX_D void recompress_truncate(const double* lam, const int* ordr, int K, double
 // T / L_r all in shared memory (small K: the O(K) sequential phases then run
 // at shared-memory instead of L2 latency)
 template <int MODE, int NT>
-__global__ void __launch_bounds__(NT) recompress_core(const RecDesc* __restrict__ desc, double eps, int rule,
+__global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1) recompress_core(const RecDesc* __restrict__ desc, double eps, int rule,
                                                             const double2* __restrict__ G, double2* __restrict__ W,
                                                             int32_t* __restrict__ rank_out,
                                                             int32_t* __restrict__ flags_out) {
