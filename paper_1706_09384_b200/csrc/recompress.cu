@@ -17,7 +17,7 @@
 #include "hmatrix.h"
 
 #ifndef HMX_RC_MINB
-#define HMX_RC_MINB 1
+#define HMX_RC_MINB 8
 #endif
 namespace hmx {
 
