@@ -212,6 +212,86 @@ __device__ void tridiagonalize(double2* E, int K, double* d, double* e, double2*
   __syncthreads();
 }
 
+// Packed lower-triangular Hermitian storage (column-major): element (i, j),
+// i >= j, at pk_col(j, K) + (i - j).  Halves the shared memory of E, so twice
+// as many leaves are resident per SM in the latency-bound small-K classes.
+HMX_HD int pk_col(int j, int K) { return j * (2 * K - j + 1) / 2; }
+
+// Same reduction as tridiagonalize, on packed lower storage; the Householder
+// vectors end up in the strictly lower part of the packed columns.
+template <int NT>
+__device__ void tridiagonalize_packed(double2* E, int K, double* d, double* e, double2* tau, double2* vbuf,
+                                      double2* pbuf, Scalars& S, double* red) {
+  const int tid = threadIdx.x;
+  for (int k = 0; k + 1 < K; ++k) {
+    const int n = K - k - 1;
+    double2* col = E + pk_col(k, K) + 1;  // x, length n
+    double xn2 = 0.0;
+    for (int i = 1 + tid; i < n; i += NT) xn2 += cabs2(col[i]);
+    xn2 = block_sum<NT>(xn2, red);
+    if (tid == 0) {
+      const double2 alpha = col[0];
+      d[k] = E[pk_col(k, K)].x;
+      if (xn2 == 0.0 && alpha.y == 0.0) {
+        S.tau = cmk(0.0, 0.0);
+        S.beta = alpha.x;
+      } else {
+        const double nrm = sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xn2);
+        const double beta = alpha.x >= 0.0 ? -nrm : nrm;
+        S.beta = beta;
+        S.tau = cmk((beta - alpha.x) / beta, -alpha.y / beta);
+        S.scale = cdiv(cmk(1.0, 0.0), csub(alpha, cmk(beta, 0.0)));
+      }
+      e[k] = S.beta;
+      tau[k] = S.tau;
+    }
+    __syncthreads();
+    const double2 tk = S.tau;
+    if (tk.x == 0.0 && tk.y == 0.0) continue;
+    const double2 sc = S.scale;
+    for (int i = tid; i < n; i += NT) {
+      const double2 vi = i == 0 ? cmk(1.0, 0.0) : cmul(col[i], sc);
+      vbuf[i] = vi;
+      col[i] = vi;
+    }
+    __syncthreads();
+    // p = tau A' v, A' = E(k+1:, k+1:): row i of the Hermitian trailing block is
+    // column gi below the diagonal and the conjugated row gi left of it
+    const int g0 = k + 1;
+    for (int i = tid; i < n; i += NT) {
+      const int gi = g0 + i;
+      double2 s0 = cmk(0.0, 0.0), s1 = cmk(0.0, 0.0);
+      for (int j = 0; j < i; ++j) s0 = cfma(E[pk_col(g0 + j, K) + (i - j)], vbuf[j], s0);
+      const double2* ci = E + pk_col(gi, K);  // column gi, rows gi..K-1
+      for (int j = i; j < n; ++j) s1 = cfma_cj(vbuf[j], ci[j - i], s1);  // conj(A(j, i)) v_j
+      // diagonal term: A(i, i) real; cfma_cj used conj(A(i, i)) = A(i, i)
+      pbuf[i] = cmul(tk, cadd(s0, s1));
+    }
+    __syncthreads();
+    double2 dot = cmk(0.0, 0.0);
+    for (int i = tid; i < n; i += NT) dot = cfma_ca(pbuf[i], vbuf[i], dot);  // sum conj(p) v
+    dot = block_sum2<NT>(dot, red);
+    const double2 a2 = cscale(cmul(tk, dot), -0.5);
+    for (int i = tid; i < n; i += NT) pbuf[i] = cadd(pbuf[i], cmul(a2, vbuf[i]));  // w
+    __syncthreads();
+    for (int t = tid; t < n * n; t += NT) {
+      const int i = t % n, j = t / n;
+      if (i < j) continue;
+      double2* ap = E + pk_col(g0 + j, K) + (i - j);
+      double2 a = *ap;
+      a = csub(a, cmul(vbuf[i], cconj(pbuf[j])));
+      a = csub(a, cmul(pbuf[i], cconj(vbuf[j])));
+      *ap = a;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    d[K - 1] = E[pk_col(K - 1, K)].x;
+    e[K - 1] = 0.0;
+  }
+  __syncthreads();
+}
+
 // Implicit QL with Wilkinson-type shift on the real symmetric tridiagonal
 // (d, e); eigenvectors accumulated in Z (row-major, ld ldz, identity on
 // entry).  The rotation chain of one QL iteration is generated by thread 0
@@ -572,12 +652,13 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1
   int ldz;
   double2* gtile = reinterpret_cast<double2*>(ordr + K + (K & 1) + 2);
   gtile = reinterpret_cast<double2*>((reinterpret_cast<uintptr_t>(gtile) + 15) & ~uintptr_t(15));
+  const int KP = K * (K + 1) / 2;  // packed lower-triangular size
   if (SMEM) {
-    E = gtile;  // no GEMM tiles in the shared-memory variant
-    Z = reinterpret_cast<double*>(E);  // overlays E after the reduction (8 K (K+1) <= 16 K^2 bytes)
+    E = gtile;  // packed lower triangle (pk_col); no GEMM tiles in the shared-memory variant
+    Z = reinterpret_cast<double*>(E);  // QL fallback overlays E: K (K+1) doubles = packed E bytes
     ldz = K + 1;
     if (MODE == 2) {
-      A = E + KK;
+      A = E + KP;
       B = A + KK;
     }
   } else {
@@ -640,28 +721,37 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1
       B[t] = s;
     }
     __syncthreads();
+    // lower triangle only (E is Hermitian), packed
     for (int t = tid; t < K * K; t += NT) {
       const int i = t % K, j = t / K;
+      if (i < j) continue;
       double2 s = cmk(0.0, 0.0);
       for (int k = j; k < K; ++k) s = cfma_cj(B[i + (int64_t)k * K], A[j + (int64_t)k * K], s);
-      E[i + (int64_t)j * K] = s;
+      if (i == j) s.y = 0.0;
+      E[pk_col(j, K) + (i - j)] = s;
     }
     __syncthreads();
   }
-  for (int t = tid; t < K * K; t += NT) {  // Hermitian symmetrise (roundoff)
-    const int i = t % K, j = t / K;
-    if (i < j) {
-      const double2 a = E[i + (int64_t)j * K], b = E[j + (int64_t)i * K];
-      const double2 h = cscale(cadd(a, cconj(b)), 0.5);
-      E[i + (int64_t)j * K] = h;
-      E[j + (int64_t)i * K] = cconj(h);
-    } else if (i == j) {
-      E[i + (int64_t)i * K].y = 0.0;
+  if constexpr (!SMEM) {
+    for (int t = tid; t < K * K; t += NT) {  // Hermitian symmetrise (roundoff)
+      const int i = t % K, j = t / K;
+      if (i < j) {
+        const double2 a = E[i + (int64_t)j * K], b = E[j + (int64_t)i * K];
+        const double2 h = cscale(cadd(a, cconj(b)), 0.5);
+        E[i + (int64_t)j * K] = h;
+        E[j + (int64_t)i * K] = cconj(h);
+      } else if (i == j) {
+        E[i + (int64_t)i * K].y = 0.0;
+      }
     }
+    __syncthreads();
   }
-  __syncthreads();
   // ---- eigen-decomposition E = Q Z diag(lam) Z^T Q^H --------------------------------
-  tridiagonalize<NT>(E, K, d, e, tau, vbuf, pbuf, S, red);
+  if constexpr (SMEM)
+    tridiagonalize_packed<NT>(E, K, d, e, tau, vbuf, pbuf, S, red);
+  else
+    tridiagonalize<NT>(E, K, d, e, tau, vbuf, pbuf, S, red);
+  bool hv_packed = SMEM;  // reflector k at E + pk_col(k, K) + 1 (else Hv(k+1:, k), ld K)
   double2* Hv = E;  // Householder vectors v_k = Hv(k+1:, k)
   // fast path: bisection eigenvalues + twisted eigenvectors (rc: e^2 scratch)
   double pivmin = 0.0;
@@ -689,8 +779,9 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1
       Hv = gA + 2 * KK;
       for (int t = tid; t < K * K; t += NT) {
         const int i = t % K, j = t / K;
-        if (i > j) Hv[t] = E[t];
+        if (i > j) Hv[t] = E[pk_col(j, K) + (i - j)];
       }
+      hv_packed = false;
       __syncthreads();
     }
     tridiag_ql<NT>(d, e, Z, ldz, K, rc, rs, S);
@@ -723,7 +814,7 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1
     const double2 tk = tau[k];
     if (tk.x == 0.0 && tk.y == 0.0) continue;
     const int n = K - k - 1;
-    const double2* v = Hv + (k + 1) + (int64_t)k * K;
+    const double2* v = hv_packed ? E + pk_col(k, K) + 1 : Hv + (k + 1) + (int64_t)k * K;
     // s_c = v^H B(k+1:, c), one warp per column
     const int lane = tid & 31, warp = tid >> 5;
     for (int c = warp; c < r; c += NT / 32) {
@@ -916,11 +1007,11 @@ int launch_recompress_core(Ctx& c, const RecDesc* d_desc, int64_t nblk, int kmax
   const char* e_all = std::getenv("HMX_RC_ALLSMEM_MAX");
   const int all_max = e_all ? std::atoi(e_all) : kRecompressAllSmemMax;
   if (kmax <= all_max) {
-    const size_t smem = vec + 3 * sizeof(double2) * (size_t)kmax * kmax;
+    const size_t smem = vec + sizeof(double2) * ((size_t)kmax * (kmax + 1) / 2 + 2 * (size_t)kmax * kmax);
     HMX_CUDA_TRY(cudaFuncSetAttribute(recompress_core<2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     recompress_core<2, 128><<<(unsigned)nblk, 128, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
   } else if (kmax <= kRecompressSmemMax) {
-    const size_t smem = vec + sizeof(double2) * (size_t)kmax * kmax;
+    const size_t smem = vec + sizeof(double2) * ((size_t)kmax * (kmax + 1) / 2);  // packed E
     if (kmax <= 64) {
       HMX_CUDA_TRY(
           cudaFuncSetAttribute(recompress_core<1, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
