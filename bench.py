@@ -424,6 +424,10 @@ def hmx_arm(args):
                              "worst_leaf_eps": float(ratio.max()), "leaves_above_eps": int((ratio > 1).sum()),
                              "leaves_above_3eps": int((ratio > 3).sum())}
     if not args.no_solve:
+        # its own job: the U32k H-matrix and the cached workspaces are handed back first
+        del H
+        L.hmx_ctx_release_cache(_lib.context(local))
+        torch.cuda.synchronize()
         line["time_to_solve"] = time_to_solve(args.solve_config, local)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
