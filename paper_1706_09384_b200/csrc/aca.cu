@@ -793,8 +793,11 @@ HMX_D void tc_gram_finalize(const double* __restrict__ scr, int noct, int nwork,
   }
 }
 
+#ifndef HMX_TC_MINB
+#define HMX_TC_MINB 1
+#endif
 template <int KIND, int STAGES>
-__global__ void __launch_bounds__(kTcThreads, 1)
+__global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
     aca_tc_kernel(GreenParams P, PointsSoA pts, const AcaDesc* __restrict__ desc, const int32_t* __restrict__ order,
                   double eps, double floor, double2* __restrict__ U, double2* __restrict__ V,
                   double2* __restrict__ G, AcaOut* __restrict__ out, int kcap_max) {
@@ -1097,7 +1100,9 @@ int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const 
     // 3-stage ring when it fits in shared memory, else 2 stages, else the CUDA-core kernel
     int smem_max = 0;
     HMX_CUDA_TRY(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
-    const int stages = aca_tc_smem(kcap_max, m_max, 3) <= (size_t)smem_max   ? 3
+    const char* e_st = std::getenv("HMX_TC_STAGES");
+    const int want = e_st ? std::atoi(e_st) : 3;
+    const int stages = want >= 3 && aca_tc_smem(kcap_max, m_max, 3) <= (size_t)smem_max ? 3
                        : aca_tc_smem(kcap_max, m_max, 2) <= (size_t)smem_max ? 2
                                                                                : 0;
     if (stages) {
