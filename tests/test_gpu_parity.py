@@ -160,3 +160,34 @@ def test_gmres_iterations_vs_oracle(tag, n):
     assert all(h1 <= h0 * (1 + 1e-12) for h0, h1 in zip(res.history, res.history[1:]))
     z = hmx.solve_gmres(H, np.zeros_like(b))
     assert z.iters == 0 and not np.any(z.x)
+
+
+@pytest.mark.parametrize("tag,n", [("U8k", 4096), ("T65k", 4096)])
+def test_aca_kernel_variants_agree(tag, n, monkeypatch):
+    """The three ACA kernels for large d = 3 leaves (m + n >= 320 points) --
+    tensor-core with a 3-stage ring (default), tensor-core with a 2-stage
+    ring, CUDA-core (HMX_ACA_TC=0) -- each reproduce the oracle's steps /
+    ranks (+-1) and the compression bar on every leaf, and agree with each
+    other."""
+    from paper_1706_09384_b200.hmatrix import block_errors
+
+    pb = Problem(tag, n)
+    adm = pb.table[:, 0] == 1
+    sizes = (pb.table[:, 2] - pb.table[:, 1]) + (pb.table[:, 4] - pb.table[:, 3])
+    assert (sizes[adm] >= 320).sum() >= 100, "too few large leaves at this size"
+    oh = pb.oracle_h()
+    infos = []
+    for env in ({}, {"HMX_TC_STAGES": "2"}, {"HMX_ACA_TC": "0"}):
+        for k in ("HMX_TC_STAGES", "HMX_ACA_TC"):
+            monkeypatch.delenv(k, raising=False)
+        for k, v in env.items():
+            monkeypatch.setenv(k, v)
+        H, _ = pb.device_h()
+        info = H.block_info()
+        assert np.abs(info["steps"][adm] - oh.steps[adm]).max() <= 1, env
+        assert np.abs(info["rank_after"][adm] - oh.rank_after[adm]).max() <= 1, env
+        err2, norm2 = block_errors(H, pb.spec, pb.cloud)
+        assert np.sqrt(err2[adm] / norm2[adm]).max() <= 3 * pb.w.eps, env
+        infos.append(info)
+    for info in infos[1:]:
+        assert np.abs(info["rank_after"][adm] - infos[0]["rank_after"][adm]).max() <= 1
