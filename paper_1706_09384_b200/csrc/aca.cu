@@ -648,15 +648,27 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
   double* resb = reinterpret_cast<double*>(ring);
   bool first = true;
   for (int64_t r0 = (int64_t)warp * kTcRows; r0 < rows; r0 += (int64_t)kTcWarps * kTcRows) {
-    auto stage = [&](int co, int buf) {
+    // per-lane copy slots of a stage (fixed for the row block): element
+    // e = lane + 32 i is (column e / kTcRows, row e % kTcRows) of the octet
+    constexpr int kSlots = (8 * kTcRows) / 32;
+    int soff[kSlots];        // shared-memory offset within a stage
+    int64_t goff[kSlots];    // global offset at column octet 0
+    int colv[kSlots];        // column within the octet (kTcRows: row out of range)
 #pragma unroll
-      for (int i = 0; i < (8 * kTcRows) / 32; ++i) {
-        const int e = lane + 32 * i;
-        const int col = e / kTcRows, row = e - col * kTcRows;
-        const int64_t q = r0 + row;
-        const int l = co * 8 + col;
-        const bool v = q < rows && l < K;
-        tc_cp16(ring + buf * kTcStage + col * kTcCol + row, F + (v ? q + (int64_t)l * rows : 0), v);
+    for (int i = 0; i < kSlots; ++i) {
+      const int e = lane + 32 * i;
+      const int col = e / kTcRows, row = e - col * kTcRows;
+      soff[i] = col * kTcCol + row;
+      goff[i] = r0 + row + (int64_t)col * rows;
+      colv[i] = (r0 + row < rows) ? col : kTcRows;
+    }
+    auto stage = [&](int co, int buf) {
+      const int64_t base = (int64_t)co * 8 * rows;
+      const int lim = K - co * 8;  // columns of this octet inside the panel
+#pragma unroll
+      for (int i = 0; i < kSlots; ++i) {
+        const bool v = colv[i] < lim;
+        tc_cp16(ring + buf * kTcStage + soff[i], F + (v ? base + goff[i] : 0), v);
       }
       asm volatile("cp.async.commit_group;");
     };
