@@ -145,6 +145,19 @@ int hmx_block_errors(hmx_hmatrix* h, const hmx_kernel* k, const double* pts_tree
                      int64_t n_points, double self_shift, double* err2, double* norm2);
 void hmx_hmatrix_free(hmx_hmatrix* h);
 
+/* ---- low-rank layer, one block at a time ------------------------ */
+/* aca_partial (d = 1) / aca_vector (d = 3) on the block generator of (X, Y, NY) with the same device kernel
+ * and pinned decisions as hmx_assemble; recompress != 0 also applies recompress
+ * (SPEC.md:318-326).  U: (d m) x cap, V: (d n) x cap complex row-major (first *rank columns filled);
+ * *status: bit0 converged, bit1 max_rank reached, bit3 fallback needed (returns HMX_EPIVOT). */
+int hmx_aca_block(hmx_ctx* ctx, const hmx_kernel* k, const double* X, int64_t m, const double* Y, int64_t n,
+                  const double* NY, int32_t has_shift, double shift, const hmx_aca_cfg* cfg, int32_t recompress,
+                  int64_t cap, double* U, double* V, int64_t* rank, int64_t* steps, int32_t* status);
+/* recompress(f, eps) of U (dm x K), V (dn x K) complex row-major -> Uout (dm x K),
+ * Vout (dn x K) row-major with leading dimension *rank <= K */
+int hmx_recompress(hmx_ctx* ctx, int64_t dm, int64_t dn, int64_t K, const double* U, const double* V, double eps,
+                   int32_t trunc_rule, int64_t* rank, double* Uout, double* Vout);
+
 /* ---- H-matvec / GMRES ---------------------------------------------------------- */
 /* y = A_H x, x and y in ORIGINAL point order (d N complex each) */
 int hmx_matvec(hmx_hmatrix* h, const double* x, double* y, int32_t mem);

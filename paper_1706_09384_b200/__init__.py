@@ -15,6 +15,7 @@ from .estimate import EstimatorReport, estimate  # noqa: F401
 from .hmatrix import HMatrix, StorageReport, assemble, block_errors, matvec, storage_report  # noqa: F401
 from .kernels import (KernelSpec, Material, Wavenumbers, assemble_dense, elasto_t_block,  # noqa: F401
                       elasto_u_block, eval_elasto_t, eval_elasto_u, eval_scalar, scalar_block)
-from .lowrank import ACAConfig, LowRankFactor  # noqa: F401
+from .lowrank import (ACAConfig, ACAResult, BlockGenerator, LowRankFactor, aca_full, aca_partial,  # noqa: F401
+                      aca_vector, numerical_rank, randomized_svd, recompress)
 from .snapfile import snapshot  # noqa: F401
 from .solve import GmresConfig, solve_gmres  # noqa: F401

@@ -1263,3 +1263,242 @@ int hmx_gmres(hmx_hmatrix* h, const double* b, double* x, double tol, int32_t re
 }
 
 }  // extern "C"
+
+// ---- single-block low-rank entry points (aca_partial /
+// aca_vector on a BlockGenerator, recompress on a LowRankFactor) -------------------
+// The same device kernels as the batched assembly (aca_kernel, recompress_core,
+// form_gemm) run on one block, so the reference's lowrank API gets the device
+// algorithm leaf by leaf.
+namespace {
+
+// G(:, :) = F^H F for a (rows x K) column-major panel, ld = rows; thread per entry
+__global__ void gram_full(const double2* __restrict__ F, int64_t rows, int K, double2* __restrict__ G, int ldg) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= K * K) return;
+  const int i = t % K, j = t / K;
+  double2 s = cmk(0.0, 0.0);
+  for (int64_t q = 0; q < rows; ++q) s = cfma_ca(F[q + (int64_t)i * rows], F[q + (int64_t)j * rows], s);
+  if (i == j) s.y = 0.0;
+  G[i + (int64_t)j * ldg] = s;
+}
+
+// row-major host (rows x cols) <-> column-major device (ld = rows)
+void to_colmajor(const double2* h, int64_t rows, int64_t cols, std::vector<double2>& out) {
+  out.resize((size_t)(rows * cols));
+  for (int64_t i = 0; i < rows; ++i)
+    for (int64_t j = 0; j < cols; ++j) out[(size_t)(i + j * rows)] = h[i * cols + j];
+}
+void from_colmajor(const std::vector<double2>& in, int64_t rows, int64_t cols, int64_t ldh, double2* h) {
+  for (int64_t i = 0; i < rows; ++i)
+    for (int64_t j = 0; j < cols; ++j) h[i * ldh + j] = in[(size_t)(i + j * rows)];
+}
+
+// Recompression of device factors U (dm x K), V (dn x K) with their Gram pair
+// in G (kcap = K); W: 6 K^2 workspace; results into Uo (dm x r), Vo (dn x r).
+int recompress_device(Ctx& c, DevBuf& mem, const double2* dU, const double2* dV, int64_t dm, int64_t dn, int K,
+                      double2* G, double eps, int rule, int* r_out, double2** Uo, double2** Vo) {
+  RecDesc rd;
+  rd.goff = 0;
+  rd.woff = 0;
+  rd.K = K;
+  rd.kcap = K;
+  double2* W;
+  RecDesc* d_rd;
+  int32_t *d_rank, *d_flag;
+  int rc;
+  if ((rc = mem.alloc(&W, 6 * (int64_t)K * K)) || (rc = mem.alloc(&d_rd, 1)) || (rc = mem.alloc(&d_rank, 1)) ||
+      (rc = mem.alloc(&d_flag, 1)))
+    return rc;
+  HMX_CUDA_TRY(cudaMemcpyAsync(d_rd, &rd, sizeof(RecDesc), cudaMemcpyHostToDevice, c.stream));
+  if ((rc = launch_recompress_core(c, d_rd, 1, K, eps, rule, G, W, d_rank, d_flag))) return rc;
+  int32_t hr = 0;
+  HMX_CUDA_TRY(cudaMemcpyAsync(&hr, d_rank, sizeof(int32_t), cudaMemcpyDeviceToHost, c.stream));
+  HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  *r_out = hr;
+  if (hr == 0) return HMX_OK;
+  if ((rc = mem.alloc(Uo, dm * hr)) || (rc = mem.alloc(Vo, dn * hr))) return rc;
+  FormDesc fd[2];
+  int64_t ts[2];
+  int64_t nt = 0;
+  for (int side = 0; side < 2; ++side) {
+    FormDesc& f = fd[side];
+    const int64_t rows = side == 0 ? dm : dn;
+    f.A = side == 0 ? dU : dV;
+    f.W = W + 4 * (int64_t)K * K + (side == 0 ? 0 : (int64_t)K * hr);
+    f.C = side == 0 ? *Uo : *Vo;
+    f.rows = (int32_t)rows;
+    f.K = K;
+    f.r = hr;
+    f.lda = (int32_t)rows;
+    f.ldc = (int32_t)rows;
+    f.pad = 0;
+    ts[side] = nt;
+    nt += hmx_cdiv(rows, 64) * hmx_cdiv(hr, 32);
+  }
+  FormDesc* d_fd;
+  int64_t* d_ts;
+  if ((rc = mem.alloc(&d_fd, 2)) || (rc = mem.alloc(&d_ts, 2))) return rc;
+  HMX_CUDA_TRY(cudaMemcpyAsync(d_fd, fd, sizeof(fd), cudaMemcpyHostToDevice, c.stream));
+  HMX_CUDA_TRY(cudaMemcpyAsync(d_ts, ts, sizeof(ts), cudaMemcpyHostToDevice, c.stream));
+  return launch_form(c, d_fd, 2, nt, d_ts);
+}
+
+}  // namespace
+
+extern "C" {
+
+int hmx_aca_block(hmx_ctx* ctx, const hmx_kernel* k, const double* X, int64_t m, const double* Y, int64_t n,
+                  const double* NY, int32_t has_shift, double shift, const hmx_aca_cfg* cfg, int32_t recompress,
+                  int64_t cap, double* U, double* V, int64_t* rank, int64_t* steps, int32_t* status) {
+  if (!ctx || !k || !X || !Y || !cfg || !U || !V || !rank || !steps || !status || m <= 0 || n <= 0 || cap < 0)
+    return HMX_EINVAL;
+  if (k->kind == HMX_ELASTO_T && !NY) {
+    hmx_set_error("hmx_aca_block: elasto T needs column normals");
+    return HMX_EINVAL;
+  }
+  Ctx& c = ctx->c;
+  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  const int d = k->kind == HMX_HELMHOLTZ ? 1 : 3;
+  const int64_t dmin = d * std::min(m, n);
+  const int64_t maxr = cfg->max_rank > 0 ? std::min<int64_t>(cfg->max_rank, dmin) : dmin;
+  if (maxr > 1020) {
+    hmx_set_error("hmx_aca_block: max rank %lld above the device limit 1020", (long long)maxr);
+    return HMX_EINVAL;
+  }
+  // points of the block: rows then columns (normals only matter for columns)
+  std::vector<double> pts((size_t)(3 * (m + n))), nrm;
+  std::copy(X, X + 3 * m, pts.begin());
+  std::copy(Y, Y + 3 * n, pts.begin() + 3 * m);
+  if (NY) {
+    nrm.assign((size_t)(3 * (m + n)), 0.0);
+    std::copy(NY, NY + 3 * n, nrm.begin() + 3 * m);
+  }
+  DevPoints P3;
+  int rc;
+  if ((rc = P3.upload(c, pts.data(), NY ? nrm.data() : nullptr, m + n))) return rc;
+  const GreenParams P = make_params(k, has_shift, shift);
+  const double s3f = cfg->sigma3_floor > 0 ? cfg->sigma3_floor : 1e-12;
+  int64_t kc = std::min<int64_t>(maxr, 64);
+  kc = std::max<int64_t>(d, (kc / d) * d);
+  for (;;) {
+    DevBuf mem(c);
+    AcaDesc ds;
+    ds.r0 = 0;
+    ds.c0 = m;
+    ds.m = (int32_t)m;
+    ds.n = (int32_t)n;
+    ds.kcap = (int32_t)kc;
+    ds.max_rank = (int32_t)maxr;
+    ds.uoff = 0;
+    ds.voff = 0;
+    ds.goff = 0;
+    double2 *dU, *dV, *G;
+    AcaDesc* d_desc;
+    AcaOut* d_out;
+    int32_t* d_order;
+    if ((rc = mem.alloc(&dU, d * m * kc)) || (rc = mem.alloc(&dV, d * n * kc)) || (rc = mem.alloc(&G, 2 * kc * kc)) ||
+        (rc = mem.alloc(&d_desc, 1)) || (rc = mem.alloc(&d_out, 1)) || (rc = mem.alloc(&d_order, 1)))
+      return rc;
+    const int32_t zero = 0;
+    HMX_CUDA_TRY(cudaMemcpyAsync(d_desc, &ds, sizeof(AcaDesc), cudaMemcpyHostToDevice, c.stream));
+    HMX_CUDA_TRY(cudaMemcpyAsync(d_order, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, c.stream));
+    const int variant = m + n < kAcaNarrowMax ? kAcaNarrow : kAcaWide;
+    if ((rc = launch_aca(c, d, P, P3.soa, d_desc, d_order, 1, (int)kc, (int)m, cfg->eps, s3f, dU, dV, G, d_out,
+                         variant)))
+      return rc;
+    AcaOut o;
+    HMX_CUDA_TRY(cudaMemcpyAsync(&o, d_out, sizeof(AcaOut), cudaMemcpyDeviceToHost, c.stream));
+    HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    if (o.status & 4) {  // column capacity: rerun with twice the columns (same result)
+      if (kc >= maxr) {
+        hmx_set_error("hmx_aca_block: capacity overflow at the maximal rank");
+        return HMX_ENOMEM;
+      }
+      kc = std::min<int64_t>(maxr, 2 * kc);
+      kc = std::max<int64_t>(d, (kc / d) * d);
+      continue;
+    }
+    *steps = o.steps;
+    *status = o.status;
+    if (o.status & 8) {
+      *rank = 0;
+      hmx_set_error("hmx_aca_block: all sigma_3 pivots below the floor (FallbackNeeded)");
+      return HMX_EPIVOT;
+    }
+    int K = o.rank;
+    const double2* srcU = dU;
+    const double2* srcV = dV;
+    int64_t ldU = d * m, ldV = d * n;
+    if (recompress && K > 0) {
+      // the Gram pair of the ACA factors has ld kcap; recompress_core wants kcap = K
+      double2* G2;
+      if ((rc = mem.alloc(&G2, 2 * (int64_t)K * K))) return rc;
+      HMX_CUDA_TRY(cudaMemcpy2DAsync(G2, sizeof(double2) * K, G, sizeof(double2) * kc, sizeof(double2) * K, K,
+                                     cudaMemcpyDeviceToDevice, c.stream));
+      HMX_CUDA_TRY(cudaMemcpy2DAsync(G2 + (int64_t)K * K, sizeof(double2) * K, G + kc * kc, sizeof(double2) * kc,
+                                     sizeof(double2) * K, K, cudaMemcpyDeviceToDevice, c.stream));
+      int r = 0;
+      double2 *Uo = nullptr, *Vo = nullptr;
+      if ((rc = recompress_device(c, mem, dU, dV, d * m, d * n, K, G2, cfg->eps, cfg->trunc_rule, &r, &Uo, &Vo)))
+        return rc;
+      K = r;
+      srcU = Uo;
+      srcV = Vo;
+    }
+    if (K > cap) {
+      hmx_set_error("hmx_aca_block: rank %d exceeds the output capacity %lld", K, (long long)cap);
+      return HMX_EINVAL;
+    }
+    *rank = K;
+    if (K > 0) {
+      std::vector<double2> hu((size_t)(ldU * K)), hv((size_t)(ldV * K));
+      HMX_CUDA_TRY(cudaMemcpyAsync(hu.data(), srcU, sizeof(double2) * hu.size(), cudaMemcpyDeviceToHost, c.stream));
+      HMX_CUDA_TRY(cudaMemcpyAsync(hv.data(), srcV, sizeof(double2) * hv.size(), cudaMemcpyDeviceToHost, c.stream));
+      HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+      from_colmajor(hu, ldU, K, cap, reinterpret_cast<double2*>(U));
+      from_colmajor(hv, ldV, K, cap, reinterpret_cast<double2*>(V));
+    }
+    return HMX_OK;
+  }
+}
+
+int hmx_recompress(hmx_ctx* ctx, int64_t dm, int64_t dn, int64_t K, const double* U, const double* V, double eps,
+                   int32_t trunc_rule, int64_t* rank, double* Uout, double* Vout) {
+  if (!ctx || !U || !V || !rank || !Uout || !Vout || dm <= 0 || dn <= 0 || K < 0) return HMX_EINVAL;
+  if (K > 1020) {
+    hmx_set_error("hmx_recompress: rank %lld above the device limit 1020", (long long)K);
+    return HMX_EINVAL;
+  }
+  *rank = 0;
+  if (K == 0) return HMX_OK;
+  Ctx& c = ctx->c;
+  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  DevBuf mem(c);
+  std::vector<double2> hu, hv;
+  to_colmajor(reinterpret_cast<const double2*>(U), dm, K, hu);
+  to_colmajor(reinterpret_cast<const double2*>(V), dn, K, hv);
+  double2 *dU, *dV, *G;
+  int rc;
+  if ((rc = mem.alloc(&dU, dm * K)) || (rc = mem.alloc(&dV, dn * K)) || (rc = mem.alloc(&G, 2 * K * K))) return rc;
+  HMX_CUDA_TRY(cudaMemcpyAsync(dU, hu.data(), sizeof(double2) * hu.size(), cudaMemcpyHostToDevice, c.stream));
+  HMX_CUDA_TRY(cudaMemcpyAsync(dV, hv.data(), sizeof(double2) * hv.size(), cudaMemcpyHostToDevice, c.stream));
+  const int nthr = 128, nblk = (int)hmx_cdiv(K * K, nthr);
+  gram_full<<<nblk, nthr, 0, c.stream>>>(dU, dm, (int)K, G, (int)K);
+  gram_full<<<nblk, nthr, 0, c.stream>>>(dV, dn, (int)K, G + K * K, (int)K);
+  HMX_CUDA_TRY(cudaGetLastError());
+  int r = 0;
+  double2 *Uo = nullptr, *Vo = nullptr;
+  if ((rc = recompress_device(c, mem, dU, dV, dm, dn, (int)K, G, eps, trunc_rule, &r, &Uo, &Vo))) return rc;
+  *rank = r;
+  if (r > 0) {
+    std::vector<double2> ou((size_t)(dm * r)), ov((size_t)(dn * r));
+    HMX_CUDA_TRY(cudaMemcpyAsync(ou.data(), Uo, sizeof(double2) * ou.size(), cudaMemcpyDeviceToHost, c.stream));
+    HMX_CUDA_TRY(cudaMemcpyAsync(ov.data(), Vo, sizeof(double2) * ov.size(), cudaMemcpyDeviceToHost, c.stream));
+    HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    from_colmajor(ou, dm, r, r, reinterpret_cast<double2*>(Uout));
+    from_colmajor(ov, dn, r, r, reinterpret_cast<double2*>(Vout));
+  }
+  return HMX_OK;
+}
+
+}  // extern "C"
