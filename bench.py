@@ -359,6 +359,8 @@ def hmx_arm(args):
     # ---- assembly roofline (FP64)
     dfma = C.c_double()
     _lib.check(L.hmx_bench_dfma(_lib.context(local), C.byref(dfma)), "dfma")
+    read_bw = C.c_double()  # read-only streaming rate: the matvec kernels read ~all their bytes
+    _lib.check(L.hmx_bench_read_bw(_lib.context(local), C.byref(read_bw)), "read_bw")
     from paper_1706_09384_b200.flops import PAIR_FLOPS
 
     pair_flops = PAIR_FLOPS[w.kind] * st["pairs_evaluated"]
@@ -383,6 +385,8 @@ def hmx_arm(args):
                      else "fallback 6.65 TB/s (B200_PROFILING.md)",
                      "bytes_per_launch": dom_bytes, "ms_per_launch": dom_ms,
                      "whole_matvec_frac": (mv_bytes / (ms_max / K * 1e-3) / 1e9) / hbm_peak,
+                     "read_only_ceiling_gbs": read_bw.value,
+                     "frac_of_read_only_ceiling": dom_gbs / read_bw.value,
                      "vs_8TBps": (mv_bytes / (ms_max / K * 1e-3) / 1e9) / 8000.0},
         "matvec_phases": ({"gather_ms": ph[0] / nc, "fused_vhx_row_gemv_ms": p1_ms, "fused_GBps": dom_gbs,
                            "finalize_ms": ph[3] / nc, "bytes": mv_bytes} if fused else

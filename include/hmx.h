@@ -170,6 +170,8 @@ int hmx_profile_begin(hmx_hmatrix* h);
 int hmx_profile_end(hmx_hmatrix* h, int64_t* n_calls, double* phase_ms_sum);
 /* FP64 DFMA throughput of the device (TFLOP/s), measured by a dependent-chain microkernel */
 int hmx_bench_dfma(hmx_ctx* ctx, double* tflops);
+/* read-only HBM streaming rate (GB/s), 4 GiB buffer, 16-byte streaming loads: the ceiling of read-dominated kernels */
+int hmx_bench_read_bw(hmx_ctx* ctx, double* gbs);
 int hmx_gmres(hmx_hmatrix* h, const double* b, double* x, double tol, int32_t restart, int64_t max_iters,
               int32_t mem, int64_t* iters, double* history, int64_t history_cap, int64_t* history_len,
               int32_t* converged);

@@ -76,6 +76,7 @@ SIGNATURES = {
     "hmx_profile_begin": (C.c_int, [P]),
     "hmx_profile_end": (C.c_int, [P, C.POINTER(i64), P]),
     "hmx_bench_dfma": (C.c_int, [P, C.POINTER(f64)]),
+    "hmx_bench_read_bw": (C.c_int, [P, C.POINTER(f64)]),
     "hmx_gmres": (C.c_int, [P, P, P, f64, i32, i64, i32, C.POINTER(i64), P, i64,
                             C.POINTER(i64), C.POINTER(i32)]),
 }

@@ -1222,6 +1222,12 @@ int hmx_profile_end(hmx_hmatrix* h, int64_t* n_calls, double* phase_ms_sum) {
   return HMX_OK;
 }
 
+int hmx_bench_read_bw(hmx_ctx* ctx, double* gbs) {
+  if (!ctx || !gbs) return HMX_EINVAL;
+  HMX_CUDA_TRY(cudaSetDevice(ctx->c.device));
+  return hmx::bench_read_bw(ctx->c, gbs);
+}
+
 int hmx_bench_dfma(hmx_ctx* ctx, double* tflops) {
   if (!ctx || !tflops) return HMX_EINVAL;
   HMX_CUDA_TRY(cudaSetDevice(ctx->c.device));

@@ -101,6 +101,49 @@ int bench_dfma(Ctx& c, double* tflops) {
   return HMX_OK;
 }
 
+// read-only HBM streaming rate (roofline ceiling of the read-dominated matvec
+// kernels): sum of a 4 GiB buffer with 16-byte streaming loads, 8 CTAs per SM
+__global__ void read_stream(const double2* __restrict__ a, size_t n, double* out) {
+  double s = 0;
+  size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  const size_t st = (size_t)gridDim.x * blockDim.x;
+  for (; i + 3 * st < n; i += 4 * st) {
+    const double2 x0 = __ldcs(a + i), x1 = __ldcs(a + i + st), x2 = __ldcs(a + i + 2 * st), x3 = __ldcs(a + i + 3 * st);
+    s += ((x0.x + x1.x) + (x2.x + x3.x)) + ((x0.y + x1.y) + (x2.y + x3.y));
+  }
+  for (; i < n; i += st) {
+    const double2 x = __ldcs(a + i);
+    s += x.x + x.y;
+  }
+  if (s == 1.2345) out[0] = s;
+}
+
+int bench_read_bw(Ctx& c, double* gbs) {
+  const size_t n = ((size_t)4 << 30) / sizeof(double2);
+  double2* a = nullptr;
+  double* out = nullptr;
+  HMX_CUDA_TRY(cudaMalloc(&a, n * sizeof(double2)));
+  HMX_CUDA_TRY(cudaMalloc(&out, sizeof(double)));
+  HMX_CUDA_TRY(cudaMemsetAsync(a, 0, n * sizeof(double2), c.stream));
+  const int blocks = c.num_sms * 8;
+  read_stream<<<blocks, 256, 0, c.stream>>>(a, n, out);  // warm-up
+  cudaEvent_t e0, e1;
+  HMX_CUDA_TRY(cudaEventCreate(&e0));
+  HMX_CUDA_TRY(cudaEventCreate(&e1));
+  HMX_CUDA_TRY(cudaEventRecord(e0, c.stream));
+  for (int r = 0; r < 5; ++r) read_stream<<<blocks, 256, 0, c.stream>>>(a, n, out);
+  HMX_CUDA_TRY(cudaEventRecord(e1, c.stream));
+  HMX_CUDA_TRY(cudaEventSynchronize(e1));
+  float ms = 0;
+  HMX_CUDA_TRY(cudaEventElapsedTime(&ms, e0, e1));
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(a);
+  cudaFree(out);
+  *gbs = 5.0 * n * sizeof(double2) / (ms * 1e-3) / 1e9;
+  return HMX_OK;
+}
+
 int launch_dense_fill(Ctx& c, const GreenParams& P, const PointsSoA& pts, const int64_t* d_desc, int64_t ndense,
                       double2* row_stream, int32_t* d_err) {
   if (ndense == 0) return HMX_OK;

@@ -197,6 +197,7 @@ int64_t err_tiles_of(int64_t m, int64_t n);
 
 // dense.cu: FP64 peak microbenchmark
 int bench_dfma(Ctx& c, double* tflops);
+int bench_read_bw(Ctx& c, double* gbs);
 
 // gmres.cu
 int gmres_device(DeviceH& H, const double2* b_dev, double2* x_dev, double tol, int restart, int64_t max_iters,
