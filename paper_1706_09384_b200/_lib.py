@@ -131,6 +131,13 @@ def f64c(a, shape=None):
 _ctx = {}
 
 
+def release_cached(device=0):
+    """Hand the context's cached device blocks back to the driver (before a
+    library such as cuSOLVER has to allocate on the same device)."""
+    if device in _ctx:
+        check(lib().hmx_ctx_release_cache(_ctx[device]), "hmx_ctx_release_cache")
+
+
 def context(device=0):
     """Process-wide hmx context per device."""
     if device not in _ctx:

@@ -607,10 +607,44 @@ constexpr int kTcRows = HMX_TC_ROWS, kTcOct = kTcRows / 8, kTcKs = kTcRows / 4;
 #define HMX_TC_WARPS 8
 #endif
 constexpr int kTcWarps = HMX_TC_WARPS, kTcThreads = 32 * kTcWarps;
+#ifndef HMX_TC_PF
+#define HMX_TC_PF 1
+#endif
+constexpr int kTcPf = HMX_TC_PF;  // Gram-scratch prefetch distance (octets)
 // per-warp cp.async ring: 2 stages of one column octet x kTcRows rows, columns
 // padded to kTcCol rows (the Gram fragments read 8 columns x 4 rows: the pad
 // spreads the 8 columns over all banks)
 constexpr int kTcCol = kTcRows + 4, kTcStage = 8 * kTcCol;  // double2 units; ring = STAGES x kTcStage
+
+// HMX_TC_PROF (experiment builds only): clock64 phase cycles of the
+// tensor-core ACA (thread 0 per CTA for the step phases 0-6; lane 0 of every
+// warp for 8 = streaming loop, 9 = epilogue), read by hmx_debug_tc_prof.
+#ifdef HMX_TC_PROF
+__device__ unsigned long long g_tc_prof[16];
+#define TC_MARK(i)                                                                   \
+  do {                                                                               \
+    if (threadIdx.x == 0) {                                                          \
+      const long long t_ = clock64();                                                \
+      atomicAdd(&g_tc_prof[(i)], (unsigned long long)(t_ - tc_t0));                  \
+      tc_t0 = t_;                                                                    \
+    }                                                                                \
+  } while (0)
+#define TC_WMARK(i)                                                                  \
+  do {                                                                               \
+    if ((threadIdx.x & 31) == 0) {                                                   \
+      const long long t_ = clock64();                                                \
+      atomicAdd(&g_tc_prof[(i)], (unsigned long long)(t_ - tw_t0));                  \
+      tw_t0 = t_;                                                                    \
+    }                                                                                \
+  } while (0)
+#else
+#define TC_MARK(i) \
+  do {             \
+  } while (0)
+#define TC_WMARK(i) \
+  do {              \
+  } while (0)
+#endif
 
 HMX_D void dmma(double& c0, double& c1, double a, double b) {
   asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
@@ -631,44 +665,72 @@ HMX_D void tc_cp16(double2* smem, const double2* gmem, bool valid) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0));
 }
+HMX_D void tc_cp16s(unsigned sa, const double2* gmem) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+}
+HMX_D void tc_cp16sz(unsigned sa, const double2* gmem, bool valid) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0));
+}
 
 // Fused pass over panel F (rows = 3 npts, ld = rows, K columns) for the row
 // blocks of this warp.  Each column octet of a row block is brought into the
-// warp's shared-memory ring with cp.async one octet ahead (no registers held by
-// loads in flight), then feeds both contractions from shared memory.  Residual
-// fragments of each row block are left in resb (aliases the ring: kTcRows x 12
-// doubles, C1 n = 0..5 then C2 n = 0..5) and `epi(rb_row0)` is called by the
-// whole warp; with pend, the Gram partials of the pending columns [Pc, Pc + 3)
-// go to scr (this warp's slice: noct x 32 lanes x 4).
+// warp's shared-memory ring with cp.async kTcStages - 1 octets ahead (no
+// registers held by loads in flight), then feeds both contractions from shared
+// memory.  Residual fragments of each row block are left in resb (aliases the
+// ring: kTcRows x 12 doubles, C1 n = 0..5 then C2 n = 0..5) and `epi(rb_row0)`
+// is called by the whole warp; with pend, the Gram partials of the pending
+// columns [Pc, Pc + 3) go to scr (this warp's slice: noct x 32 lanes x 4).
+// Copy slots: lane element e = lane + 32 i is (column e / kTcRows, row
+// e % kTcRows) of an octet; its shared address and its global offset from the
+// octet's first element are fixed for the pass, only the octet base moves.
+// The Gram B operand (the pending columns of the row block) is read into
+// registers once per row block.
 template <int kTcStages, class Epi>
 HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const double2* piv, int lds, bool pend,
                    int Pc, double* __restrict__ scr, int noct, double2* ring, double2* nfs, Epi&& epi) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int fr = lane >> 2, fk = lane & 3;
   double* resb = reinterpret_cast<double*>(ring);
+  constexpr int kSlots = (8 * kTcRows) / 32;
+  constexpr unsigned kStageBytes = sizeof(double2) * kTcStage;
+  const unsigned ring_sa = (unsigned)__cvta_generic_to_shared(ring);
+  unsigned sa[kSlots];  // shared address in stage 0
+  int goff[kSlots];     // element offset from the octet's (row r0, column 0)
+  int srow[kSlots];     // row within the block
+  int scol[kSlots];     // column within the octet
+#pragma unroll
+  for (int i = 0; i < kSlots; ++i) {
+    const int e = lane + 32 * i;
+    const int col = e / kTcRows, row = e - col * kTcRows;
+    sa[i] = ring_sa + (unsigned)(sizeof(double2) * (col * kTcCol + row));
+    goff[i] = row + col * (int)rows;
+    srow[i] = row;
+    scol[i] = col;
+  }
+  // B fragment of the residual for column l (pivot row staged with zeros past K)
+  const bool bre = fr < 3, bon = fr < 6;
+  const int bcol = bre ? fr : (bon ? fr - 3 : 0);  // lanes fr >= 6 read row 0 and use 0
+  const double2* pbase = piv + bcol * lds;
   bool first = true;
+#ifdef HMX_TC_PROF
+  long long tw_t0 = clock64();
+#endif
   for (int64_t r0 = (int64_t)warp * kTcRows; r0 < rows; r0 += (int64_t)kTcWarps * kTcRows) {
-    // per-lane copy slots of a stage (fixed for the row block): element
-    // e = lane + 32 i is (column e / kTcRows, row e % kTcRows) of the octet
-    constexpr int kSlots = (8 * kTcRows) / 32;
-    int soff[kSlots];        // shared-memory offset within a stage
-    int64_t goff[kSlots];    // global offset at column octet 0
-    int colv[kSlots];        // column within the octet (kTcRows: row out of range)
-#pragma unroll
-    for (int i = 0; i < kSlots; ++i) {
-      const int e = lane + 32 * i;
-      const int col = e / kTcRows, row = e - col * kTcRows;
-      soff[i] = col * kTcCol + row;
-      goff[i] = r0 + row + (int64_t)col * rows;
-      colv[i] = (r0 + row < rows) ? col : kTcRows;
-    }
+    const int rlim = rows - r0 < (int64_t)kTcRows ? (int)(rows - r0) : kTcRows;  // valid rows of this block
+    const double2* Fr = F + r0;
     auto stage = [&](int co, int buf) {
-      const int64_t base = (int64_t)co * 8 * rows;
-      const int lim = K - co * 8;  // columns of this octet inside the panel
+      const double2* Fo = Fr + (int64_t)co * 8 * rows;
+      const unsigned so = (unsigned)buf * kStageBytes;
+      const int clim = K - co * 8;  // columns of this octet inside the panel
+      if (rlim == kTcRows && clim >= 8) {
 #pragma unroll
-      for (int i = 0; i < kSlots; ++i) {
-        const bool v = colv[i] < lim;
-        tc_cp16(ring + buf * kTcStage + soff[i], F + (v ? base + goff[i] : 0), v);
+        for (int i = 0; i < kSlots; ++i) tc_cp16s(sa[i] + so, Fo + goff[i]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < kSlots; ++i) {
+          const bool v = srow[i] < rlim && scol[i] < clim;
+          tc_cp16sz(sa[i] + so, v ? Fo + goff[i] : F, v);
+        }
       }
       asm volatile("cp.async.commit_group;");
     };
@@ -676,9 +738,8 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
     if (pend) {
       for (int e = lane; e < 3 * kTcRows; e += 32) {
         const int c = e / kTcRows, row = e - c * kTcRows;
-        const int64_t q = r0 + row;
-        const bool v = q < rows;
-        tc_cp16(nfs + c * kTcRows + row, F + (v ? q + (int64_t)(Pc + c) * rows : 0), v);
+        const bool v = row < rlim;
+        tc_cp16(nfs + c * kTcRows + row, v ? Fr + row + (int64_t)(Pc + c) * rows : F, v);
       }
     }
 #pragma unroll
@@ -689,36 +750,53 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
     double c1[kTcOct][2], c2[kTcOct][2];
 #pragma unroll
     for (int o = 0; o < kTcOct; ++o) c1[o][0] = c1[o][1] = c2[o][0] = c2[o][1] = 0.0;
-    double nx[4] = {0.0, 0.0, 0.0, 0.0};  // scratch partials of the next octet (prefetched)
-    if (pend && !first) {
-      const double* d0 = scr + (int64_t)lane * 4;
-      nx[0] = d0[0];
-      nx[1] = d0[1];
-      nx[2] = d0[2];
-      nx[3] = d0[3];
+    double bj[kTcKs];  // Gram B fragments: pending column fr mod 3 (re / im) at row 4 j + fk
+    // this warp's Gram partials of its earlier row blocks (global scratch, L2):
+    // a register queue of kTcPf octets ahead hides the L2 round trip
+    double nx[kTcPf][4];
+#pragma unroll
+    for (int q = 0; q < kTcPf; ++q) {
+      nx[q][0] = nx[q][1] = nx[q][2] = nx[q][3] = 0.0;
+      if (pend && !first && q < noct) {
+        const double* dq = scr + ((int64_t)q * 32 + lane) * 4;
+        nx[q][0] = dq[0];
+        nx[q][1] = dq[1];
+        nx[q][2] = dq[2];
+        nx[q][3] = dq[3];
+      }
     }
     for (int co = 0; co < noct; ++co) {
       if (co + kTcStages - 1 < noct) stage(co + kTcStages - 1, (co + kTcStages - 1) % kTcStages);
       else asm volatile("cp.async.commit_group;");
-      // this warp's Gram partials of the earlier row blocks: loaded one octet ahead
       double* d = scr + ((int64_t)co * 32 + lane) * 4;
-      double g3[2] = {nx[0], nx[1]}, g4[2] = {nx[2], nx[3]};
-      if (pend && !first && co + 1 < noct) {
-        const double* dn = d + 128;
-        nx[0] = dn[0];
-        nx[1] = dn[1];
-        nx[2] = dn[2];
-        nx[3] = dn[3];
+      double g3[2] = {nx[0][0], nx[0][1]}, g4[2] = {nx[0][2], nx[0][3]};
+#pragma unroll
+      for (int q = 0; q + 1 < kTcPf; ++q)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) nx[q][t] = nx[q + 1][t];
+      if (pend && !first && co + kTcPf < noct) {
+        const double* dn = d + 128 * kTcPf;
+        nx[kTcPf - 1][0] = dn[0];
+        nx[kTcPf - 1][1] = dn[1];
+        nx[kTcPf - 1][2] = dn[2];
+        nx[kTcPf - 1][3] = dn[3];
       }
       asm volatile("cp.async.wait_group %0;" ::"n"(kTcStages - 1) : "memory");
       __syncwarp();
+      if (pend && co == 0) {
+#pragma unroll
+        for (int j = 0; j < kTcKs; ++j) {
+          const double2 x = nfs[bcol * kTcRows + 4 * j + fk];
+          bj[j] = bon ? (bre ? x.x : x.y) : 0.0;
+        }
+      }
       const double2* T = ring + (co % kTcStages) * kTcStage;  // T[col * kTcCol + row]
       const int l0 = co * 8;
       // residual: two k-steps of 4 columns
 #pragma unroll
       for (int h = 0; h < 2; ++h) {
-        const int l = l0 + 4 * h + fk;
-        const double b = l < K ? piv_frag(piv, lds, l, fr) : 0.0;
+        const double2 pv = pbase[l0 + 4 * h + fk];
+        const double b = bon ? (bre ? pv.x : pv.y) : 0.0;
 #pragma unroll
         for (int o = 0; o < kTcOct; ++o) {
           const double2 a = T[(4 * h + fk) * kTcCol + 8 * o + fr];
@@ -727,11 +805,11 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
         }
       }
       if (pend) {
-        // A' = F^T: m = column l0 + fr, k = row r0 + 4 j + fk; 6 independent
-        // accumulator chains (a short chain serialises on the MMA latency)
-        double h3[6][2], h4[6][2];
+        // A' = F^T: m = column l0 + fr, k = row r0 + 4 j + fk; 4 independent
+        // accumulator chains per product (a single chain serialises on the MMA latency)
+        double h3[4][2], h4[4][2];
 #pragma unroll
-        for (int cidx = 0; cidx < 6; ++cidx) h3[cidx][0] = h3[cidx][1] = h4[cidx][0] = h4[cidx][1] = 0.0;
+        for (int cidx = 0; cidx < 4; ++cidx) h3[cidx][0] = h3[cidx][1] = h4[cidx][0] = h4[cidx][1] = 0.0;
         h3[0][0] = g3[0];
         h3[0][1] = g3[1];
         h4[0][0] = g4[0];
@@ -739,23 +817,13 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
 #pragma unroll
         for (int j = 0; j < kTcKs; ++j) {
           const double2 a = T[fr * kTcCol + 4 * j + fk];
-          // B'[k][n] = pending column n mod 3 (re for n < 3, im for 3 <= n < 6) at row 4 j + k
-          double bj = 0.0;
-          if (fr < 6) {
-            const double2 x = nfs[(fr < 3 ? fr : fr - 3) * kTcRows + 4 * j + fk];
-            bj = fr < 3 ? x.x : x.y;
-          }
-          dmma(h3[j % 6][0], h3[j % 6][1], a.x, bj);
-          dmma(h4[j % 6][0], h4[j % 6][1], a.y, bj);
+          dmma(h3[j % 4][0], h3[j % 4][1], a.x, bj[j]);
+          dmma(h4[j % 4][0], h4[j % 4][1], a.y, bj[j]);
         }
-        g3[0] = ((h3[0][0] + h3[1][0]) + (h3[2][0] + h3[3][0])) + (h3[4][0] + h3[5][0]);
-        g3[1] = ((h3[0][1] + h3[1][1]) + (h3[2][1] + h3[3][1])) + (h3[4][1] + h3[5][1]);
-        g4[0] = ((h4[0][0] + h4[1][0]) + (h4[2][0] + h4[3][0])) + (h4[4][0] + h4[5][0]);
-        g4[1] = ((h4[0][1] + h4[1][1]) + (h4[2][1] + h4[3][1])) + (h4[4][1] + h4[5][1]);
-        d[0] = g3[0];
-        d[1] = g3[1];
-        d[2] = g4[0];
-        d[3] = g4[1];
+        d[0] = (h3[0][0] + h3[1][0]) + (h3[2][0] + h3[3][0]);
+        d[1] = (h3[0][1] + h3[1][1]) + (h3[2][1] + h3[3][1]);
+        d[2] = (h4[0][0] + h4[1][0]) + (h4[2][0] + h4[3][0]);
+        d[3] = (h4[0][1] + h4[1][1]) + (h4[2][1] + h4[3][1]);
       }
       __syncwarp();  // this buffer is refilled by the next iteration's prefetch
     }
@@ -773,8 +841,10 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
         }
       }
     __syncwarp();
+    TC_WMARK(8);
     epi(r0);
     __syncwarp();
+    TC_WMARK(9);
     first = false;
   }
 }
@@ -853,6 +923,9 @@ __global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
   }
   __syncthreads();
   int status = 0;
+#ifdef HMX_TC_PROF
+  long long tc_t0 = clock64();
+#endif
 
   for (;;) {
     const int ipiv = sh.ipiv;
@@ -879,6 +952,7 @@ __global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
       Urow[t] = l < K ? Ub[(int64_t)(D * ipiv + a) + (int64_t)l * ldu] : cmk(0.0, 0.0);
     }
     __syncthreads();
+    TC_MARK(0);
 
     // ---- row pass over V ----------------------------------------------------------------
     ArgMax best{-1.0, 0x7fffffff};
@@ -918,6 +992,7 @@ __global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
       sh.red_s[warp] = rs1;
     }
     __syncthreads();
+    TC_MARK(1);
     if (pend) tc_gram_finalize(scr, noct_cap, nwork_v, GV, kcap, Pc, K);
     if (tid == 0) {
       ArgMax bb{sh.red_v[0], sh.red_i[0]};
@@ -988,6 +1063,7 @@ __global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
 #pragma unroll
     for (int t = 0; t < 9; ++t) gam[t] = sh.gamma[t];
     __syncthreads();
+    TC_MARK(2);
 
     // ---- column pass over U ---------------------------------------------------------------
     best = ArgMax{-1.0, 0x7fffffff};
@@ -1029,6 +1105,7 @@ __global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
       sh.red_i[warp] = best.i;
     }
     __syncthreads();
+    TC_MARK(3);
     if (pend) tc_gram_finalize(scr, noct_cap, nwork_u, GU, kcap, Pc, K);
     if (tid == 0) {
       ArgMax bb{sh.red_v[0], sh.red_i[0]};
@@ -1065,8 +1142,10 @@ __global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
       sh.ipiv = sh.bbi;
     }
     __syncthreads();
+    TC_MARK(4);
   }
   __syncthreads();
+  TC_MARK(5);
   if (tid == 0) {
     AcaOut o;
     o.steps = sh.steps;
@@ -1156,3 +1235,12 @@ int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const 
 }
 
 }  // namespace hmx
+
+#ifdef HMX_TC_PROF
+extern "C" int hmx_debug_tc_prof(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, hmx::g_tc_prof, sizeof(hmx::g_tc_prof)) != cudaSuccess) return 2;
+  unsigned long long z[16] = {};
+  cudaMemcpyToSymbol(hmx::g_tc_prof, z, sizeof(z));
+  return 0;
+}
+#endif

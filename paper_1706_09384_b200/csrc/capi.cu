@@ -522,8 +522,10 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     int64_t dmin = d * std::min(rows_of(b), cols_of(b));
     maxr[b] = cfg->max_rank > 0 ? std::min<int64_t>(cfg->max_rank, dmin) : dmin;
   }
+  tick("aca: bounds");
   size_t free_b = 0, total_b = 0;
   HMX_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  tick("aca: meminfo");
   // memory cached by this context counts as free; U, V and the Gram matrices get
   // kAcaBudgetFrac of it (the Grams are released before the final streams are allocated)
   double avail = (double)free_b + (double)c.cached_bytes;
@@ -546,18 +548,44 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     // K <= a + 2 d kappa diam with a <= 70, docs in DESIGN.md 3).  Leaves that
     // outgrow it are re-run with twice the capacity (same result, deterministic).
     const double kap = k->kind == 0 ? std::fabs(k->kappa) : std::max(std::fabs(k->ks), std::fabs(k->kp));
+    // Cluster diameters from "atom" boxes: the distinct cluster boundaries of
+    // the admissible leaves cut [0, np) into atoms; one pass over the points
+    // boxes every atom, and a cluster's box is the merge of its atoms' boxes.
+    std::vector<int64_t> cuts;
+    cuts.reserve(4 * adm.size() + 2);
+    for (int64_t b : adm)
+      for (int q = 1; q <= 4; ++q) cuts.push_back(table[5 * b + q]);
+    std::sort(cuts.begin(), cuts.end());
+    cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+    const size_t na = cuts.empty() ? 0 : cuts.size() - 1;
+    std::vector<double> abox(6 * na);
+    for (size_t a = 0; a < na; ++a) {
+      double lo0 = INFINITY, lo1 = INFINITY, lo2 = INFINITY, hi0 = -INFINITY, hi1 = -INFINITY, hi2 = -INFINITY;
+      for (int64_t t = cuts[a]; t < cuts[a + 1]; ++t) {
+        const double* q = pts_tree + 3 * t;
+        lo0 = std::min(lo0, q[0]);
+        hi0 = std::max(hi0, q[0]);
+        lo1 = std::min(lo1, q[1]);
+        hi1 = std::max(hi1, q[1]);
+        lo2 = std::min(lo2, q[2]);
+        hi2 = std::max(hi2, q[2]);
+      }
+      double* bx = &abox[6 * a];
+      bx[0] = lo0, bx[1] = lo1, bx[2] = lo2, bx[3] = hi0, bx[4] = hi1, bx[5] = hi2;
+    }
+    auto atom = [&](int64_t v) { return (size_t)(std::lower_bound(cuts.begin(), cuts.end(), v) - cuts.begin()); };
     auto diam = [&](int64_t a0, int64_t a1) {
       double lo3[3] = {INFINITY, INFINITY, INFINITY}, hi3[3] = {-INFINITY, -INFINITY, -INFINITY};
-      for (int64_t t = a0; t < a1; ++t)
+      for (size_t a = atom(a0), e = atom(a1); a < e; ++a)
         for (int q = 0; q < 3; ++q) {
-          lo3[q] = std::min(lo3[q], pts_tree[3 * t + q]);
-          hi3[q] = std::max(hi3[q], pts_tree[3 * t + q]);
+          lo3[q] = std::min(lo3[q], abox[6 * a + q]);
+          hi3[q] = std::max(hi3[q], abox[6 * a + 3 + q]);
         }
       return std::sqrt((hi3[0] - lo3[0]) * (hi3[0] - lo3[0]) + (hi3[1] - lo3[1]) * (hi3[1] - lo3[1]) +
                        (hi3[2] - lo3[2]) * (hi3[2] - lo3[2]));
     };
     const double floor_cols = d == 1 ? 36.0 : 60.0;
-    // clusters are shared by many leaves: one box per distinct (start, stop)
+    // clusters are shared by many leaves: one diameter per distinct (start, stop)
     std::map<std::pair<int64_t, int64_t>, double> dcache;
     auto diam_c = [&](int64_t a0, int64_t a1) {
       auto it = dcache.find({a0, a1});
@@ -591,6 +619,8 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       for (int64_t b : adm) kcap[b] = std::max<int64_t>(d, round_d((int64_t)(kcap[b] * f)));
     }
   }
+  tick("aca: capacity model");
+  PlanPre pre;
   std::deque<AcaPass> passes;  // stable addresses (Pending keeps pointers)
   std::vector<int64_t> todo = adm;
   const double s3f = cfg->sigma3_floor > 0 ? cfg->sigma3_floor : 1e-12;
@@ -794,14 +824,26 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       mark("aca narrow done");
       HMX_CUDA_TRY(cudaMemcpyAsync(ps.out.data() + nwide, d_out + nwide, sizeof(AcaOut) * (todo.size() - nwide),
                                    cudaMemcpyDeviceToHost, c.stream));
-      HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));  // small leaves only; the large ones keep running
-      if ((rc = consume(ps, nwide, todo.size()))) return fail(rc);
     }
-    if (nwide) {
+    // the rank-independent half of the matvec plan, while the ACA runs
+    if (pre.segs.empty()) build_plan_pre(H, pre);
+    // HMX_WIDE_FIRST=1: consume the wide leaves (aux, finished first) before
+    // the narrow ones so their large-K recompression is queued behind the
+    // narrow ACA instead of after it (measured 2-5% slower: off by default)
+    const char* e_wf = std::getenv("HMX_WIDE_FIRST");
+    const bool wide_first = e_wf && e_wf[0] == '1';
+    auto consume_wide = [&]() -> int {
+      if (!nwide) return HMX_OK;
       HMX_CUDA_TRY(cudaStreamSynchronize(c.aux));
       OnAux on(c);
-      if ((rc = consume(ps, 0, nwide))) return fail(rc);
+      return consume(ps, 0, nwide);
+    };
+    if (wide_first && (rc = consume_wide())) return fail(rc);
+    if (todo.size() > nwide) {
+      HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+      if ((rc = consume(ps, nwide, todo.size()))) return fail(rc);
     }
+    if (!wide_first && (rc = consume_wide())) return fail(rc);
     H.aca_passes++;
     if (nfb) {
       H.n_fallback += nfb;
@@ -857,7 +899,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
 
   // ---- 3. layout + matvec plan ----------------------------------------------------------------
   if (verbose) setenv("HMX_VERBOSE_PLAN", "1", 1);
-  if ((rc = build_matvec_plan(H, {}))) return fail(rc);
+  if ((rc = build_matvec_plan(H, &pre))) return fail(rc);
 
   // ---- 4a. dense leaves ---------------------------------------------------------------------
   HMX_CUDA_TRY(cudaEventRecord(ev[3], c.stream));
@@ -991,7 +1033,7 @@ int hmx_hmatrix_load(hmx_ctx* ctx, int32_t d, int64_t np, const int64_t* perm, c
     std::vector<int64_t> p(perm, perm + np);
     if ((rc = dev_upload(c, &H.d_perm, p))) return fail(rc);
   }
-  if ((rc = build_matvec_plan(H, {}))) return fail(rc);
+  if ((rc = build_matvec_plan(H))) return fail(rc);
   std::vector<double2> row(H.row_elems), vs(std::max<int64_t>(H.v_elems, 0));
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t m = table[5 * b + 2] - table[5 * b + 1], n = table[5 * b + 4] - table[5 * b + 3];

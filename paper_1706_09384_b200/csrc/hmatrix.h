@@ -123,7 +123,16 @@ void warm_gmres();
 void warm_estimate();
 
 // matvec.cu
-int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& seg_level);
+// Rank-independent part of the matvec plan (row segments, nesting levels);
+// hmx_assemble builds it on the host while the ACA kernels run.
+struct PlanPre {
+  std::vector<std::pair<int64_t, int64_t>> segs;  // (r0, r1) per row segment, nesting order
+  std::vector<int64_t> bseg;                      // leaf -> segment
+  std::vector<int64_t> level;                     // segment -> nesting level
+  int64_t nlevels = 0;
+};
+void build_plan_pre(const DeviceH& H, PlanPre& pre);
+int build_matvec_plan(DeviceH& H, const PlanPre* pre = nullptr);
 int matvec_device(DeviceH& H, const double2* x_orig_dev, double2* y_orig_dev, float* phase_ms);
 
 // dense.cu

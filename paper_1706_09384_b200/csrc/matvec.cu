@@ -184,9 +184,42 @@ void warm_matvec() {
   cudaFuncGetAttributes(&a, mv_finalize);
 }
 
+void build_plan_pre(const DeviceH& H, PlanPre& pre) {
+  const int64_t nb = H.nb;
+  // row segments keyed by (r0, r1): leaves sorted by (r0 asc, r1 desc) = nesting order
+  std::vector<int64_t> byrow(nb);
+  std::iota(byrow.begin(), byrow.end(), int64_t(0));
+  std::sort(byrow.begin(), byrow.end(), [&](int64_t a, int64_t b) {
+    const int64_t a0 = H.table[5 * a + 1], b0 = H.table[5 * b + 1];
+    if (a0 != b0) return a0 < b0;
+    const int64_t a1 = H.table[5 * a + 2], b1 = H.table[5 * b + 2];
+    return a1 != b1 ? a1 > b1 : a < b;
+  });
+  auto& segs = pre.segs;
+  segs.clear();
+  pre.bseg.assign(nb, 0);
+  for (int64_t q = 0; q < nb; ++q) {
+    const int64_t b = byrow[q];
+    const std::pair<int64_t, int64_t> key(H.table[5 * b + 1], H.table[5 * b + 2]);
+    if (segs.empty() || segs.back() != key) segs.push_back(key);
+    pre.bseg[b] = (int64_t)segs.size() - 1;
+  }
+  const int64_t ns = (int64_t)segs.size();
+  pre.level.assign(ns, 0);
+  std::vector<int64_t> stack;
+  int64_t maxlev = 0;
+  for (int64_t g = 0; g < ns; ++g) {
+    while (!stack.empty() && segs[stack.back()].second <= segs[g].first) stack.pop_back();
+    pre.level[g] = (int64_t)stack.size();
+    maxlev = std::max(maxlev, pre.level[g]);
+    stack.push_back(g);
+  }
+  pre.nlevels = maxlev + 1;
+}
+
 // Builds segments, levels, stream offsets and the phase-1/phase-2 work lists.
 // Requires H.table, H.rank_after (low-rank leaves), H.d, H.np.
-int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
+int build_matvec_plan(DeviceH& H, const PlanPre* pre_in) {
   const auto t0 = std::chrono::steady_clock::now();
   const bool verbose = std::getenv("HMX_VERBOSE_PLAN") != nullptr;
   auto tick = [&](const char* what) {
@@ -196,36 +229,16 @@ int build_matvec_plan(DeviceH& H, const std::vector<int64_t>& /*unused*/) {
   };
   const int d = H.d;
   const int64_t nb = H.nb;
-  // ---- row segments keyed by (r0, r1): sort leaves by (r0 asc, r1 desc) = nesting order
-  std::vector<int64_t> byrow(nb);
-  std::iota(byrow.begin(), byrow.end(), int64_t(0));
-  std::sort(byrow.begin(), byrow.end(), [&](int64_t a, int64_t b) {
-    const int64_t a0 = H.table[5 * a + 1], b0 = H.table[5 * b + 1];
-    if (a0 != b0) return a0 < b0;
-    const int64_t a1 = H.table[5 * a + 2], b1 = H.table[5 * b + 2];
-    return a1 != b1 ? a1 > b1 : a < b;
-  });
-  std::vector<std::pair<int64_t, int64_t>> segs;
-  std::vector<int64_t> bseg(nb);
-  for (int64_t q = 0; q < nb; ++q) {
-    const int64_t b = byrow[q];
-    const std::pair<int64_t, int64_t> key(H.table[5 * b + 1], H.table[5 * b + 2]);
-    if (segs.empty() || segs.back() != key) segs.push_back(key);
-    bseg[b] = (int64_t)segs.size() - 1;
-  }
+  PlanPre own;
+  const bool have = pre_in && !pre_in->segs.empty();  // e.g. no admissible leaf: no ACA pass built it
+  if (!have) build_plan_pre(H, own);
+  const PlanPre& pre = have ? *pre_in : own;
+  const auto& segs = pre.segs;
+  const auto& bseg = pre.bseg;
+  const auto& level = pre.level;
   const int64_t ns = (int64_t)segs.size();
-  std::vector<int64_t> level(ns);
-  {
-    std::vector<int64_t> stack;
-    int64_t maxlev = 0;
-    for (int64_t g = 0; g < ns; ++g) {
-      while (!stack.empty() && segs[stack.back()].second <= segs[g].first) stack.pop_back();
-      level[g] = (int64_t)stack.size();
-      maxlev = std::max(maxlev, level[g]);
-      stack.push_back(g);
-    }
-    H.nlevels = maxlev + 1;
-  }
+  H.nlevels = pre.nlevels;
+  tick("segments");
   std::vector<int64_t> ncols(ns, 0), colstart(nb, 0);
   for (int64_t b = 0; b < nb; ++b) {
     const int64_t g = bseg[b];

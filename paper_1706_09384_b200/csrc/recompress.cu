@@ -21,6 +21,26 @@
 #endif
 namespace hmx {
 
+// HMX_RC_PROF (experiment builds only): per-phase clock64 cycles of thread 0,
+// summed over CTAs, per MODE (16 slots each: 0-8 phases, 14 sum K, 15 CTAs);
+// read back by hmx_debug_rc_prof.
+#ifdef HMX_RC_PROF
+__device__ unsigned long long g_rc_prof[3 * 16];
+#define RC_MARK(i)                                                  \
+  do {                                                              \
+    __syncthreads();                                                \
+    if (threadIdx.x == 0) {                                         \
+      const long long t_ = clock64();                               \
+      atomicAdd(&g_rc_prof[MODE * 16 + (i)], (unsigned long long)(t_ - rc_t0)); \
+      rc_t0 = t_;                                                   \
+    }                                                               \
+  } while (0)
+#else
+#define RC_MARK(i) \
+  do {             \
+  } while (0)
+#endif
+
 namespace {
 
 
@@ -668,6 +688,13 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1
   }
 
   if (tid == 0) s_flag = 0;
+#ifdef HMX_RC_PROF
+  long long rc_t0 = clock64();
+  if (tid == 0) {
+    atomicAdd(&g_rc_prof[MODE * 16 + 14], (unsigned long long)K);
+    atomicAdd(&g_rc_prof[MODE * 16 + 15], 1ull);
+  }
+#endif
   // ---- scaled Cholesky of G_V: A = D^-1 G_V D^-1, R^H R = A (upper R) ----------
   for (int i = tid; i < K; i += NT) {
     const double g = GV[i + (int64_t)i * kcap].x;
@@ -708,6 +735,7 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1
     A[t] = (i <= j) ? cscale(A[t], dscale[j]) : cmk(0.0, 0.0);
   }
   __syncthreads();
+  RC_MARK(0);
   // ---- T = R G_U (B), E = T R^H --------------------------------------------------
   if constexpr (!SMEM) {
     // large K: shared-memory tiled products (the naive loops are L2-latency bound)
@@ -747,6 +775,7 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1
     __syncthreads();
   }
   // ---- eigen-decomposition E = Q Z diag(lam) Z^T Q^H --------------------------------
+  RC_MARK(1);
   if constexpr (SMEM)
     tridiagonalize_packed<NT>(E, K, d, e, tau, vbuf, pbuf, S, red);
   else
@@ -755,6 +784,7 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1
   double2* Hv = E;  // Householder vectors v_k = Hv(k+1:, k)
   // fast path: bisection eigenvalues + twisted eigenvectors (rc: e^2 scratch)
   double pivmin = 0.0;
+  RC_MARK(2);
   bisect_all<NT>(d, e, rc, K, rs, red, pivmin);  // rs = ascending eigenvalues
   for (int i = tid; i < K; i += NT) {
     lam[i] = fmax(rs[K - 1 - i], 0.0);  // descending
@@ -765,6 +795,7 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1
   __syncthreads();
   int r = s_r;
   bool fast_ok = true;
+  RC_MARK(3);
   if (r > 0) {
     double* uscr = reinterpret_cast<double*>(Wuv);  // K doubles per kept vector
     for (int c2 = tid; c2 < r; c2 += NT)
@@ -772,6 +803,7 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1
     __syncthreads();
     fast_ok = cgs2_columns<NT>(B, K, r, reinterpret_cast<double*>(pbuf), red);
   }
+  RC_MARK(4);
   if (!fast_ok) {
     // near-degenerate eigenvalues: implicit QL with accumulated vectors
     if (SMEM) {
@@ -810,6 +842,7 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1
   }
   if (r == 0) return;
   // ---- L_r = Q Z_r : B (K x r) ------------------------------------------------------
+  RC_MARK(5);
   for (int k = K - 2; k >= 0; --k) {
     const double2 tk = tau[k];
     if (tk.x == 0.0 && tk.y == 0.0) continue;
@@ -831,6 +864,7 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1
     __syncthreads();
   }
   // ---- W_U = R^H L_r S^-1/2, W_V = R^{-1} L_r S^1/2 ------------------------------------
+  RC_MARK(6);
   double2* Wu = Wuv;
   double2* Wv = Wuv + (int64_t)K * r;
   if constexpr (!SMEM) {
@@ -845,6 +879,7 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1
     }
   }
   // W_V: R X = L_r by column-oriented back substitution, parallel over (row, column)
+  RC_MARK(7);
   for (int t = tid; t < K * r; t += NT) Wv[t] = B[t];
   __syncthreads();
   for (int i = K - 1; i >= 0; --i) {
@@ -858,6 +893,7 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1
     __syncthreads();
   }
   for (int t = tid; t < K * r; t += NT) Wv[t] = cscale(Wv[t], sqrt(sqrt(lam[ordr[t / K]])));
+  RC_MARK(8);
 }
 
 // C (rows x r, ldc) = A (rows x K, lda) * W (K x r, ld K) on the FP64 tensor
@@ -1053,3 +1089,13 @@ int launch_form(Ctx& c, const FormDesc* d_desc, int64_t nitems, int64_t ntiles_t
 }
 
 }  // namespace hmx
+
+#ifdef HMX_RC_PROF
+// experiment builds: read (and reset) the recompression phase counters
+extern "C" int hmx_debug_rc_prof(unsigned long long* out) {
+  if (cudaMemcpyFromSymbol(out, hmx::g_rc_prof, sizeof(hmx::g_rc_prof)) != cudaSuccess) return 2;
+  unsigned long long z[3 * 16] = {};
+  cudaMemcpyToSymbol(hmx::g_rc_prof, z, sizeof(z));
+  return 0;
+}
+#endif

@@ -189,6 +189,9 @@ def _torch_dev(device=0):
 
     if not torch.cuda.is_available():
         raise RuntimeError("CUDA device required")
+    from . import _lib
+
+    _lib.release_cached(device)  # cuSOLVER workspaces must not compete with the assembly cache
     return torch, torch.device("cuda", device)
 
 
