@@ -640,9 +640,19 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   auto recompress_subset = [&](AcaPass& ps, std::vector<int64_t> live) -> int {
     if (live.empty()) return HMX_OK;
     // largest K first, launched in K classes so small leaves do not pay for big shared memory
-    std::sort(live.begin(), live.end(), [&](int64_t x, int64_t y) {
-      return ps.out[x].rank != ps.out[y].rank ? ps.out[x].rank > ps.out[y].rank : x < y;
-    });
+    {
+      // counting sort on the rank (descending), stable in position order: the
+      // order of sort(rank desc, position asc) without the comparison sort
+      int kmax = 0;
+      for (int64_t x : live) kmax = std::max(kmax, ps.out[x].rank);
+      std::vector<int64_t> cnt((size_t)kmax + 2, 0);
+      for (int64_t x : live) cnt[(size_t)(kmax - ps.out[x].rank) + 1]++;
+      for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
+      std::vector<int64_t> sorted(live.size());
+      std::sort(live.begin(), live.end());
+      for (int64_t x : live) sorted[(size_t)cnt[(size_t)(kmax - ps.out[x].rank)]++] = x;
+      live.swap(sorted);
+    }
     std::vector<RecDesc> rd(live.size());
     int64_t wo = 0;
     for (size_t q = 0; q < live.size(); ++q) {
@@ -671,7 +681,11 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     // when issued on the auxiliary stream, only the large-K class stays there;
     // the shared-memory classes go to the main stream (ordered after this
     // point by an event) so they overlap the long large-K CTAs
-    const bool on_aux = c.stream == c.aux;
+    // HMX_RC_FORK=1: the wide leaves' shared-memory classes go to the main stream
+    // (behind the narrow leaves' classes); default: they stay on aux after the
+    // large-K class, so the two streams' class sequences run side by side
+    const char* e_fk = std::getenv("HMX_RC_FORK");
+    const bool on_aux = c.stream == c.aux && e_fk && e_fk[0] == '1';
     bool forked = false;
     for (int ci = 0; ci < ncls && q0 < rd.size(); ++ci) {
       const int lim_lo = ci + 1 < ncls ? classes[ci + 1] : 0;
@@ -692,6 +706,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
         }
         e = launch_recompress_core(c, d_rd + q0, (int64_t)(q1 - q0), rd[q0].K, cfg->eps, cfg->trunc_rule, ps.G, W,
                                    d_rank + q0, d_flag + q0);
+        mark("  rc class K<=" + std::to_string(rd[q0].K) + " n=" + std::to_string(q1 - q0));
         c.stream = saved;
         if (e) return e;
       }

@@ -16,6 +16,10 @@
 
 #include "hmatrix.h"
 
+#ifndef HMX_RC_NT64_MAX
+#define HMX_RC_NT64_MAX 0
+#endif
+constexpr int kRecompressNt64Max = HMX_RC_NT64_MAX;  // K classes run by 64-thread CTAs
 #ifndef HMX_RC_MINB
 #define HMX_RC_MINB 8
 #endif
@@ -492,7 +496,35 @@ __device__ void bisect_all(const double* d, const double* e, double* e2, int K, 
   // absolute tolerance (abstol = ulp ||T||), so eigenvalues far below ||T||
   // (all truncated away) do not iterate down to their own relative precision
   const double atol = 4.4e-16 * span + pivmin;
-  // multisection: 3 independent Sturm chains per step (ILP) -> 2 bits per step
+  // multisection: 3 independent Sturm chains per thread (ILP); with K <= NT / 2
+  // (NT / 4) a group of T = 2 (4) adjacent lanes shares one eigenvalue and
+  // tests 3 T points per step -> log2(3 T + 1) bits per step instead of 2
+  const int T = 4 * K <= NT ? 4 : (2 * K <= NT ? 2 : 1);
+  if (T > 1) {
+    const int j = tid / T, sub = tid % T, P = 3 * T;
+    const int lane = tid & 31;
+    const unsigned gmask = ((1u << T) - 1u) << (lane & ~(T - 1));
+    if (j < K) {
+      double a = lo, b = hi;
+      for (int it = 0; it < 40; ++it) {
+        if (b - a <= fmax(atol, 4.4e-16 * fmax(fabs(a), fabs(b)))) break;
+        const double h = (b - a) / (double)(P + 1);
+        const int p0 = 3 * sub;
+        const double x1 = a + (double)(p0 + 1) * h, x2 = a + (double)(p0 + 2) * h, x3 = a + (double)(p0 + 3) * h;
+        int c1, c2, c3;
+        sturm_count3(d, e2, K, x1, x2, x3, pivmin, c1, c2, c3);
+        int first = c1 > j ? p0 : (c2 > j ? p0 + 1 : (c3 > j ? p0 + 2 : P));
+        for (int o = 1; o < T; o <<= 1) first = min(first, __shfl_xor_sync(gmask, first, o));
+        const double na = first == 0 ? a : a + (double)first * h;
+        const double nb = first == P ? b : a + (double)(first + 1) * h;
+        a = na;
+        b = nb;
+      }
+      if (sub == 0) lam_asc[j] = 0.5 * (a + b);
+    }
+    __syncthreads();
+    return;
+  }
   for (int j = tid; j < K; j += NT) {
     double a = lo, b = hi;
     for (int it = 0; it < 40; ++it) {
@@ -629,7 +661,7 @@ HMX_D void recompress_truncate(const double* lam, const int* ordr, int K, double
 // T / L_r all in shared memory (small K: the O(K) sequential phases then run
 // at shared-memory instead of L2 latency)
 template <int MODE, int NT>
-__global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : 1) recompress_core(const RecDesc* __restrict__ desc, double eps, int rule,
+__global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : (NT == 64 && MODE == 1 ? 16 : 1)) recompress_core(const RecDesc* __restrict__ desc, double eps, int rule,
                                                             const double2* __restrict__ G, double2* __restrict__ W,
                                                             int32_t* __restrict__ rank_out,
                                                             int32_t* __restrict__ flags_out) {
@@ -1025,6 +1057,7 @@ void warm_recompress() {
   cudaFuncAttributes a;
   cudaFuncGetAttributes(&a, recompress_core<2, 128>);
   cudaFuncGetAttributes(&a, recompress_core<1, 128>);
+  cudaFuncGetAttributes(&a, recompress_core<1, 64>);
   cudaFuncGetAttributes(&a, recompress_core<1, 256>);
   cudaFuncGetAttributes(&a, recompress_core<0, 256>);
   cudaFuncGetAttributes(&a, recompress_core<0, 512>);
@@ -1048,7 +1081,14 @@ int launch_recompress_core(Ctx& c, const RecDesc* d_desc, int64_t nblk, int kmax
     recompress_core<2, 128><<<(unsigned)nblk, 128, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
   } else if (kmax <= kRecompressSmemMax) {
     const size_t smem = vec + sizeof(double2) * ((size_t)kmax * (kmax + 1) / 2);  // packed E
-    if (kmax <= 64) {
+    const char* e_64 = std::getenv("HMX_RC_NT64_MAX");
+    const int nt64_max = e_64 ? std::atoi(e_64) : kRecompressNt64Max;
+    if (kmax <= nt64_max) {
+      // small K: 2-warp CTAs (cheaper barriers, twice the leaves per SM)
+      HMX_CUDA_TRY(
+          cudaFuncSetAttribute(recompress_core<1, 64>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      recompress_core<1, 64><<<(unsigned)nblk, 64, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
+    } else if (kmax <= 64) {
       HMX_CUDA_TRY(
           cudaFuncSetAttribute(recompress_core<1, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
       recompress_core<1, 128><<<(unsigned)nblk, 128, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);

@@ -4,7 +4,7 @@ for c in $cfgs; do
   for i in 1 2; do
     for v in "$@"; do
       lib=${v%%|*}; envs=${v#*|}; [ "$envs" = "$v" ] && envs=""
-      echo -n "$(basename $lib) [$envs] $c: "; env $envs HMX_LIB=$lib python tools/asm_repeat.py $c 2 | tail -1
+      echo -n "$(basename $lib) [$envs] $c: "; env $envs HMX_LIB=$lib python tools/asm_repeat.py $c ${REPS:-2} | tail -1
     done
   done
 done

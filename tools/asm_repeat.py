@@ -13,6 +13,7 @@ w = WORKLOADS[tag]
 cloud = hmx.make_geometry("sphere", w.n_points, 1.0, d=w.d)
 ct = hmx.build_cluster_tree(cloud, w.n_leaf)
 bt = hmx.build_block_tree(ct, ct, w.eta)
+tot = []
 for r in range(reps):
     t0 = time.perf_counter()
     H, rep = hmx.assemble(w.spec(), cloud, ct, bt, hmx.ACAConfig(eps_aca=w.eps))
@@ -21,3 +22,8 @@ for r in range(reps):
           f"{st['t_recompress_ms']:.1f}  form {st['t_form_ms']:.1f}  wall {1e3 * (time.perf_counter() - t0):.1f}",
           flush=True)
     del H
+    if r > 0:
+        tot.append(st["t_total_ms"])
+if tot:
+    import statistics
+    print(f"{tag} summary over reps 1..{reps - 1}: min {min(tot):.1f} ms  median {statistics.median(tot):.1f} ms")
