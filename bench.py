@@ -46,6 +46,9 @@ def parse():
     ap.add_argument("--no-solve", action="store_true", help="skip the T65k time-to-solve run")
     ap.add_argument("--no-estimate", action="store_true", help="skip the delta_{H,F} estimator timing")
     ap.add_argument("--solve-config", default="T65k")
+    ap.add_argument("--shard", action="store_true",
+                    help="block-row sharded H (SURVEY 8(e)): each rank assembles 1/N of the leaves, one "
+                         "all-reduce of y per matvec, strong scaling (default: independent replicas)")
     return ap.parse_args()
 
 
@@ -227,6 +230,7 @@ def time_to_solve(tag, device):
     bt = hmx.build_block_tree(ct, ct, w.eta)
     t_tree = time.perf_counter() - t0
     torch.cuda.synchronize()
+    free_before = torch.cuda.mem_get_info(device)[0]
     t0 = time.perf_counter()
     H, rep = hmx.assemble(w.spec(), cloud, ct, bt, hmx.ACAConfig(eps_aca=w.eps), device=device)
     t_asm = time.perf_counter() - t0
@@ -244,7 +248,8 @@ def time_to_solve(tag, device):
            "time_to_solve_s": st["t_total_ms"] * 1e-3 + t_gm,
            "time_to_solve_with_tree_s": st["t_total_ms"] * 1e-3 + t_gm + t_tree,
            "max_rank_before": rep.max_rank_before, "max_rank_after": rep.max_rank_after,
-           "matvec_bytes": st["matvec_bytes"]}
+           "matvec_bytes": st["matvec_bytes"], "aca_passes": st["aca_passes"],
+           "free_gb_before_assembly": free_before / 1e9}
     del H
     return out
 
@@ -446,7 +451,12 @@ def hmx_arm(args):
     if not args.no_solve:
         # its own job: the U32k H-matrix and the cached workspaces are handed back first
         del H
+        import gc
+
+        gc.collect()
         L.hmx_ctx_release_cache(_lib.context(local))
+        del Xd, Y
+        torch.cuda.empty_cache()
         torch.cuda.synchronize()
         line["time_to_solve"] = time_to_solve(args.solve_config, local)
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
@@ -464,9 +474,101 @@ def hmx_arm(args):
         dist.destroy_process_group()
 
 
+# ----------------------------------------------------------------------------------------------
+def shard_arm(args):
+    """--shard: block-row sharded U32k H-matvec (strong scaling).  Rank p
+    assembles its stripe of the leaves (no collective); a step is the sharded
+    matvec: local stripe matvec + one NCCL all-reduce of y (d N complex128).
+    value = full-H algorithmic bytes x K / device time (max over ranks)."""
+    import torch
+
+    import paper_1706_09384_b200 as hmx
+    from paper_1706_09384_b200 import shard
+    from paper_1706_09384_b200.configs import WORKLOADS
+    from paper_1706_09384_b200.dist import max_over_ranks
+
+    ws, rank, local = dist_setup(args)
+    torch.cuda.set_device(local)
+    if ws > 1:
+        import torch.distributed as tdist
+
+        tdist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    w = WORKLOADS[args.config]
+    cloud = hmx.make_geometry("sphere", w.n_points, 1.0, d=w.d)
+    ct = hmx.build_cluster_tree(cloud, w.n_leaf)
+    bt = hmx.build_block_tree(ct, ct, w.eta)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    sh = shard.assemble_sharded(w.spec(), cloud, ct, bt, hmx.ACAConfig(eps_aca=w.eps), rank, ws, device=local)
+    torch.cuda.synchronize()
+    t_asm = max_over_ranks(time.perf_counter() - t0, f"cuda:{local}")
+    st = sh.local.stats() if sh.local is not None else {"matvec_bytes": 0.0, "phase2_bytes": 0.0}
+    # full-H algorithmic bytes: the stripes' leaf bytes sum to the full H's, x / y counted once
+    n = w.d * w.n_points
+    leaf_b = torch.tensor([float(st["matvec_bytes"]) - 32.0 * n if sh.local is not None else 0.0],
+                          dtype=torch.float64, device=f"cuda:{local}")
+    if ws > 1:
+        tdist.all_reduce(leaf_b)
+    mv_bytes = float(leaf_b.item()) + 32.0 * n
+    K, W = args.steps, args.warmup
+    rng = np.random.default_rng(SEED)
+    X = torch.from_numpy(np.stack([rng.standard_normal(n) + 1j * rng.standard_normal(n) for _ in range(K + W)]))
+    Xd = X.to(f"cuda:{local}")
+    for j in range(W):
+        sh.matvec(Xd[K + j])
+    torch.cuda.synchronize()
+    if ws > 1:
+        tdist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(local) as clk:
+        torch.cuda.synchronize()
+        e0.record()
+        for j in range(K):
+            sh.matvec(Xd[j])
+        e1.record()
+        torch.cuda.synchronize()
+    ms = max_over_ranks(e0.elapsed_time(e1), f"cuda:{local}")
+    # e2e: pinned host x -> device, sharded matvec, y -> pinned host, every step
+    Xh = X.pin_memory()
+    Yh = torch.empty(n, dtype=torch.complex128).pin_memory()
+    if ws > 1:
+        tdist.barrier()
+    f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    f0.record()
+    for j in range(K):
+        y = sh.matvec(Xh[j].to(f"cuda:{local}", non_blocking=True))
+        Yh.copy_(y, non_blocking=True)
+    f1.record()
+    torch.cuda.synchronize()
+    e2e_ms = max_over_ranks(f0.elapsed_time(f1), f"cuda:{local}")
+    line = {
+        "metric": f"{args.config} H-matvec algorithmic HBM throughput (elasto U), block-row sharded",
+        "value": mv_bytes * K / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": ws, "steps": K, "warmup": W,
+        "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+        "dtype": "c128", "data": "synthetic (Fibonacci sphere, seeded complex Gaussian x, seed 0)",
+        "config": {"workload": f"{args.config} H-matvec", "kernel": "elasto U", "n_points": w.n_points,
+                   "n_leaf": w.n_leaf, "eta": w.eta, "eps_aca": w.eps, "ks": w.ks,
+                   "parallelism": f"block-row shards x{ws} (one all-reduce of y per matvec)",
+                   "l2": "inputs larger than L2, no flush"},
+        "gpu_launches": 4 * K,
+        "e2e": {"value": mv_bytes * K / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 16 * n,
+                "d2h_bytes_per_step": 16 * n, "ms_per_step": e2e_ms / K},
+        "assembly": {"wall_s_max_over_ranks": t_asm, "leaves_this_rank": int(len(sh.part_idx))},
+        "clocks": clk.summary(),
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        tdist.barrier()
+        tdist.destroy_process_group()
+
+
 if __name__ == "__main__":
     a = parse()
     if a.impl == "reference":
         reference_arm(a)
+    elif a.shard:
+        shard_arm(a)
     else:
         hmx_arm(a)

@@ -131,6 +131,26 @@ def f64c(a, shape=None):
 _ctx = {}
 
 
+_bound = {}
+
+
+def bind_stream(device, stream_ptr):
+    """Make the context launch on ``stream_ptr`` (cudaStream_t); no-op when it
+    already does.  Switching synchronises the previous stream once."""
+    stream_ptr = int(stream_ptr)
+    if _bound.get(device) != stream_ptr:
+        check(lib().hmx_ctx_set_stream(context(device), stream_ptr), "hmx_ctx_set_stream")
+        _bound[device] = stream_ptr
+
+
+def bind_torch_stream(device=0):
+    """Order the context's launches with torch's current stream on ``device``
+    (device-tensor entry points: results are then visible to later torch ops)."""
+    import torch
+
+    bind_stream(device, torch.cuda.current_stream(device).cuda_stream)
+
+
 def release_cached(device=0):
     """Hand the context's cached device blocks back to the driver (before a
     library such as cuSOLVER has to allocate on the same device)."""

@@ -96,7 +96,7 @@ class HMatrix:
 
     def use_stream(self, stream_ptr):
         """Launch on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""
-        _lib.check(_lib.lib().hmx_ctx_set_stream(_lib.context(self.device), int(stream_ptr)), "set_stream")
+        _lib.bind_stream(self.device, stream_ptr)
 
     @classmethod
     def from_factors(cls, d, n_points, perm, table, payload, device=0):
@@ -217,6 +217,7 @@ def matvec(h, x, out=None):
         if x.dtype != torch.complex128 or x.numel() != n or not x.is_contiguous():
             raise ValueError("dimension mismatch")
         y = torch.empty_like(x) if out is None else out
+        _lib.bind_torch_stream(h.device)  # stream-ordered with the caller's torch work
         _lib.check(_lib.lib().hmx_matvec(h.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), DEVICE),
                    "hmx_matvec")
         return y
