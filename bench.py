@@ -406,8 +406,8 @@ def hmx_arm(args):
                            "row_gemv_GBps": dom_gbs, "finalize_ms": ph[3] / nc, "bytes": mv_bytes}),
         "assembly": {"ms": st["t_total_ms"], "wall_s": t_asm_wall, "ms_warm": st_warm["t_total_ms"],
                      "wall_s_warm": t_asm_wall_warm,
-                     "note": "ms = first assembly in the process (includes cold cudaMalloc of the ACA "
-                             "workspaces); ms_warm = a second assembly of the same problem (steady state)",
+                     "note": "ms = first assembly in the process (empty allocator cache, cold host vectors, "
+                             "clocks ramping); ms_warm = a second assembly of the same problem (steady state)",
                      "tree_build_s": t_tree,
                      "aca_ms": st["t_aca_ms"], "recompress_ms": st["t_recompress_ms"],
                      "dense_ms": st["t_dense_ms"], "form_ms": st["t_form_ms"],
