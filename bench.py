@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-solve", action="store_true", help="skip the T65k time-to-solve run")
     ap.add_argument("--no-estimate", action="store_true", help="skip the delta_{H,F} estimator timing")
     ap.add_argument("--solve-config", default="T65k")
+    ap.add_argument("--extra-configs", default="U131k,U8k,H4k",
+                    help="other BASELINE configs measured briefly (assembly + 20 matvecs); '' to skip")
     ap.add_argument("--shard", action="store_true",
                     help="block-row sharded H (SURVEY 8(e)): each rank assembles 1/N of the leaves, one "
                          "all-reduce of y per matvec, strong scaling (default: independent replicas)")
@@ -254,6 +256,51 @@ def time_to_solve(tag, device):
     return out
 
 
+def config_summary(tag, device, dfma_tflops, steps=20):
+    """Brief measurement of another BASELINE config: steady-state assembly
+    (second call) and the device H-matvec (mean of ``steps`` calls)."""
+    import torch
+
+    import paper_1706_09384_b200 as hmx
+    from paper_1706_09384_b200.configs import WORKLOADS
+    from paper_1706_09384_b200.flops import PAIR_FLOPS, survey_flops
+
+    w = WORKLOADS[tag]
+    cloud = hmx.make_geometry("sphere", w.n_points, 1.0, d=w.d)
+    ct = hmx.build_cluster_tree(cloud, w.n_leaf)
+    bt = hmx.build_block_tree(ct, ct, w.eta)
+    H, rep = hmx.assemble(w.spec(), cloud, ct, bt, hmx.ACAConfig(eps_aca=w.eps), device=device)
+    del H  # the second assembly is the steady-state one
+    H, rep = hmx.assemble(w.spec(), cloud, ct, bt, hmx.ACAConfig(eps_aca=w.eps), device=device)
+    st = H.stats()
+    n = w.d * w.n_points
+    x = torch.randn(n, dtype=torch.complex128, device=f"cuda:{device}")
+    y = torch.empty_like(x)
+    for _ in range(3):
+        hmx.matvec(H, x, out=y)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record()
+    for _ in range(steps):
+        hmx.matvec(H, x, out=y)
+    e1.record()
+    torch.cuda.synchronize()
+    mv_ms = e0.elapsed_time(e1) / steps
+    bi = H.block_info()
+    t = st["t_total_ms"] * 1e-3
+    sv, _ = survey_flops(H.table, bi["steps"], bi["rank_before"], bi["rank_after"], w.d, w.kind,
+                         st["pairs_evaluated"])
+    ex = st["flops_assembly"] + PAIR_FLOPS[w.kind] * st["pairs_evaluated"]
+    out = {"n_points": w.n_points, "kind": w.kind, "n_leaf": w.n_leaf, "assembly_ms": st["t_total_ms"],
+           "green_entries_per_s": w.d * w.d * st["pairs_evaluated"] / t,
+           "fp64_frac_survey_model": sv / t / 1e12 / dfma_tflops, "fp64_frac_executed": ex / t / 1e12 / dfma_tflops,
+           "matvec_ms": mv_ms, "matvec_GBps": st["matvec_bytes"] / (mv_ms * 1e-3) / 1e9,
+           "matvec_bytes": st["matvec_bytes"], "l2_resident": st["matvec_bytes"] < 100e6,
+           "max_rank_after": rep.max_rank_after, "tau": rep.tau}
+    del H
+    return out
+
+
 def hmx_arm(args):
     import torch
 
@@ -448,6 +495,14 @@ def hmx_arm(args):
                              "delta_h_frob_rel": float(np.sqrt(err2.sum() / norm2.sum())),
                              "worst_leaf_eps": float(ratio.max()), "leaves_above_eps": int((ratio > 1).sum()),
                              "leaves_above_3eps": int((ratio > 3).sum())}
+    if args.extra_configs:
+        del H
+        L.hmx_ctx_release_cache(_lib.context(local))
+        line["other_configs"] = {}
+        for tag in [t for t in args.extra_configs.split(",") if t]:
+            line["other_configs"][tag] = config_summary(tag, local, dfma.value)
+            L.hmx_ctx_release_cache(_lib.context(local))
+        H = None
     if not args.no_solve:
         # its own job: the U32k H-matrix and the cached workspaces are handed back first
         del H
