@@ -19,6 +19,7 @@
 #include <cstring>
 #include <string>
 #include <map>
+#include <unordered_map>
 #include <vector>
 
 #include "../../include/hmx.h"
@@ -552,11 +553,13 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     // the admissible leaves cut [0, np) into atoms; one pass over the points
     // boxes every atom, and a cluster's box is the merge of its atoms' boxes.
     std::vector<int64_t> cuts;
-    cuts.reserve(4 * adm.size() + 2);
-    for (int64_t b : adm)
-      for (int q = 1; q <= 4; ++q) cuts.push_back(table[5 * b + q]);
-    std::sort(cuts.begin(), cuts.end());
-    cuts.erase(std::unique(cuts.begin(), cuts.end()), cuts.end());
+    {
+      std::vector<unsigned char> mark((size_t)np + 1, 0);  // boundaries are point indices in [0, np]
+      for (int64_t b : adm)
+        for (int q = 1; q <= 4; ++q) mark[(size_t)table[5 * b + q]] = 1;
+      for (int64_t v = 0; v <= np; ++v)
+        if (mark[(size_t)v]) cuts.push_back(v);
+    }
     const size_t na = cuts.empty() ? 0 : cuts.size() - 1;
     std::vector<double> abox(6 * na);
     for (size_t a = 0; a < na; ++a) {
@@ -586,12 +589,14 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     };
     const double floor_cols = d == 1 ? 36.0 : 60.0;
     // clusters are shared by many leaves: one diameter per distinct (start, stop)
-    std::map<std::pair<int64_t, int64_t>, double> dcache;
+    std::unordered_map<int64_t, double> dcache;
+    dcache.reserve(2 * adm.size() + 16);
     auto diam_c = [&](int64_t a0, int64_t a1) {
-      auto it = dcache.find({a0, a1});
+      const int64_t key = a0 * (np + 1) + a1;
+      auto it = dcache.find(key);
       if (it != dcache.end()) return it->second;
       const double v = diam(a0, a1);
-      dcache.emplace(std::make_pair(a0, a1), v);
+      dcache.emplace(key, v);
       return v;
     };
     for (int64_t b : adm) {
@@ -754,10 +759,18 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   while (!todo.empty()) {
     passes.emplace_back(c);
     AcaPass& ps = passes.back();
-    std::sort(todo.begin(), todo.end(), [&](int64_t x, int64_t y) {
-      const int64_t ca = rows_of(x) + cols_of(x), cb = rows_of(y) + cols_of(y);
-      return ca != cb ? ca > cb : x < y;
-    });
+    {
+      // LPT order (m + n descending, leaf index ascending) by a counting sort
+      std::sort(todo.begin(), todo.end());
+      int64_t smax = 0;
+      for (int64_t b : todo) smax = std::max<int64_t>(smax, rows_of(b) + cols_of(b));
+      std::vector<int64_t> cnt((size_t)smax + 2, 0);
+      for (int64_t b : todo) cnt[(size_t)(smax - (rows_of(b) + cols_of(b))) + 1]++;
+      for (size_t i = 1; i < cnt.size(); ++i) cnt[i] += cnt[i - 1];
+      std::vector<int64_t> srt(todo.size());
+      for (int64_t b : todo) srt[(size_t)cnt[(size_t)(smax - (rows_of(b) + cols_of(b)))]++] = b;
+      todo.swap(srt);
+    }
     ps.blocks = todo;
     int64_t uo = 0, vo = 0, go = 0;
     ps.desc.resize(todo.size());
