@@ -274,6 +274,11 @@ int hmx_ctx_create(int32_t device, hmx_ctx** out) {
   HMX_CUDA_TRY(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
   c->c.own_stream = true;
   HMX_CUDA_TRY(cudaStreamCreateWithFlags(&c->c.aux, cudaStreamNonBlocking));
+  {
+    int lo = 0, hi = 0;  // hi = greatest priority (numerically lowest)
+    HMX_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    HMX_CUDA_TRY(cudaStreamCreateWithPriority(&c->c.rerun, cudaStreamNonBlocking, hi));
+  }
   // HMX_POOL=1: stream-ordered pool allocations (measured slower for the first
   // assembly and for T65k on this driver; off by default)
   if (const char* ep = std::getenv("HMX_POOL"); ep && ep[0] == '1') {
@@ -326,6 +331,7 @@ int hmx_ctx_destroy(hmx_ctx* ctx) {
   cudaSetDevice(ctx->c.device);
   if (ctx->c.own_stream && ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
   if (ctx->c.aux) cudaStreamDestroy(ctx->c.aux);
+  if (ctx->c.rerun) cudaStreamDestroy(ctx->c.rerun);
   if (ctx->c.pool) cudaMemPoolDestroy(ctx->c.pool);
   release_cache(ctx->c);
   delete ctx;
@@ -587,7 +593,11 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       return std::sqrt((hi3[0] - lo3[0]) * (hi3[0] - lo3[0]) + (hi3[1] - lo3[1]) * (hi3[1] - lo3[1]) +
                        (hi3[2] - lo3[2]) * (hi3[2] - lo3[2]));
     };
-    const double floor_cols = d == 1 ? 36.0 : 60.0;
+    // K <= a + 2 d kappa diam with a = 66 (d = 3), and at low frequency a
+    // geometry-independent floor of 78 columns: tools/kcap_census.py over the
+    // five configs (U131k, kappa_s = 2, needs K + 3 <= kcap at K = 66-81)
+    const double floor_cols = d == 1 ? 36.0 : 66.0;
+    const double floor_lo = d == 1 ? 36.0 : 78.0;
     // clusters are shared by many leaves: one diameter per distinct (start, stop)
     std::unordered_map<int64_t, double> dcache;
     dcache.reserve(2 * adm.size() + 16);
@@ -602,7 +612,8 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     for (int64_t b : adm) {
       const double dm =
           std::max(diam_c(table[5 * b + 1], table[5 * b + 2]), diam_c(table[5 * b + 3], table[5 * b + 4]));
-      const int64_t est = round_d((int64_t)std::ceil(floor_cols + 2.0 * d * kap * dm) + d - 1);
+      const int64_t est =
+          round_d((int64_t)std::ceil(std::max(floor_lo, floor_cols + 2.0 * d * kap * dm)) + d - 1);
       kcap[b] = std::min<int64_t>(maxr[b], std::min<int64_t>(est, round_d(kMaxAcaCols)));
     }
     // fit the budget: scale the model down uniformly if needed
@@ -756,7 +767,36 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     if (nfb) return HMX_OK;
     return recompress_subset(ps, std::move(live));
   };
+  // Capacity-overflow reruns (passes after the first) depend only on the
+  // points and their own workspaces: they go to a high-priority stream
+  // (ordered after everything issued before this assembly) and overlap the
+  // first pass's remaining recompression instead of trailing it.
+  cudaEvent_t ev_start;
+  HMX_CUDA_TRY(cudaEventCreateWithFlags(&ev_start, cudaEventDisableTiming));
+  HMX_CUDA_TRY(cudaEventRecord(ev_start, c.stream));
+  HMX_CUDA_TRY(cudaStreamWaitEvent(c.rerun, ev_start, 0));
+  cudaEventDestroy(ev_start);
+  struct StreamSwap {
+    Ctx& c;
+    cudaStream_t s0, a0;
+    bool on = false;
+    void enter() {
+      if (!on) {
+        s0 = c.stream;
+        a0 = c.aux;
+        c.stream = c.aux = c.rerun;
+        on = true;
+      }
+    }
+    ~StreamSwap() {
+      if (on) {
+        c.stream = s0;
+        c.aux = a0;
+      }
+    }
+  } rerun_swap{c, nullptr, nullptr};
   while (!todo.empty()) {
+    if (H.aca_passes > 0) rerun_swap.enter();
     passes.emplace_back(c);
     AcaPass& ps = passes.back();
     {
@@ -888,6 +928,16 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     cudaEventDestroy(join);
     todo.swap(next);
     next.clear();
+  }
+  if (rerun_swap.on) {  // back to the context streams; main waits for the reruns
+    c.stream = rerun_swap.s0;
+    c.aux = rerun_swap.a0;
+    rerun_swap.on = false;
+    cudaEvent_t join;
+    HMX_CUDA_TRY(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+    HMX_CUDA_TRY(cudaEventRecord(join, c.rerun));
+    HMX_CUDA_TRY(cudaStreamWaitEvent(c.stream, join, 0));
+    cudaEventDestroy(join);
   }
   HMX_CUDA_TRY(cudaEventRecord(ev[1], c.stream));
   tick("aca done");

@@ -29,6 +29,7 @@ struct Ctx {
   cudaMemPool_t pool = nullptr;  // stream-ordered pool, never released to the driver between assemblies
   cudaStream_t stream = nullptr;
   cudaStream_t aux = nullptr;  // second stream for concurrent launches inside assembly
+  cudaStream_t rerun = nullptr;  // high-priority stream for ACA capacity-overflow reruns
   bool own_stream = false;
   int num_sms = 148;
   size_t l2_bytes = 0;
