@@ -637,7 +637,16 @@ __device__ unsigned long long g_tc_prof[16];
       tw_t0 = t_;                                                                    \
     }                                                                                \
   } while (0)
+#define TC_T0() const long long te0_ = clock64()
+#define TC_TADD(i) \
+  do { if ((threadIdx.x & 31) == 0) atomicAdd(&g_tc_prof[(i)], (unsigned long long)(clock64() - te0_)); } while (0)
 #else
+#define TC_T0() \
+  do {          \
+  } while (0)
+#define TC_TADD(i) \
+  do {             \
+  } while (0)
 #define TC_MARK(i) \
   do {             \
   } while (0)
@@ -963,7 +972,11 @@ __global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
       const int j = (int)(r0 / 3) + p;
       if (p < kTcRows / 3 && j < n) {
         double2 R[9];
-        green_xy_k<KIND>(P, pts, ds.r0 + ipiv, pts, ds.c0 + j, R);
+        {
+          TC_T0();
+          green_xy_k<KIND>(P, pts, ds.r0 + ipiv, pts, ds.c0 + j, R);
+          TC_TADD(10);
+        }
 #pragma unroll
         for (int c = 0; c < 3; ++c) {
           const double* rr = reinterpret_cast<const double*>(ring) + (3 * p + c) * 12;  // V row 3 j + c
@@ -979,7 +992,11 @@ __global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
 #pragma unroll
           for (int c = 0; c < 3; ++c) Vb[(int64_t)(3 * j + c) + (int64_t)(K + a) * ldv] = cconj(R[a * 3 + c]);
         double s1, s3;
-        svals3(R, s1, s3);
+        {
+          TC_T0();
+          svals3(R, s1, s3);
+          TC_TADD(11);
+        }
         rs1 = fmax(rs1, s1);
         best = argmax_pick(best, ArgMax{s3, j});
       }

@@ -979,6 +979,10 @@ __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __rest
   const int fr = lane >> 2, fk = lane & 3;  // fragment row / k (A), column group lane / k (B)
   const int row0 = tm * TM, col0 = tn * TN;
   const int nk = (ds.K + TK - 1) / TK;
+  // valid row octets / 4-column groups of this warp's 32 x 8 sub-tile (small r,
+  // short last row tile: the MMAs on the zero padding are skipped)
+  const int no = min(4, max(0, (ds.rows - (row0 + wm * 32) + 7) / 8));
+  const int ng = min(2, max(0, (ds.r - (col0 + wn * 8) + 3) / 4));
   auto stage = [&](int kc, int buf) {
     const int k0 = kc * TK;
     for (int t = tid; t < TK * TM; t += kFormThreads) {
@@ -1025,10 +1029,11 @@ __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __rest
 #pragma unroll
       for (int o = 0; o < 4; ++o)
 #pragma unroll
-        for (int g = 0; g < 2; ++g) {
-          dmma_8x8x4(c1[o][g][0], c1[o][g][1], av[o].x, bv[g]);
-          dmma_8x8x4(c2[o][g][0], c2[o][g][1], av[o].y, bv[g]);
-        }
+        for (int g = 0; g < 2; ++g)
+          if (o < no && g < ng) {  // warp-uniform: no MMAs on row octets / column groups past the item
+            dmma_8x8x4(c1[o][g][0], c1[o][g][1], av[o].x, bv[g]);
+            dmma_8x8x4(c2[o][g][0], c2[o][g][1], av[o].y, bv[g]);
+          }
     }
   }
   cp_async_wait<0>();

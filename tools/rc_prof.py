@@ -51,3 +51,4 @@ for tag in sys.argv[1:] or ["U32k"]:
         tot = sum(v[:6])
         print("  TC ACA (thread 0, summed over CTAs): " + "  ".join(f"{n} {100 * x / max(tot, 1):.1f}%" for n, x in zip(tn, v[:6])))
         print(f"  TC warps: streaming {v[8] / 1e9:.2f} Gcyc, epilogue {v[9] / 1e9:.2f} Gcyc; thread-0 total {tot / 1e9:.2f} Gcyc")
+        print(f"  TC row-pass epilogue parts (lane 0 of each warp): Green's {v[10] / 1e9:.2f} Gcyc, sigma_3 {v[11] / 1e9:.2f} Gcyc")
