@@ -137,6 +137,12 @@ int hmx_hmatrix_block_info(const hmx_hmatrix* h, int64_t* steps, int64_t* rank_b
                            int32_t* flags);
 /* copy leaf b out (layouts as in hmx_hmatrix_load) */
 int hmx_hmatrix_get_block(const hmx_hmatrix* h, int64_t b, double* a, double* v);
+/* zero-copy device view of the leaf payloads (input of the H-LU, which the reference's
+ * hmatrix module runs on its in-memory per-leaf payloads): per leaf b the offset of its dense block / U
+ * columns in the row stream (column-major, leading dimension ld[b]) and of its V columns in the V stream
+ * (column-major, leading dimension d n); bufs = {row stream device pointer, row elements, V stream device
+ * pointer, V elements} (complex128 elements).  The views stay valid while h lives and must not be written. */
+int hmx_hmatrix_device_layout(const hmx_hmatrix* h, int64_t* moff, int64_t* ld, int64_t* voff, uint64_t* bufs);
 /* delta_{H,F} estimator kernel (SPEC.md:507-515 estimate(): "for each AdmissibleLeaf regenerate the
  * dense block from the kernel, accumulate ||A_block - U V*||_F^2").  Per leaf b:
  * err2[b] = ||A_b - U_b V_b^H||_F^2 (0 for dense leaves), norm2[b] = ||A_b||_F^2 of the regenerated

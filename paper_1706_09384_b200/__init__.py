@@ -12,6 +12,7 @@ from .geometry import (AABB, AdmissibleLeaf, BlockTree, ClusterNode, ClusterTree
                        PointCloud, Subdivided, build_block_tree, build_cluster_tree, diam_box,
                        dist_box, is_admissible, make_geometry, sparsity_pattern)
 from .estimate import EstimatorReport, estimate  # noqa: F401
+from .hierarchical_lu import LUFactors, formatted_addmul, hlu, lu_matvec, solve_direct, triangular_solve  # noqa: F401
 from .hmatrix import HMatrix, StorageReport, assemble, block_errors, matvec, storage_report  # noqa: F401
 from .kernels import (KernelSpec, Material, Wavenumbers, assemble_dense, elasto_t_block,  # noqa: F401
                       elasto_u_block, eval_elasto_t, eval_elasto_u, eval_scalar, scalar_block)

@@ -66,6 +66,7 @@ SIGNATURES = {
     "hmx_hmatrix_stats": (C.c_int, [P, C.POINTER(HmxStats)]),
     "hmx_hmatrix_block_info": (C.c_int, [P, P, P, P, P]),
     "hmx_hmatrix_get_block": (C.c_int, [P, i64, P, P]),
+    "hmx_hmatrix_device_layout": (C.c_int, [P, P, P, P, P]),
     "hmx_block_errors": (C.c_int, [P, P, P, P, i64, C.c_double, P, P]),
     "hmx_aca_block": (C.c_int, [P, C.POINTER(HmxKernel), P, i64, P, i64, P, i32, f64, C.POINTER(HmxAcaCfg), i32,
                                 i64, P, P, C.POINTER(i64), C.POINTER(i64), C.POINTER(i32)]),

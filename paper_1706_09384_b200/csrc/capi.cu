@@ -1194,6 +1194,23 @@ int hmx_hmatrix_block_info(const hmx_hmatrix* h, int64_t* steps, int64_t* rank_b
   return HMX_OK;
 }
 
+int hmx_hmatrix_device_layout(const hmx_hmatrix* h, int64_t* moff, int64_t* ld, int64_t* voff, uint64_t* bufs) {
+  if (!h || !moff || !ld || !voff || !bufs) return HMX_EINVAL;
+  const DeviceH& H = h->H;
+  HMX_CUDA_TRY(cudaSetDevice(H.ctx->device));
+  HMX_CUDA_TRY(cudaStreamSynchronize(H.ctx->stream));
+  for (int64_t b = 0; b < H.nb; ++b) {
+    moff[b] = H.leaf_moff[b];
+    ld[b] = H.leaf_ld[b];
+    voff[b] = H.leaf_voff[b];
+  }
+  bufs[0] = reinterpret_cast<uint64_t>(H.d_row);
+  bufs[1] = static_cast<uint64_t>(H.row_elems);
+  bufs[2] = reinterpret_cast<uint64_t>(H.d_v);
+  bufs[3] = static_cast<uint64_t>(H.v_elems);
+  return HMX_OK;
+}
+
 int hmx_hmatrix_get_block(const hmx_hmatrix* h, int64_t b, double* a, double* v) {
   if (!h || !a || b < 0 || b >= h->H.nb) return HMX_EINVAL;
   const DeviceH& H = h->H;

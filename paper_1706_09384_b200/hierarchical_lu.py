@@ -1,0 +1,719 @@
+"""Formatted H-arithmetic and the recursive H-LU on the device -- the reference's
+``hmatx.hmatrix`` operations ``formatted_addmul``, ``hlu``, ``triangular_solve``
+and ``hmatx.solve.solve_direct`` (section 3.2,
+"the LU factorization is classically decomposed into 4 steps").  The reference
+module is absent from the mount; SURVEY 8(f) row 4.
+
+Layout.  The factorisation works on a device-resident copy of the assembled
+H-matrix's leaves, rebuilt into the block tree of ``BlockTree.root``
+(``geometry.py:277-295``): ``Dense`` (dm x dn complex128), ``LowRank``
+(U dm x k, V dn x k, block = U V^H) and ``Sub`` (grid of children over the
+cluster children).  The leaves are taken zero-copy from the assembly's HBM
+streams (``hmx_hmatrix_device_layout``) and cloned, so the source H stays
+immutable.  All index ranges are dofs in tree order.
+
+Arithmetic (all complex128 on the device, torch's current stream):
+* dense diagonal leaves: pivoted LU (cuSOLVER getrf); L = P L~ unit lower,
+  U upper, the permutation kept as an index vector;
+* triangular solves with dense / low-rank / hierarchical right-hand sides
+  (low-rank: only U, resp. V, is transformed);
+* ``formatted_addmul`` C <- C + alpha A B over the 27 format cases: a
+  low-rank operand multiplies through its thin factors, hierarchical x
+  hierarchical recurses over the cluster children, dense targets accumulate
+  densely; low-rank targets collect addends and are truncated once, with
+  eps_LU, when they are next read (QR of both factor panels, SVD of the K x K
+  core, the Frobenius-tail rule of ``recompress``).  A
+  product landing on a low-rank target without a low-rank operand is formed
+  per child block and agglomerated into one factor pair (padded factors,
+  one truncation).
+
+The LU is in place: ``LUFactors.lower`` / ``.upper`` are the strictly lower /
+upper blocks plus the unit-lower / upper factors of the diagonal leaves of the
+same tree.
+"""
+
+import time
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from . import _lib
+from .errors import FactorizationError
+from .geometry import AdmissibleLeaf, DenseLeaf, Subdivided
+
+_RULES = ("frobenius", "spectral")
+
+
+def _torch():
+    import torch
+
+    if not torch.cuda.is_available():
+        raise RuntimeError("hlu: a CUDA device is required (no CPU fallback)")
+    return torch
+
+
+# --------------------------------------------------------------------------------------------
+# node types
+# --------------------------------------------------------------------------------------------
+class Dense:
+    __slots__ = ("r0", "r1", "c0", "c1", "a", "L", "U", "pidx", "pinv")
+
+    def __init__(self, r0, r1, c0, c1, a):
+        self.r0, self.r1, self.c0, self.c1, self.a = r0, r1, c0, c1, a
+        self.L = self.U = self.pidx = self.pinv = None
+
+
+class LowRank:
+    __slots__ = ("r0", "r1", "c0", "c1", "u", "v", "pend")
+
+    def __init__(self, r0, r1, c0, c1, u, v):
+        self.r0, self.r1, self.c0, self.c1, self.u, self.v = r0, r1, c0, c1, u, v
+        self.pend = []
+
+    @property
+    def rank(self):
+        return int(self.u.shape[1])
+
+
+class Sub:
+    __slots__ = ("r0", "r1", "c0", "c1", "rs", "cs", "ch")
+
+    def __init__(self, r0, r1, c0, c1, rs, cs, ch):
+        self.r0, self.r1, self.c0, self.c1, self.rs, self.cs, self.ch = r0, r1, c0, c1, rs, cs, ch
+
+
+@dataclass
+class Arith:
+    """Truncation settings + counters of one formatted-arithmetic session."""
+
+    eps: float
+    rule: str = "frobenius"
+    n_trunc: int = 0
+    n_getrf: int = 0
+    max_rank: int = 0
+
+    def __post_init__(self):
+        if self.rule not in _RULES:
+            raise ValueError(f"unknown truncation rule {self.rule!r}")
+        if not self.eps >= 0:
+            raise ValueError("eps_lu must be >= 0")
+
+
+def _trank(s, eps, rule):
+    """Kept rank for descending singular values (the recompress rule)."""
+    if s.size == 0 or s[0] == 0.0:
+        return 0
+    if rule == "spectral":
+        return int(np.count_nonzero(s > eps * s[0]))
+    sq = s * s
+    tail = np.concatenate([np.cumsum(sq[::-1])[::-1], [0.0]])
+    return int(np.flatnonzero(tail <= (eps * eps) * tail[0])[0])
+
+
+def _trunc(ar, u, v):
+    """(U, V) -> truncated (U', V') with U' V'^H ~ U V^H (QR, QR, SVD of the core)."""
+    torch = _torch()
+    if u.shape[1] == 0:
+        return u, v
+    ar.n_trunc += 1
+    qu, ru = torch.linalg.qr(u)
+    qv, rv = torch.linalg.qr(v)
+    p, s, lh = torch.linalg.svd(ru @ rv.mH, full_matrices=False)
+    r = _trank(s.cpu().numpy(), ar.eps, ar.rule)
+    ar.max_rank = max(ar.max_rank, r)
+    root = s[:r].sqrt().to(u.dtype)
+    return (qu @ p[:, :r]) * root, (qv @ lh.mH[:, :r]) * root
+
+
+def _dense_to_lr(ar, m):
+    torch = _torch()
+    ar.n_trunc += 1
+    p, s, lh = torch.linalg.svd(m, full_matrices=False)
+    r = _trank(s.cpu().numpy(), ar.eps, ar.rule)
+    ar.max_rank = max(ar.max_rank, r)
+    root = s[:r].sqrt().to(m.dtype)
+    return p[:, :r] * root, lh.mH[:, :r] * root
+
+
+def _flush(ar, x):
+    if x.pend:
+        torch = _torch()
+        us = [x.u] + [p[0] for p in x.pend]
+        vs = [x.v] + [p[1] for p in x.pend]
+        x.pend = []
+        x.u, x.v = _trunc(ar, torch.cat(us, 1), torch.cat(vs, 1))
+
+
+# --------------------------------------------------------------------------------------------
+# products with dense multivectors, conversion
+# --------------------------------------------------------------------------------------------
+def _mul(ar, x, X):
+    """x @ X for a dense multivector X (rows = x's columns)."""
+    if isinstance(x, Dense):
+        return x.a @ X
+    if isinstance(x, LowRank):
+        _flush(ar, x)
+        return x.u @ (x.v.mH @ X)
+    out = X.new_zeros((x.r1 - x.r0, X.shape[1]))
+    for i, (a, b) in enumerate(x.rs):
+        for j, (c, e) in enumerate(x.cs):
+            out[a - x.r0:b - x.r0] += _mul(ar, x.ch[i][j], X[c - x.c0:e - x.c0])
+    return out
+
+
+def _mulh(ar, x, X):
+    """x^H @ X for a dense multivector X (rows = x's rows)."""
+    if isinstance(x, Dense):
+        return x.a.mH @ X
+    if isinstance(x, LowRank):
+        _flush(ar, x)
+        return x.v @ (x.u.mH @ X)
+    out = X.new_zeros((x.c1 - x.c0, X.shape[1]))
+    for i, (a, b) in enumerate(x.rs):
+        for j, (c, e) in enumerate(x.cs):
+            out[c - x.c0:e - x.c0] += _mulh(ar, x.ch[i][j], X[a - x.r0:b - x.r0])
+    return out
+
+
+def _dense(ar, x):
+    torch = _torch()
+    if isinstance(x, Dense):
+        return x.a
+    if isinstance(x, LowRank):
+        _flush(ar, x)
+        return x.u @ x.v.mH
+    out = torch.zeros((x.r1 - x.r0, x.c1 - x.c0), dtype=torch.complex128, device=_dev_of(x))
+    for i, (a, b) in enumerate(x.rs):
+        for j, (c, e) in enumerate(x.cs):
+            out[a - x.r0:b - x.r0, c - x.c0:e - x.c0] = _dense(ar, x.ch[i][j])
+    return out
+
+
+def _dev_of(x):
+    while isinstance(x, Sub):
+        x = x.ch[0][0]
+    return x.a.device if isinstance(x, Dense) else x.u.device
+
+
+def _part(ar, x, i, k, r0, r1, c0, c1):
+    """Sub-block [r0, r1) x [c0, c1) of operand x: child (i, k) of a Sub, a view of a leaf."""
+    if isinstance(x, Sub):
+        ch = x.ch[i][k]
+        if (ch.r0, ch.r1, ch.c0, ch.c1) != (r0, r1, c0, c1):
+            raise ValueError("formatted_addmul: non-conformal block partitions")
+        return ch
+    if (x.r0, x.r1, x.c0, x.c1) == (r0, r1, c0, c1):
+        return x
+    if isinstance(x, Dense):
+        return Dense(r0, r1, c0, c1, x.a[r0 - x.r0:r1 - x.r0, c0 - x.c0:c1 - x.c0])
+    _flush(ar, x)
+    return LowRank(r0, r1, c0, c1, x.u[r0 - x.r0:r1 - x.r0], x.v[c0 - x.c0:c1 - x.c0])
+
+
+def _parts(x, rows):
+    if isinstance(x, Sub):
+        return x.rs if rows else x.cs
+    return [(x.r0, x.r1)] if rows else [(x.c0, x.c1)]
+
+
+# --------------------------------------------------------------------------------------------
+# formatted addition / multiplication
+# --------------------------------------------------------------------------------------------
+def _add_lr(ar, C, U, V):
+    """C += U V^H."""
+    if U.shape[1] == 0:
+        return
+    if isinstance(C, Dense):
+        C.a.addmm_(U, V.mH)
+    elif isinstance(C, LowRank):
+        C.pend.append((U, V))
+    else:
+        for i, (a, b) in enumerate(C.rs):
+            for j, (c, e) in enumerate(C.cs):
+                _add_lr(ar, C.ch[i][j], U[a - C.r0:b - C.r0], V[c - C.c0:e - C.c0])
+
+
+def _add_dense(ar, C, M):
+    """C += M (dense addend)."""
+    if isinstance(C, Dense):
+        C.a += M
+    elif isinstance(C, LowRank):
+        C.pend.append(_dense_to_lr(ar, M))
+    else:
+        for i, (a, b) in enumerate(C.rs):
+            for j, (c, e) in enumerate(C.cs):
+                _add_dense(ar, C.ch[i][j], M[a - C.r0:b - C.r0, c - C.c0:e - C.c0])
+
+
+def _prod_lr(ar, A, B):
+    """Low-rank (U, V) with U V^H ~ A B (truncated with eps)."""
+    torch = _torch()
+    if isinstance(A, LowRank):
+        _flush(ar, A)
+        return A.u, _mulh(ar, B, A.v)
+    if isinstance(B, LowRank):
+        _flush(ar, B)
+        return _mul(ar, A, B.u), B.v
+    if isinstance(A, Dense) and isinstance(B, Dense):
+        return _dense_to_lr(ar, A.a @ B.a)
+    # at least one hierarchical operand: per child block, then agglomerate with one truncation
+    m, n = A.r1 - A.r0, B.c1 - B.c0
+    Rp, Cp = _parts(A, True), _parts(B, False)
+    Kp = A.cs if isinstance(A, Sub) else B.rs
+    us, vs = [], []
+    for i, (ra, rb) in enumerate(Rp):
+        for j, (ca, cb) in enumerate(Cp):
+            for k, (ka, kb) in enumerate(Kp):
+                u, v = _prod_lr(ar, _part(ar, A, i, k, ra, rb, ka, kb), _part(ar, B, k, j, ka, kb, ca, cb))
+                if u.shape[1] == 0:
+                    continue
+                up = u.new_zeros((m, u.shape[1]))
+                vp = v.new_zeros((n, v.shape[1]))
+                up[ra - A.r0:rb - A.r0] = u
+                vp[ca - B.c0:cb - B.c0] = v
+                us.append(up)
+                vs.append(vp)
+    if not us:
+        dev = _dev_of(A)
+        z = torch.zeros((m, 0), dtype=torch.complex128, device=dev)
+        return z, torch.zeros((n, 0), dtype=torch.complex128, device=dev)
+    return _trunc(ar, torch.cat(us, 1), torch.cat(vs, 1))
+
+
+def _addmul(ar, C, A, B, alpha=-1.0):
+    """C <- C + alpha A B (formatted, truncation eps_LU on low-rank targets)."""
+    if isinstance(A, LowRank) and isinstance(B, LowRank):
+        # rank min(r_A, r_B) through the r_A x r_B core A.v^H B.u
+        _flush(ar, A)
+        _flush(ar, B)
+        core = A.v.mH @ B.u
+        if A.rank <= B.rank:
+            _add_lr(ar, C, alpha * A.u, B.v @ core.mH)
+        else:
+            _add_lr(ar, C, alpha * (A.u @ core), B.v)
+        return
+    if isinstance(A, LowRank):
+        _flush(ar, A)
+        if A.rank:
+            _add_lr(ar, C, alpha * A.u, _mulh(ar, B, A.v))
+        return
+    if isinstance(B, LowRank):
+        _flush(ar, B)
+        if B.rank:
+            _add_lr(ar, C, alpha * _mul(ar, A, B.u), B.v)
+        return
+    if isinstance(C, Sub):
+        Kp = A.cs if isinstance(A, Sub) else (B.rs if isinstance(B, Sub) else [(A.c0, A.c1)])
+        for i, (ra, rb) in enumerate(C.rs):
+            for j, (ca, cb) in enumerate(C.cs):
+                for k, (ka, kb) in enumerate(Kp):
+                    _addmul(ar, C.ch[i][j], _part(ar, A, i, k, ra, rb, ka, kb),
+                            _part(ar, B, k, j, ka, kb, ca, cb), alpha)
+        return
+    if isinstance(C, Dense):
+        if isinstance(A, Dense) and isinstance(B, Dense):
+            C.a.addmm_(A.a, B.a, alpha=alpha)
+        else:
+            C.a.add_(_mul(ar, A, _dense(ar, B)), alpha=alpha)
+        return
+    u, v = _prod_lr(ar, A, B)
+    if u.shape[1]:
+        C.pend.append((alpha * u, v))
+
+
+# --------------------------------------------------------------------------------------------
+# LU and triangular solves
+# --------------------------------------------------------------------------------------------
+def _lu(ar, x, path):
+    torch = _torch()
+    if isinstance(x, Dense):
+        ar.n_getrf += 1
+        lu, piv, info = torch.linalg.lu_factor_ex(x.a)
+        P, L, U = torch.lu_unpack(lu, piv)
+        d = U.diagonal().abs()
+        dmax = float(d.max()) if d.numel() else 0.0
+        if int(info) != 0 or d.numel() == 0 or float(d.min()) <= 1e-14 * max(dmax, 1e-300):
+            raise FactorizationError(f"hlu: singular dense diagonal leaf at block path {path} "
+                                     f"(rows [{x.r0}, {x.r1}))")
+        x.L, x.U = L, U
+        x.pidx = P.real.argmax(0)   # P^T X = X[pidx]
+        x.pinv = P.real.argmax(1)   # P X = X[pinv]
+        x.a = None
+        return
+    if not isinstance(x, Sub) or x.rs != x.cs:
+        raise ValueError("hlu: diagonal block is not square / hierarchical")
+    p = len(x.rs)
+    for k in range(p):
+        _lu(ar, x.ch[k][k], path + (k,))
+        for j in range(k + 1, p):
+            _solve_lower(ar, x.ch[k][k], x.ch[k][j])
+        for i in range(k + 1, p):
+            _solve_upper_right(ar, x.ch[k][k], x.ch[i][k])
+        for i in range(k + 1, p):
+            for j in range(k + 1, p):
+                _addmul(ar, x.ch[i][j], x.ch[i][k], x.ch[k][j], -1.0)
+
+
+def _lsolve(ar, L, X):
+    """L^{-1} X for a dense multivector (L = factored diagonal node)."""
+    torch = _torch()
+    if isinstance(L, Dense):
+        return torch.linalg.solve_triangular(L.L, X[L.pidx], upper=False, unitriangular=True)
+    X = X.clone()
+    for k, (a, b) in enumerate(L.rs):
+        xk = _lsolve(ar, L.ch[k][k], X[a - L.r0:b - L.r0])
+        X[a - L.r0:b - L.r0] = xk
+        for i in range(k + 1, len(L.rs)):
+            c, e = L.rs[i]
+            X[c - L.r0:e - L.r0] -= _mul(ar, L.ch[i][k], xk)
+    return X
+
+
+def _usolve(ar, U, X):
+    """U^{-1} X for a dense multivector."""
+    torch = _torch()
+    if isinstance(U, Dense):
+        return torch.linalg.solve_triangular(U.U, X, upper=True)
+    X = X.clone()
+    for k in range(len(U.rs) - 1, -1, -1):
+        a, b = U.rs[k]
+        xk = _usolve(ar, U.ch[k][k], X[a - U.r0:b - U.r0])
+        X[a - U.r0:b - U.r0] = xk
+        for i in range(k):
+            c, e = U.rs[i]
+            X[c - U.r0:e - U.r0] -= _mul(ar, U.ch[i][k], xk)
+    return X
+
+
+def _rsolve(ar, U, Y):
+    """Y U^{-1} for a dense multivector Y (columns = U's columns)."""
+    torch = _torch()
+    if isinstance(U, Dense):
+        return torch.linalg.solve_triangular(U.U, Y, upper=True, left=False)
+    Y = Y.clone()
+    for k, (a, b) in enumerate(U.cs):
+        yk = _rsolve(ar, U.ch[k][k], Y[:, a - U.c0:b - U.c0])
+        Y[:, a - U.c0:b - U.c0] = yk
+        for j in range(k + 1, len(U.cs)):
+            c, e = U.cs[j]
+            Y[:, c - U.c0:e - U.c0] -= _mulh(ar, U.ch[k][j], yk.mH).mH
+    return Y
+
+
+def _solve_lower(ar, L, B):
+    """B <- L^{-1} B (B any format, same row cluster as L)."""
+    if isinstance(B, Dense):
+        B.a = _lsolve(ar, L, B.a)
+    elif isinstance(B, LowRank):
+        _flush(ar, B)
+        if B.rank:
+            B.u = _lsolve(ar, L, B.u)
+    elif isinstance(L, Sub):
+        p = len(L.rs)
+        for j in range(len(B.cs)):
+            for k in range(p):
+                _solve_lower(ar, L.ch[k][k], B.ch[k][j])
+                for i in range(k + 1, p):
+                    _addmul(ar, B.ch[i][j], L.ch[i][k], B.ch[k][j], -1.0)
+    else:
+        for j in range(len(B.cs)):
+            _solve_lower(ar, L, B.ch[0][j])
+
+
+def _solve_upper_right(ar, U, B):
+    """B <- B U^{-1} (B any format, same column cluster as U)."""
+    if isinstance(B, Dense):
+        B.a = _rsolve(ar, U, B.a)
+    elif isinstance(B, LowRank):
+        _flush(ar, B)
+        if B.rank:
+            B.v = _rsolve(ar, U, B.v.mH).mH
+    elif isinstance(U, Sub):
+        p = len(U.cs)
+        for i in range(len(B.rs)):
+            for k in range(p):
+                _solve_upper_right(ar, U.ch[k][k], B.ch[i][k])
+                for j in range(k + 1, p):
+                    _addmul(ar, B.ch[i][j], B.ch[i][k], U.ch[k][j], -1.0)
+    else:
+        for i in range(len(B.rs)):
+            _solve_upper_right(ar, U, B.ch[i][0])
+
+
+def _lmul(ar, L, X):
+    """L X (unit-lower factor incl. the leaf permutations)."""
+    if isinstance(L, Dense):
+        return (L.L @ X)[L.pinv]
+    out = X.new_zeros(X.shape)
+    for i, (a, b) in enumerate(L.rs):
+        acc = _lmul(ar, L.ch[i][i], X[a - L.r0:b - L.r0])
+        for j in range(i):
+            c, e = L.rs[j]
+            acc = acc + _mul(ar, L.ch[i][j], X[c - L.r0:e - L.r0])
+        out[a - L.r0:b - L.r0] = acc
+    return out
+
+
+def _umul(ar, U, X):
+    if isinstance(U, Dense):
+        return U.U @ X
+    out = X.new_zeros(X.shape)
+    for i, (a, b) in enumerate(U.rs):
+        acc = _umul(ar, U.ch[i][i], X[a - U.r0:b - U.r0])
+        for j in range(i + 1, len(U.rs)):
+            c, e = U.rs[j]
+            acc = acc + _mul(ar, U.ch[i][j], X[c - U.r0:e - U.r0])
+        out[a - U.r0:b - U.r0] = acc
+    return out
+
+
+def _flush_all(ar, x):
+    if isinstance(x, LowRank):
+        _flush(ar, x)
+    elif isinstance(x, Sub):
+        for row in x.ch:
+            for c in row:
+                _flush_all(ar, c)
+
+
+def _walk(x):
+    if isinstance(x, Sub):
+        for row in x.ch:
+            for c in row:
+                yield from _walk(c)
+    else:
+        yield x
+
+
+# --------------------------------------------------------------------------------------------
+# construction
+# --------------------------------------------------------------------------------------------
+class _CAI:
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (int(n),), "typestr": "<c16", "data": (int(ptr), False),
+                                         "version": 3, "strides": None}
+
+
+def _build(root, d, leaf_of, make_leaf):
+    def rec(node):
+        if isinstance(node, (DenseLeaf, AdmissibleLeaf)):
+            return make_leaf(leaf_of[(node.row.index, node.col.index)])
+        r, c = node.row, node.col
+        rk = (r,) if r.is_leaf else r.children
+        ck = (c,) if c.is_leaf else c.children
+        kids = [rec(k) for k in node.children]
+        grid = [kids[i * len(ck):(i + 1) * len(ck)] for i in range(len(rk))]
+        return Sub(d * r.start, d * r.stop, d * c.start, d * c.stop,
+                   [(d * q.start, d * q.stop) for q in rk], [(d * q.start, d * q.stop) for q in ck], grid)
+
+    return rec(root)
+
+
+def _leaf_index(bt):
+    return {(int(t[5]), int(t[6])): b for b, t in enumerate(bt.table)}
+
+
+def copy_hmatrix(h, block_tree=None):
+    """Device node tree holding a private copy of every leaf of the assembled H
+    (zero-copy views of the HBM streams, cloned)."""
+    torch = _torch()
+    bt = block_tree if block_tree is not None else h.block_tree
+    if bt is None:
+        raise ValueError("hlu needs the H-matrix's block tree")
+    nb = len(h.table)
+    moff = np.empty(nb, np.int64)
+    ld = np.empty(nb, np.int64)
+    voff = np.empty(nb, np.int64)
+    bufs = np.empty(4, np.uint64)
+    _lib.check(_lib.lib().hmx_hmatrix_device_layout(h.handle, _lib.ptr(moff), _lib.ptr(ld), _lib.ptr(voff),
+                                                    _lib.ptr(bufs)), "hmx_hmatrix_device_layout")
+    dev = torch.device("cuda", h.device)
+    R = torch.as_tensor(_CAI(bufs[0], bufs[1]), device=dev)
+    Vs = torch.as_tensor(_CAI(bufs[2], bufs[3]), device=dev) if bufs[3] else None
+    ranks = h.block_info()["rank_after"]
+    d = h.d
+    tab = np.asarray(h.table)
+
+    def make_leaf(b):
+        k, r0, r1, c0, c1 = (int(t) for t in tab[b][:5])
+        dm, dn = d * (r1 - r0), d * (c1 - c0)
+        o, l = int(moff[b]), int(ld[b])
+        if k == 0:
+            a = R[o:o + l * dn].view(dn, l)[:, :dm].transpose(0, 1).contiguous()
+            return Dense(d * r0, d * r1, d * c0, d * c1, a)
+        r = int(ranks[b])
+        if r == 0:
+            u = torch.zeros((dm, 0), dtype=torch.complex128, device=dev)
+            v = torch.zeros((dn, 0), dtype=torch.complex128, device=dev)
+        else:
+            u = R[o:o + l * r].view(r, l)[:, :dm].transpose(0, 1).contiguous()
+            vo = int(voff[b])
+            v = Vs[vo:vo + dn * r].view(r, dn).transpose(0, 1).contiguous()
+        return LowRank(d * r0, d * r1, d * c0, d * c1, u, v)
+
+    return _build(bt.root, d, _leaf_index(bt), make_leaf)
+
+
+def from_dense(bt, d, A, eps, rule="frobenius", device=0):
+    """Node tree of a dense (tree-ordered) matrix on the block partition ``bt``:
+    dense leaves copied, admissible leaves compressed by truncated SVD with ``eps``
+    (test / formatted_addmul operands)."""
+    torch = _torch()
+    dev = torch.device("cuda", device)
+    At = torch.as_tensor(np.ascontiguousarray(A), dtype=torch.complex128, device=dev)
+    ar = Arith(eps, rule)
+    tab = bt.table
+
+    def make_leaf(b):
+        k, r0, r1, c0, c1 = (int(t) for t in tab[b][:5])
+        blk = At[d * r0:d * r1, d * c0:d * c1]
+        if k == 0:
+            return Dense(d * r0, d * r1, d * c0, d * c1, blk.clone())
+        u, v = _dense_to_lr(ar, blk)
+        return LowRank(d * r0, d * r1, d * c0, d * c1, u.contiguous(), v.contiguous())
+
+    return _build(bt.root, d, _leaf_index(bt), make_leaf)
+
+
+def to_dense(x, ar=None):
+    """Dense (tree-ordered) device matrix of a node tree."""
+    return _dense(ar or Arith(0.0), x)
+
+
+def formatted_addmul(target, a, b, eps_lu, rule="frobenius"):
+    """target <- target + a b in the H-format of ``target`` (
+    PAPER.md 3.2 "A''' <- A + A' A''", the 27 format cases); low-rank targets
+    are truncated with ``eps_lu``.  Returns the updated target."""
+    if (a.r0, a.r1) != (target.r0, target.r1) or (b.c0, b.c1) != (target.c0, target.c1) or \
+            (a.c0, a.c1) != (b.r0, b.r1):
+        raise ValueError("formatted_addmul: non-conformal ranges")
+    ar = Arith(eps_lu, rule)
+    _addmul(ar, target, a, b, 1.0)
+    _flush_all(ar, target)
+    return target
+
+
+# --------------------------------------------------------------------------------------------
+# public API: hlu / triangular_solve / solve_direct
+# --------------------------------------------------------------------------------------------
+@dataclass
+class _Tri:
+    """``LUFactors.lower`` / ``.upper``: a triangular view of the in-place factor tree."""
+
+    root: object
+    lower: bool
+
+
+@dataclass
+class LUFactors:
+    """L_H (unit lower by block convention, leaf pivots folded
+    in), U_H (upper), eps_LU.  Both views share the in-place factor tree."""
+
+    lower: _Tri
+    upper: _Tri
+    eps_lu: float
+    d: int
+    perm: np.ndarray
+    n: int
+    stats: dict = field(default_factory=dict)
+
+    @property
+    def root(self):
+        return self.lower.root
+
+    def storage(self):
+        """Complex entries stored by the factors (dense leaves count dm x dn)."""
+        tot = 0
+        for x in _walk(self.root):
+            if isinstance(x, Dense):
+                tot += (x.r1 - x.r0) * (x.c1 - x.c0)
+            else:
+                tot += x.rank * ((x.r1 - x.r0) + (x.c1 - x.c0))
+        return tot
+
+
+def hlu(h, eps_lu, rule="frobenius", block_tree=None):
+    """Recursive H-LU of an assembled square H-matrix: steps
+    (1) LU(A11), (2) U12 = L11^{-1} A12, (3) L21 = A21 U11^{-1}, (4) A22 -= L21 U12
+    by ``formatted_addmul`` with truncation ``eps_lu``, recurse; dense leaves by
+    pivoted LU.  Raises ``FactorizationError`` on a singular diagonal leaf."""
+    torch = _torch()
+    if h.block_tree is None and block_tree is None:
+        raise ValueError("hlu needs the H-matrix's block tree")
+    bt = block_tree if block_tree is not None else h.block_tree
+    if bt.rows is not bt.cols and not np.array_equal(bt.rows.permutation, bt.cols.permutation):
+        raise ValueError("hlu: row and column trees differ")
+    torch.cuda.set_device(h.device)
+    _lib.release_cached(h.device)
+    t0 = time.perf_counter()
+    root = copy_hmatrix(h, bt)
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    ar = Arith(float(eps_lu), rule)
+    _lu(ar, root, ())
+    _flush_all(ar, root)
+    torch.cuda.synchronize()
+    t2 = time.perf_counter()
+    f = LUFactors(lower=_Tri(root, True), upper=_Tri(root, False), eps_lu=float(eps_lu), d=h.d,
+                  perm=np.asarray(h.perm), n=h.d * h.n_points)
+    f.stats = {"copy_s": t1 - t0, "factor_s": t2 - t1, "n_truncations": ar.n_trunc, "n_getrf": ar.n_getrf,
+               "max_rank": ar.max_rank}
+    return f
+
+
+def _to_tree(f, b):
+    torch = _torch()
+    d = f.d
+    idx = torch.as_tensor((d * f.perm[:, None] + np.arange(d)[None, :]).reshape(-1), device=_dev_of(f.root))
+    return idx
+
+
+def _as_dev(f, b):
+    torch = _torch()
+    dev = _dev_of(f.root)
+    if hasattr(b, "is_cuda"):
+        bt = b.to(device=dev, dtype=torch.complex128)
+        host = False
+    else:
+        b = np.asarray(b, dtype=np.complex128)
+        bt = torch.as_tensor(b, device=dev)
+        host = True
+    if bt.shape[0] != f.n:
+        raise ValueError("dimension mismatch")
+    return bt, host
+
+
+def triangular_solve(f, b):
+    """x0 = U_H^{-1} L_H^{-1} b; b, x0 in original point order
+    (numpy in -> numpy out; CUDA tensor in -> CUDA tensor out)."""
+    bt, host = _as_dev(f, b)
+    idx = _to_tree(f, b)
+    vec = bt.dim() == 1
+    X = bt.reshape(f.n, -1)[idx]
+    ar = Arith(f.eps_lu)
+    X = _usolve(ar, f.root, _lsolve(ar, f.root, X))
+    out = X.new_empty(X.shape)
+    out[idx] = X
+    out = out.reshape(-1) if vec else out
+    return out.cpu().numpy() if host else out
+
+
+def lu_matvec(f, x):
+    """L_H U_H x (original point order) -- the consistency product of SPEC.md:417, 443."""
+    bt, host = _as_dev(f, x)
+    idx = _to_tree(f, x)
+    vec = bt.dim() == 1
+    X = bt.reshape(f.n, -1)[idx]
+    ar = Arith(f.eps_lu)
+    Y = _lmul(ar, f.root, _umul(ar, f.root, X))
+    out = Y.new_empty(Y.shape)
+    out[idx] = Y
+    out = out.reshape(-1) if vec else out
+    return out.cpu().numpy() if host else out
+
+
+def solve_direct(h, b, eps_lu, rule="frobenius"):
+    """factorise once with ``hlu(h, eps_lu)`` and solve;
+    returns (x0, LUFactors) so the factors can be reused for more right-hand sides."""
+    f = hlu(h, eps_lu, rule)
+    return triangular_solve(f, b), f
