@@ -192,7 +192,9 @@ def _dense(ar, x):
 def _dev_of(x):
     while isinstance(x, Sub):
         x = x.ch[0][0]
-    return x.a.device if isinstance(x, Dense) else x.u.device
+    if isinstance(x, Dense):
+        return (x.a if x.a is not None else x.U).device
+    return x.u.device
 
 
 def _part(ar, x, i, k, r0, r1, c0, c1):
