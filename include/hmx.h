@@ -166,6 +166,19 @@ int hmx_recompress(hmx_ctx* ctx, int64_t dm, int64_t dn, int64_t K, const double
 
 /* ---- H-matvec / GMRES ---------------------------------------------------------- */
 /* y = A_H x, x and y in ORIGINAL point order (d N complex each) */
+/* Batched truncation of accumulated low-rank sums on the device (the recompress of SPEC.md:318-326
+ * applied to the addends that formatted_addmul collects on a low-rank target; used by
+ * the H-LU).  Item i: U_i (dm_i x K_i) and V_i (dn_i x K_i), complex128, column-major, device pointers.
+ * Writes U'_i = U_i W_U (dm_i x r_i) and V'_i = V_i W_V (dn_i x r_i) column-major into Uo_i / Vo_i
+ * (capacity K_i columns, leading dimensions dm_i / dn_i) with U'_i V'_i^H the rank-r_i truncation of
+ * U_i V_i^H (same Gram / Cholesky / Hermitian eigen-solver and truncation rule as hmx_assemble);
+ * r_i -> ranks (host).  K_i <= 1020.  flags_i bit 0: the Cholesky of V_i^H V_i needed regularisation
+ * (V_i numerically rank-deficient); such an item is NOT formed and the caller re-submits it in a
+ * well-conditioned form (e.g. (U_i V_i^H, I)).  Launches on the context stream and returns once the
+ * ranks are known (one host synchronisation per batch). */
+int hmx_truncate_batch(hmx_ctx* ctx, int64_t nb, const int64_t* dm, const int64_t* dn, const int64_t* K,
+                       const uint64_t* U, const uint64_t* V, const uint64_t* Uo, const uint64_t* Vo, double eps,
+                       int32_t trunc_rule, int64_t* ranks, int32_t* flags);
 int hmx_matvec(hmx_hmatrix* h, const double* x, double* y, int32_t mem);
 /* device pointers; phase_ms[4] = gather, phase 1 (V^H x), phase 2 (row GEMV), finalize */
 int hmx_matvec_profile(hmx_hmatrix* h, const double* x_dev, double* y_dev, float* phase_ms);

@@ -21,8 +21,13 @@ Decisions (shared with the device implementation ``paper_1706_09384_b200/hierarc
    SVD(R_U R_V^H), Frobenius-tail rule of ``lowrank.truncation_rank`` (decision 8 of
    oracle/lowrank.py) with eps_LU;
 5. a product with no low-rank operand landing on a low-rank target is formed per child
-   block (dense leaf pairs compressed by SVD) and agglomerated with one truncation;
-6. a singular dense diagonal leaf (|u_ii| <= 1e-14 max |u_jj|) raises with its block path.
+   block (a dense leaf pair A B as the untruncated pair (A, B^H)) and agglomerated by
+   concatenating padded factors, truncated only above AGGLO_MAX columns;
+6. a singular dense diagonal leaf (|u_ii| <= 1e-14 max |u_jj|) raises with its block path;
+7. truncation points: a target holding more than PEND_FLUSH columns; every low-rank leaf
+   of the trailing blocks after each elimination step of the LU and of the block
+   triangular solves (the device batches each such set into one kernel call); a block
+   read as an operand; the end of hlu / formatted_addmul.
 """
 
 import numpy as np
@@ -31,6 +36,8 @@ import scipy.linalg as sla
 from .lowrank import truncation_rank
 
 DENSE, LOWRANK, SUB = 0, 1, 2
+PEND_FLUSH = 400     # decision 7: pending columns on one target before an early truncation
+AGGLO_MAX = 512      # decision 5: agglomerated product columns before an intermediate truncation
 
 
 class Node:
@@ -202,13 +209,19 @@ def _part(cx, x, i, k, r0, r1, c0, c1):
 
 
 # ---- formatted add / multiply -------------------------------------------------------------
+def _pend(cx, C, U, V):
+    C.pend.append((U, V))
+    if C.u.shape[1] + sum(p[0].shape[1] for p in C.pend) > PEND_FLUSH:
+        _flush(cx, C)
+
+
 def _add_lr(cx, C, U, V):
     if U.shape[1] == 0:
         return
     if C.kind == DENSE:
         C.a += U @ V.conj().T
     elif C.kind == LOWRANK:
-        C.pend.append((U, V))
+        _pend(cx, C, U, V)
     else:
         for i, (a, b) in enumerate(C.rs):
             for j, (c, e) in enumerate(C.cs):
@@ -223,7 +236,7 @@ def _prod_lr(cx, A, B):
         _flush(cx, B)
         return mul(cx, A, B.u), B.v
     if A.kind == DENSE and B.kind == DENSE:
-        return _compress(cx, A.a @ B.a)
+        return A.a, B.a.conj().T
     m, n = A.r1 - A.r0, B.c1 - B.c0
     Rp = A.rs if A.kind == SUB else [(A.r0, A.r1)]
     Cp = B.cs if B.kind == SUB else [(B.c0, B.c1)]
@@ -243,7 +256,8 @@ def _prod_lr(cx, A, B):
                 vs.append(vp)
     if not us:
         return np.zeros((m, 0), np.complex128), np.zeros((n, 0), np.complex128)
-    return _trunc(cx, np.concatenate(us, 1), np.concatenate(vs, 1))
+    U, V = np.concatenate(us, 1), np.concatenate(vs, 1)
+    return _trunc(cx, U, V) if U.shape[1] > AGGLO_MAX else (U, V)
 
 
 def addmul(cx, C, A, B, alpha=-1.0):
@@ -281,7 +295,7 @@ def addmul(cx, C, A, B, alpha=-1.0):
         return
     u, v = _prod_lr(cx, A, B)
     if u.shape[1]:
-        C.pend.append((alpha * u, v))
+        _pend(cx, C, alpha * u, v)
 
 
 def formatted_addmul(target, a, b, eps_lu, rule="frobenius"):
@@ -311,6 +325,9 @@ def lu(cx, x, path=()):
         for i in range(k + 1, p):
             for j in range(k + 1, p):
                 addmul(cx, x.ch[i][j], x.ch[i][k], x.ch[k][j], -1.0)
+        for i in range(k + 1, p):
+            for j in range(k + 1, p):
+                flush_all(cx, x.ch[i][j])
 
 
 def _perm_T(x, X):
@@ -380,12 +397,16 @@ def solve_lower(cx, L, B):
         if B.u.shape[1]:
             B.u = lsolve(cx, L, B.u)
     elif L.kind == SUB:
-        p = len(L.rs)
-        for j in range(len(B.cs)):
-            for k in range(p):
+        p, q = len(L.rs), len(B.cs)
+        for k in range(p):
+            for j in range(q):
                 solve_lower(cx, L.ch[k][k], B.ch[k][j])
+            for j in range(q):
                 for i in range(k + 1, p):
                     addmul(cx, B.ch[i][j], L.ch[i][k], B.ch[k][j], -1.0)
+            for i in range(k + 1, p):
+                for j in range(q):
+                    flush_all(cx, B.ch[i][j])
     else:
         for j in range(len(B.cs)):
             solve_lower(cx, L, B.ch[0][j])
@@ -399,12 +420,16 @@ def solve_upper_right(cx, U, B):
         if B.u.shape[1]:
             B.v = rsolve(cx, U, B.v.conj().T).conj().T
     elif U.kind == SUB:
-        p = len(U.cs)
-        for i in range(len(B.rs)):
-            for k in range(p):
+        p, q = len(U.cs), len(B.rs)
+        for k in range(p):
+            for i in range(q):
                 solve_upper_right(cx, U.ch[k][k], B.ch[i][k])
+            for i in range(q):
                 for j in range(k + 1, p):
                     addmul(cx, B.ch[i][j], B.ch[i][k], U.ch[k][j], -1.0)
+            for i in range(q):
+                for j in range(k + 1, p):
+                    flush_all(cx, B.ch[i][j])
     else:
         for i in range(len(B.rs)):
             solve_upper_right(cx, U, B.ch[i][0])

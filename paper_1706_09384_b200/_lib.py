@@ -71,6 +71,7 @@ SIGNATURES = {
     "hmx_aca_block": (C.c_int, [P, C.POINTER(HmxKernel), P, i64, P, i64, P, i32, f64, C.POINTER(HmxAcaCfg), i32,
                                 i64, P, P, C.POINTER(i64), C.POINTER(i64), C.POINTER(i32)]),
     "hmx_recompress": (C.c_int, [P, i64, i64, i64, P, P, f64, i32, C.POINTER(i64), P, P]),
+    "hmx_truncate_batch": (C.c_int, [P, i64, P, P, P, P, P, P, P, f64, i32, P, P]),
     "hmx_hmatrix_free": (None, [P]),
     "hmx_matvec": (C.c_int, [P, P, P, i32]),
     "hmx_matvec_profile": (C.c_int, [P, P, P, C.POINTER(C.c_float)]),

@@ -1486,6 +1486,45 @@ int recompress_device(Ctx& c, DevBuf& mem, const double2* dU, const double2* dV,
   return launch_form(c, d_fd, 2, nt, d_ts);
 }
 
+// ---- batched truncation of accumulated factor pairs (H-arithmetic) ---------------------------
+struct GramItem {
+  const double2* F;  // rows x K, column-major (ld = rows)
+  int64_t rows;
+  int32_t K, pad;
+  double2* G;  // K x K, ld = K
+};
+
+// G = F^H F, one 16 x 16 output tile per CTA; 32-row chunks of both column groups staged in shared
+// memory with coalesced column reads
+__global__ void __launch_bounds__(256) gram_batch(const GramItem* __restrict__ items, const int2* __restrict__ tiles) {
+  __shared__ double2 sa[32][17];
+  __shared__ double2 sb[32][17];
+  const int2 tl = tiles[blockIdx.x];
+  const GramItem it = items[tl.x];
+  const int K = it.K;
+  const int nt = (K + 15) / 16;
+  const int i0 = (tl.y % nt) * 16, j0 = (tl.y / nt) * 16;
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double2 s = cmk(0.0, 0.0);
+  for (int64_t q0 = 0; q0 < it.rows; q0 += 32) {
+    for (int e = threadIdx.x; e < 512; e += 256) {
+      const int r = e & 31, cc = e >> 5;
+      const int64_t q = q0 + r;
+      sa[r][cc] = (q < it.rows && i0 + cc < K) ? it.F[q + (int64_t)(i0 + cc) * it.rows] : cmk(0.0, 0.0);
+      sb[r][cc] = (q < it.rows && j0 + cc < K) ? it.F[q + (int64_t)(j0 + cc) * it.rows] : cmk(0.0, 0.0);
+    }
+    __syncthreads();
+#pragma unroll 8
+    for (int r = 0; r < 32; ++r) s = cfma_ca(sa[r][ty], sb[r][tx], s);
+    __syncthreads();
+  }
+  const int i = i0 + ty, j = j0 + tx;
+  if (i < K && j < K) {
+    if (i == j) s.y = 0.0;
+    it.G[i + (int64_t)j * K] = s;
+  }
+}
+
 }  // namespace
 
 extern "C" {
@@ -1640,6 +1679,129 @@ int hmx_recompress(hmx_ctx* ctx, int64_t dm, int64_t dn, int64_t K, const double
     HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
     from_colmajor(ou, dm, r, r, reinterpret_cast<double2*>(Uout));
     from_colmajor(ov, dn, r, r, reinterpret_cast<double2*>(Vout));
+  }
+  return HMX_OK;
+}
+
+int hmx_truncate_batch(hmx_ctx* ctx, int64_t nb, const int64_t* dm, const int64_t* dn, const int64_t* K,
+                       const uint64_t* U, const uint64_t* V, const uint64_t* Uo, const uint64_t* Vo, double eps,
+                       int32_t trunc_rule, int64_t* ranks, int32_t* flags) {
+  if (!ctx || nb < 0 || (nb > 0 && (!dm || !dn || !K || !U || !V || !Uo || !Vo || !ranks || !flags)))
+    return HMX_EINVAL;
+  if (nb == 0) return HMX_OK;
+  for (int64_t i = 0; i < nb; ++i) {
+    if (dm[i] <= 0 || dn[i] <= 0 || K[i] < 0 || (K[i] > 0 && (!U[i] || !V[i] || !Uo[i] || !Vo[i]))) {
+      hmx_set_error("hmx_truncate_batch: item %lld has invalid sizes / pointers", (long long)i);
+      return HMX_EINVAL;
+    }
+    if (K[i] > 1020) {
+      hmx_set_error("hmx_truncate_batch: item %lld has %lld columns, above the device limit 1020", (long long)i,
+                    (long long)K[i]);
+      return HMX_EINVAL;
+    }
+    ranks[i] = 0;
+    flags[i] = 0;
+  }
+  Ctx& c = ctx->c;
+  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  // items with K > 0, largest K first (the recompression launches per K class)
+  std::vector<int64_t> live;
+  for (int64_t i = 0; i < nb; ++i)
+    if (K[i] > 0) live.push_back(i);
+  if (live.empty()) return HMX_OK;
+  std::stable_sort(live.begin(), live.end(), [&](int64_t a, int64_t b) { return K[a] > K[b]; });
+  const int64_t nl = (int64_t)live.size();
+  std::vector<RecDesc> rd((size_t)nl);
+  std::vector<GramItem> gi((size_t)(2 * nl));
+  std::vector<int2> tiles;
+  int64_t go = 0, wo = 0;
+  DevBuf mem(c);
+  for (int64_t q = 0; q < nl; ++q) {
+    const int64_t k = K[live[q]];
+    rd[q].goff = go;
+    rd[q].woff = wo;
+    rd[q].K = (int32_t)k;
+    rd[q].kcap = (int32_t)k;
+    go += 2 * k * k;
+    wo += 6 * k * k;
+  }
+  double2 *G, *W;
+  int rc;
+  if ((rc = mem.alloc(&G, go)) || (rc = mem.alloc(&W, wo))) return rc;
+  for (int64_t q = 0; q < nl; ++q) {
+    const int64_t i = live[q], k = K[i];
+    for (int side = 0; side < 2; ++side) {
+      GramItem& g = gi[2 * q + side];
+      g.F = reinterpret_cast<const double2*>(side == 0 ? U[i] : V[i]);
+      g.rows = side == 0 ? dm[i] : dn[i];
+      g.K = (int32_t)k;
+      g.pad = 0;
+      g.G = G + rd[q].goff + (side == 0 ? 0 : k * k);
+      const int nt = (int)hmx_cdiv(k, 16);
+      for (int t = 0; t < nt * nt; ++t) tiles.push_back(make_int2((int)(2 * q + side), t));
+    }
+  }
+  GramItem* d_gi;
+  int2* d_tiles;
+  RecDesc* d_rd;
+  int32_t *d_rank, *d_flag;
+  if ((rc = mem.alloc(&d_gi, 2 * nl)) || (rc = mem.alloc(&d_tiles, (int64_t)tiles.size())) ||
+      (rc = mem.alloc(&d_rd, nl)) || (rc = mem.alloc(&d_rank, nl)) || (rc = mem.alloc(&d_flag, nl)))
+    return rc;
+  HMX_CUDA_TRY(cudaMemcpyAsync(d_gi, gi.data(), sizeof(GramItem) * gi.size(), cudaMemcpyHostToDevice, c.stream));
+  HMX_CUDA_TRY(
+      cudaMemcpyAsync(d_tiles, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, c.stream));
+  HMX_CUDA_TRY(cudaMemcpyAsync(d_rd, rd.data(), sizeof(RecDesc) * rd.size(), cudaMemcpyHostToDevice, c.stream));
+  gram_batch<<<(unsigned)tiles.size(), 256, 0, c.stream>>>(d_gi, d_tiles);
+  HMX_CUDA_TRY(cudaGetLastError());
+  // K classes: > 112 (global-memory variant), 61..112, <= 60 (shared-memory variants, more CTAs per SM)
+  int64_t q0 = 0;
+  while (q0 < nl) {
+    const int kc = rd[q0].K;
+    const int lo = kc > 112 ? 112 : (kc > 60 ? 60 : 0);
+    int64_t q1 = q0;
+    while (q1 < nl && rd[q1].K > lo) ++q1;
+    if ((rc = launch_recompress_core(c, d_rd + q0, q1 - q0, kc, eps, trunc_rule, G, W, d_rank + q0, d_flag + q0)))
+      return rc;
+    q0 = q1;
+  }
+  std::vector<int32_t> hr((size_t)nl), hf((size_t)nl);
+  HMX_CUDA_TRY(cudaMemcpyAsync(hr.data(), d_rank, sizeof(int32_t) * nl, cudaMemcpyDeviceToHost, c.stream));
+  HMX_CUDA_TRY(cudaMemcpyAsync(hf.data(), d_flag, sizeof(int32_t) * nl, cudaMemcpyDeviceToHost, c.stream));
+  HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  std::vector<FormDesc> fd;
+  std::vector<int64_t> ts;
+  int64_t ntiles = 0;
+  for (int64_t q = 0; q < nl; ++q) {
+    const int64_t i = live[q], k = K[i];
+    const int r = hr[q];
+    ranks[i] = r;
+    flags[i] = hf[q];
+    if (r <= 0 || (hf[q] & 1)) continue;  // a regularised (rank-deficient V) item is not formed
+    for (int side = 0; side < 2; ++side) {
+      FormDesc f;
+      const int64_t rows = side == 0 ? dm[i] : dn[i];
+      f.A = reinterpret_cast<const double2*>(side == 0 ? U[i] : V[i]);
+      f.W = W + rd[q].woff + 4 * k * k + (side == 0 ? 0 : k * r);
+      f.C = reinterpret_cast<double2*>(side == 0 ? Uo[i] : Vo[i]);
+      f.rows = (int32_t)rows;
+      f.K = (int32_t)k;
+      f.r = r;
+      f.lda = (int32_t)rows;
+      f.ldc = (int32_t)rows;
+      f.pad = 0;
+      ts.push_back(ntiles);
+      ntiles += hmx_cdiv(rows, 64) * hmx_cdiv(r, 32);
+      fd.push_back(f);
+    }
+  }
+  if (!fd.empty()) {
+    FormDesc* d_fd;
+    int64_t* d_ts;
+    if ((rc = mem.alloc(&d_fd, (int64_t)fd.size())) || (rc = mem.alloc(&d_ts, (int64_t)ts.size()))) return rc;
+    HMX_CUDA_TRY(cudaMemcpyAsync(d_fd, fd.data(), sizeof(FormDesc) * fd.size(), cudaMemcpyHostToDevice, c.stream));
+    HMX_CUDA_TRY(cudaMemcpyAsync(d_ts, ts.data(), sizeof(int64_t) * ts.size(), cudaMemcpyHostToDevice, c.stream));
+    if ((rc = launch_form(c, d_fd, (int64_t)fd.size(), ntiles, d_ts))) return rc;
   }
   return HMX_OK;
 }

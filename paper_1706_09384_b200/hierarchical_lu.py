@@ -89,6 +89,9 @@ class Arith:
     eps: float
     rule: str = "frobenius"
     n_trunc: int = 0
+    n_trunc_calls: int = 0
+    t_trunc: float = 0.0
+    k_hist: list = field(default_factory=list)
     n_getrf: int = 0
     max_rank: int = 0
 
@@ -110,38 +113,140 @@ def _trank(s, eps, rule):
     return int(np.flatnonzero(tail <= (eps * eps) * tail[0])[0])
 
 
-def _trunc(ar, u, v):
-    """(U, V) -> truncated (U', V') with U' V'^H ~ U V^H (QR, QR, SVD of the core)."""
+_PEND_FLUSH = 400     # pending columns on one low-rank target before it is truncated early
+_AGGLO_MAX = 512      # agglomerated product columns before an intermediate truncation
+_TRULES = {"frobenius": 0, "spectral": 1}
+
+
+def _kernel_batch(ar, items):
+    """One ``hmx_truncate_batch`` call: list of (U, V) -> list of (U', V') or None for items whose
+    V was numerically rank-deficient (regularised Cholesky; not formed)."""
     torch = _torch()
-    if u.shape[1] == 0:
-        return u, v
-    ar.n_trunc += 1
-    qu, ru = torch.linalg.qr(u)
-    qv, rv = torch.linalg.qr(v)
-    p, s, lh = torch.linalg.svd(ru @ rv.mH, full_matrices=False)
-    r = _trank(s.cpu().numpy(), ar.eps, ar.rule)
-    ar.max_rank = max(ar.max_rank, r)
-    root = s[:r].sqrt().to(u.dtype)
-    return (qu @ p[:, :r]) * root, (qv @ lh.mH[:, :r]) * root
+    dev = items[0][0].device
+    _lib.bind_torch_stream(dev.index or 0)
+    n = len(items)
+    dm = np.empty(n, np.int64)
+    dn = np.empty(n, np.int64)
+    K = np.empty(n, np.int64)
+    ptr = np.zeros((4, n), np.uint64)
+    keep, outs = [], []
+    for i, (u, v) in enumerate(items):
+        dm[i], K[i] = u.shape
+        dn[i] = v.shape[0]
+        uc = u.mT.contiguous()          # (K, dm) row-major = dm x K column-major
+        vc = v.mT.contiguous()
+        uo = torch.empty_like(uc)
+        vo = torch.empty_like(vc)
+        keep += [uc, vc]
+        outs.append((uo, vo))
+        ptr[:, i] = (uc.data_ptr(), vc.data_ptr(), uo.data_ptr(), vo.data_ptr())
+    ranks = np.zeros(n, np.int64)
+    flags = np.zeros(n, np.int32)
+    ar.n_trunc_calls += 1
+    ar.k_hist.append(int(K.max()))
+    t0 = time.perf_counter()
+    _lib.check(_lib.lib().hmx_truncate_batch(_lib.context(dev.index or 0), n, _lib.ptr(dm), _lib.ptr(dn),
+                                              _lib.ptr(K), _lib.ptr(ptr[0]), _lib.ptr(ptr[1]), _lib.ptr(ptr[2]),
+                                              _lib.ptr(ptr[3]), float(ar.eps), _TRULES[ar.rule],
+                                              _lib.ptr(ranks), _lib.ptr(flags)), "hmx_truncate_batch")
+    ar.t_trunc += time.perf_counter() - t0
+    res = []
+    for i, (uo, vo) in enumerate(outs):
+        if flags[i] & 1:
+            res.append(None)
+            continue
+        r = int(ranks[i])
+        res.append((uo[:r].mT, vo[:r].mT))
+    return res
+
+
+def _dense_form(u, v):
+    """U V^H as the pair (U V^H, I): the V side is orthonormal, so the kernel's Cholesky is exact."""
+    torch = _torch()
+    n = v.shape[0]
+    return u @ v.mH, torch.eye(n, dtype=u.dtype, device=u.device)
+
+
+def _truncate_batch(ar, items):
+    """items: list of (U, V) pairs (any strides) -> list of truncated (U', V') pairs, on the device
+    through ``hmx_truncate_batch`` (Gram pair, scaled Cholesky, Hermitian eigen-solver, truncation
+    rule, U' = U W_U, V' = V W_V -- the assembly's recompression kernels), one call per batch.
+    A pair with at least as many columns as V has rows, or whose V turns out numerically
+    rank-deficient, is re-submitted as (U V^H, I)."""
+    if not items:
+        return []
+    res = [None] * len(items)
+    sub, idx = [], []
+    for i, (u, v) in enumerate(items):
+        if u.shape[1] == 0:
+            res[i] = (u, v)
+            continue
+        ar.n_trunc += 1
+        sub.append(_dense_form(u, v) if u.shape[1] >= v.shape[0] else (u, v))
+        idx.append(i)
+    while idx:
+        out = _kernel_batch(ar, sub)
+        redo, ridx = [], []
+        for i, s_, o in zip(idx, sub, out):
+            if o is not None:
+                res[i] = o
+                ar.max_rank = max(ar.max_rank, o[0].shape[1])
+            elif s_[0].shape[1] < s_[1].shape[0] and s_[1].shape[0] <= 1020:
+                redo.append(_dense_form(*items[i]))
+                ridx.append(i)
+            else:
+                raise FloatingPointError("hmx_truncate_batch: rank-deficient factor pair with no "
+                                         "well-conditioned form (V rows > 1020)")
+        sub, idx = redo, ridx
+    return res
+
+
+def _trunc(ar, u, v):
+    """(U, V) -> truncated (U', V') with U' V'^H ~ U V^H."""
+    return _truncate_batch(ar, [(u, v)])[0]
 
 
 def _dense_to_lr(ar, m):
+    """Truncated SVD of a dense block (operand construction only)."""
     torch = _torch()
-    ar.n_trunc += 1
     p, s, lh = torch.linalg.svd(m, full_matrices=False)
     r = _trank(s.cpu().numpy(), ar.eps, ar.rule)
-    ar.max_rank = max(ar.max_rank, r)
     root = s[:r].sqrt().to(m.dtype)
     return p[:, :r] * root, lh.mH[:, :r] * root
 
 
+def _cat(x):
+    torch = _torch()
+    us = [x.u] + [p[0] for p in x.pend]
+    vs = [x.v] + [p[1] for p in x.pend]
+    x.pend = []
+    # stacked as (K, rows) row-major = the column-major panels the truncation kernel reads
+    return torch.cat([t.mT for t in us], 0).mT, torch.cat([t.mT for t in vs], 0).mT
+
+
 def _flush(ar, x):
     if x.pend:
-        torch = _torch()
-        us = [x.u] + [p[0] for p in x.pend]
-        vs = [x.v] + [p[1] for p in x.pend]
-        x.pend = []
-        x.u, x.v = _trunc(ar, torch.cat(us, 1), torch.cat(vs, 1))
+        x.u, x.v = _trunc(ar, *_cat(x))
+
+
+def _pending(x, out):
+    if isinstance(x, LowRank):
+        if x.pend:
+            out.append(x)
+    elif isinstance(x, Sub):
+        for row in x.ch:
+            for c in row:
+                _pending(c, out)
+
+
+def _flush_batch(ar, nodes):
+    """Truncate every pending low-rank leaf under ``nodes`` in one batched call."""
+    todo = []
+    for x in nodes:
+        _pending(x, todo)
+    if todo:
+        for x, (u, v) in zip(todo, _truncate_batch(ar, [_cat(x) for x in todo])):
+            x.u, x.v = u, v
 
 
 # --------------------------------------------------------------------------------------------
@@ -221,6 +326,12 @@ def _parts(x, rows):
 # --------------------------------------------------------------------------------------------
 # formatted addition / multiplication
 # --------------------------------------------------------------------------------------------
+def _pend(ar, C, U, V):
+    C.pend.append((U, V))
+    if C.u.shape[1] + sum(p[0].shape[1] for p in C.pend) > _PEND_FLUSH:
+        _flush(ar, C)
+
+
 def _add_lr(ar, C, U, V):
     """C += U V^H."""
     if U.shape[1] == 0:
@@ -228,23 +339,11 @@ def _add_lr(ar, C, U, V):
     if isinstance(C, Dense):
         C.a.addmm_(U, V.mH)
     elif isinstance(C, LowRank):
-        C.pend.append((U, V))
+        _pend(ar, C, U, V)
     else:
         for i, (a, b) in enumerate(C.rs):
             for j, (c, e) in enumerate(C.cs):
                 _add_lr(ar, C.ch[i][j], U[a - C.r0:b - C.r0], V[c - C.c0:e - C.c0])
-
-
-def _add_dense(ar, C, M):
-    """C += M (dense addend)."""
-    if isinstance(C, Dense):
-        C.a += M
-    elif isinstance(C, LowRank):
-        C.pend.append(_dense_to_lr(ar, M))
-    else:
-        for i, (a, b) in enumerate(C.rs):
-            for j, (c, e) in enumerate(C.cs):
-                _add_dense(ar, C.ch[i][j], M[a - C.r0:b - C.r0, c - C.c0:e - C.c0])
 
 
 def _prod_lr(ar, A, B):
@@ -257,7 +356,7 @@ def _prod_lr(ar, A, B):
         _flush(ar, B)
         return _mul(ar, A, B.u), B.v
     if isinstance(A, Dense) and isinstance(B, Dense):
-        return _dense_to_lr(ar, A.a @ B.a)
+        return A.a, B.a.mH          # untruncated: inner dimension columns
     # at least one hierarchical operand: per child block, then agglomerate with one truncation
     m, n = A.r1 - A.r0, B.c1 - B.c0
     Rp, Cp = _parts(A, True), _parts(B, False)
@@ -279,7 +378,8 @@ def _prod_lr(ar, A, B):
         dev = _dev_of(A)
         z = torch.zeros((m, 0), dtype=torch.complex128, device=dev)
         return z, torch.zeros((n, 0), dtype=torch.complex128, device=dev)
-    return _trunc(ar, torch.cat(us, 1), torch.cat(vs, 1))
+    U, V = torch.cat([t.mT for t in us], 0).mT, torch.cat([t.mT for t in vs], 0).mT
+    return _trunc(ar, U, V) if U.shape[1] > _AGGLO_MAX else (U, V)
 
 
 def _addmul(ar, C, A, B, alpha=-1.0):
@@ -320,7 +420,7 @@ def _addmul(ar, C, A, B, alpha=-1.0):
         return
     u, v = _prod_lr(ar, A, B)
     if u.shape[1]:
-        C.pend.append((alpha * u, v))
+        _pend(ar, C, alpha * u, v)
 
 
 # --------------------------------------------------------------------------------------------
@@ -354,6 +454,7 @@ def _lu(ar, x, path):
         for i in range(k + 1, p):
             for j in range(k + 1, p):
                 _addmul(ar, x.ch[i][j], x.ch[i][k], x.ch[k][j], -1.0)
+        _flush_batch(ar, [x.ch[i][j] for i in range(k + 1, p) for j in range(k + 1, p)])
 
 
 def _lsolve(ar, L, X):
@@ -411,12 +512,14 @@ def _solve_lower(ar, L, B):
         if B.rank:
             B.u = _lsolve(ar, L, B.u)
     elif isinstance(L, Sub):
-        p = len(L.rs)
-        for j in range(len(B.cs)):
-            for k in range(p):
+        p, q = len(L.rs), len(B.cs)
+        for k in range(p):
+            for j in range(q):
                 _solve_lower(ar, L.ch[k][k], B.ch[k][j])
+            for j in range(q):
                 for i in range(k + 1, p):
                     _addmul(ar, B.ch[i][j], L.ch[i][k], B.ch[k][j], -1.0)
+            _flush_batch(ar, [B.ch[i][j] for i in range(k + 1, p) for j in range(q)])
     else:
         for j in range(len(B.cs)):
             _solve_lower(ar, L, B.ch[0][j])
@@ -431,12 +534,14 @@ def _solve_upper_right(ar, U, B):
         if B.rank:
             B.v = _rsolve(ar, U, B.v.mH).mH
     elif isinstance(U, Sub):
-        p = len(U.cs)
-        for i in range(len(B.rs)):
-            for k in range(p):
+        p, q = len(U.cs), len(B.rs)
+        for k in range(p):
+            for i in range(q):
                 _solve_upper_right(ar, U.ch[k][k], B.ch[i][k])
+            for i in range(q):
                 for j in range(k + 1, p):
                     _addmul(ar, B.ch[i][j], B.ch[i][k], U.ch[k][j], -1.0)
+            _flush_batch(ar, [B.ch[i][j] for i in range(q) for j in range(k + 1, p)])
     else:
         for i in range(len(B.rs)):
             _solve_upper_right(ar, U, B.ch[i][0])
@@ -467,15 +572,6 @@ def _umul(ar, U, X):
             acc = acc + _mul(ar, U.ch[i][j], X[c - U.r0:e - U.r0])
         out[a - U.r0:b - U.r0] = acc
     return out
-
-
-def _flush_all(ar, x):
-    if isinstance(x, LowRank):
-        _flush(ar, x)
-    elif isinstance(x, Sub):
-        for row in x.ch:
-            for c in row:
-                _flush_all(ar, c)
 
 
 def _walk(x):
@@ -591,7 +687,7 @@ def formatted_addmul(target, a, b, eps_lu, rule="frobenius"):
         raise ValueError("formatted_addmul: non-conformal ranges")
     ar = Arith(eps_lu, rule)
     _addmul(ar, target, a, b, 1.0)
-    _flush_all(ar, target)
+    _flush_batch(ar, [target])
     return target
 
 
@@ -653,12 +749,14 @@ def hlu(h, eps_lu, rule="frobenius", block_tree=None):
     t1 = time.perf_counter()
     ar = Arith(float(eps_lu), rule)
     _lu(ar, root, ())
-    _flush_all(ar, root)
+    _flush_batch(ar, [root])
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     f = LUFactors(lower=_Tri(root, True), upper=_Tri(root, False), eps_lu=float(eps_lu), d=h.d,
                   perm=np.asarray(h.perm), n=h.d * h.n_points)
-    f.stats = {"copy_s": t1 - t0, "factor_s": t2 - t1, "n_truncations": ar.n_trunc, "n_getrf": ar.n_getrf,
+    f.stats = {"copy_s": t1 - t0, "factor_s": t2 - t1, "n_truncations": ar.n_trunc, "n_truncate_calls": ar.n_trunc_calls, "truncate_s": ar.t_trunc,
+               "truncate_kmax_p50_p90_max": [int(q) for q in np.percentile(ar.k_hist, [50, 90, 100])] if ar.k_hist else [],
+               "n_getrf": ar.n_getrf,
                "max_rank": ar.max_rank}
     return f
 

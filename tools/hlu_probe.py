@@ -30,6 +30,12 @@ for eps in epss:
     res = np.linalg.norm(hmx.matvec(H, x) - b) / np.linalg.norm(b)
     print(f"{tag}@{n} dofs {pb.d * n} eps_lu {eps:g}: hlu {t1 - t0:.3f} s (copy {f.stats['copy_s']:.3f}, "
           f"factor {f.stats['factor_s']:.3f}), solve {1e3 * (t2 - t1):.1f} ms, consistency {cons:.2e}, "
-          f"residual {res:.2e}, truncations {f.stats['n_truncations']}, getrf {f.stats['n_getrf']}, "
+          f"residual {res:.2e}, truncations {f.stats["n_truncations"]} in {f.stats["n_truncate_calls"]} calls, getrf {f.stats['n_getrf']}, "
           f"max rank {f.stats['max_rank']}, storage {f.storage() * 16 / 1e6:.1f} MB "
-          f"(H {rep.n_stored * 16 / 1e6:.1f} MB)", flush=True)
+          f"(H {rep.n_stored * 16 / 1e6:.1f} MB); truncate calls {f.stats['truncate_s']:.3f} s, "
+          f"call K max p50/p90/max {f.stats['truncate_kmax_p50_p90_max']}", flush=True)
+    if len(sys.argv) > 4 and eps == epss[-1]:
+        import cProfile
+        import pstats
+        cProfile.run("HL.hlu(H, eps)", "/tmp/hlu.prof")
+        pstats.Stats("/tmp/hlu.prof").sort_stats("tottime").print_stats(15)
