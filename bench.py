@@ -46,6 +46,8 @@ def parse():
     ap.add_argument("--no-solve", action="store_true", help="skip the T65k time-to-solve run")
     ap.add_argument("--no-estimate", action="store_true", help="skip the delta_{H,F} estimator timing")
     ap.add_argument("--solve-config", default="T65k")
+    ap.add_argument("--no-direct", action="store_true", help="skip the H-LU direct-solve section")
+    ap.add_argument("--direct-config", default="H4k")
     ap.add_argument("--extra-configs", default="U131k,U8k,H4k",
                     help="other BASELINE configs measured briefly (assembly + 20 matvecs); '' to skip")
     ap.add_argument("--shard", action="store_true",
@@ -253,6 +255,67 @@ def time_to_solve(tag, device):
            "matvec_bytes": st["matvec_bytes"], "aca_passes": st["aca_passes"],
            "free_gb_before_assembly": free_before / 1e9}
     del H
+    return out
+
+
+def direct_solve(tag, device, eps_lu=1e-4, cpu=True):
+    """H-LU of the assembled H with eps_LU and one
+    triangular solve on the device (a second factorisation is timed: the first call warms
+    cuSOLVER / the allocator), GMRES on the same H for comparison, and the oracle's H-LU of the same
+    leaf factors on one host core as the section's CPU baseline."""
+    import torch
+
+    import paper_1706_09384_b200 as hmx
+    from paper_1706_09384_b200 import hierarchical_lu as HL
+    from paper_1706_09384_b200.configs import WORKLOADS
+
+    w = WORKLOADS[tag]
+    cloud = hmx.make_geometry("sphere", w.n_points, 1.0, d=w.d)
+    ct = hmx.build_cluster_tree(cloud, w.n_leaf)
+    bt = hmx.build_block_tree(ct, ct, w.eta)
+    H, rep = hmx.assemble(w.spec(), cloud, ct, bt, hmx.ACAConfig(eps_aca=w.eps), device=device)
+    n = w.d * w.n_points
+    rng = np.random.default_rng(SEED)
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    HL.hlu(H, eps_lu)  # warm-up
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    f = HL.hlu(H, eps_lu)
+    t_lu = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    x = HL.triangular_solve(f, b)
+    t_sv = time.perf_counter() - t0
+    y = hmx.matvec(H, b)
+    cons = float(np.linalg.norm(HL.lu_matvec(f, b) - y) / np.linalg.norm(y))
+    res = float(np.linalg.norm(hmx.matvec(H, x) - b) / np.linalg.norm(b))
+    t0 = time.perf_counter()
+    g = hmx.solve_gmres(H, b, hmx.GmresConfig(tol=1e-4, restart=50))
+    t_gm = time.perf_counter() - t0
+    out = {"workload": f"{tag} H-LU (eps_LU {eps_lu:g}) + triangular solve", "dofs": n,
+           "hlu_s": t_lu, "solve_ms": 1e3 * t_sv, "consistency_LU_vs_AH": cons, "residual": res,
+           "rel_diff_vs_gmres": float(np.linalg.norm(g.x - x) / np.linalg.norm(x)),
+           "gmres_s": t_gm, "gmres_iterations": g.iters,
+           "factor_storage_MB": f.storage() * 16 / 1e6, "h_storage_MB": rep.n_stored * 16 / 1e6,
+           "truncations": f.stats["n_truncations"], "truncate_calls": f.stats["n_truncate_calls"],
+           "truncate_s": f.stats["truncate_s"], "dense_leaf_lu": f.stats["n_getrf"],
+           "max_rank": f.stats["max_rank"]}
+    if cpu:
+        from threadpoolctl import threadpool_limits
+
+        from oracle import hlu as OL
+
+        payload = [H.block(i) for i in range(len(H.table))]
+        payload = [p if isinstance(p, np.ndarray) else (p.u, p.v) for p in payload]
+        with threadpool_limits(1):
+            root = OL.from_payload(bt, w.d, payload)
+            t0 = time.perf_counter()
+            OL.hlu(root, eps_lu)
+            t_cpu = time.perf_counter() - t0
+        out["cpu_baseline"] = {"hlu_s": t_cpu, "cores": 1, "kind": "port",
+                               "sample": "oracle/hlu.py (numpy / LAPACK QR + SVD truncations) on the same leaf factors, "
+                                         "one thread"}
+    del f, H
+    torch.cuda.empty_cache()
     return out
 
 
@@ -514,6 +577,11 @@ def hmx_arm(args):
         torch.cuda.empty_cache()
         torch.cuda.synchronize()
         line["time_to_solve"] = time_to_solve(args.solve_config, local)
+    if not args.no_direct:
+        try:
+            line["direct_solve"] = direct_solve(args.direct_config, local, cpu=(rank == 0 and ws == 1))
+        except Exception as exc:  # reported, never fatal for the headline line
+            line["direct_solve"] = {"failed": repr(exc)}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             r = run_cpu(args.config, steps=50, warmup=1, budget_s=15.0)

@@ -32,6 +32,7 @@ upper blocks plus the unit-lower / upper factors of the diagonal leaves of the
 same tree.
 """
 
+import os
 import time
 from dataclasses import dataclass, field
 
@@ -76,10 +77,33 @@ class LowRank:
 
 
 class Sub:
-    __slots__ = ("r0", "r1", "c0", "c1", "rs", "cs", "ch")
+    __slots__ = ("r0", "r1", "c0", "c1", "rs", "cs", "ch", "fin", "dc")
 
     def __init__(self, r0, r1, c0, c1, rs, cs, ch):
         self.r0, self.r1, self.c0, self.c1, self.rs, self.cs, self.ch = r0, r1, c0, c1, rs, cs, ch
+        self.fin = False   # a finished L / U factor block: never modified again
+        self.dc = None     # its dense image, built on first use as a product operand
+
+
+_DC_MAX = 1 << 22      # largest finished block (entries) kept as a dense operand image (64 MB)
+
+
+def _finalize(x):
+    if isinstance(x, Sub):
+        x.fin = True
+        for row in x.ch:
+            for c in row:
+                _finalize(c)
+
+
+def _dense_image(ar, x):
+    """Dense image of a finished hierarchical block (one GEMM per product instead of a recursion
+    over its leaves), or None."""
+    if not x.fin or (x.r1 - x.r0) * (x.c1 - x.c0) > _DC_MAX:
+        return None
+    if x.dc is None:
+        x.dc = _dense(ar, x)
+    return x.dc
 
 
 @dataclass
@@ -115,6 +139,9 @@ def _trank(s, eps, rule):
 
 _PEND_FLUSH = 400     # pending columns on one low-rank target before it is truncated early
 _AGGLO_MAX = 512      # agglomerated product columns before an intermediate truncation
+# pairs whose kernel problem would have more columns than this are truncated by cuSOLVER QR + SVD
+# instead (the one-CTA eigen-solve of a K x K problem is latency-bound, O(K) dependent phases)
+_CUSOLVER_K = int(os.environ.get("HMX_HLU_CUSOLVER_K", "1021"))
 _TRULES = {"frobenius": 0, "spectral": 1}
 
 
@@ -161,10 +188,13 @@ def _kernel_batch(ar, items):
 
 
 def _dense_form(u, v):
-    """U V^H as the pair (U V^H, I): the V side is orthonormal, so the kernel's Cholesky is exact."""
+    """U V^H as the pair (U V^H, I) -- or, when U has fewer rows, its adjoint (V U^H, I) with the
+    result swapped back: the V side is orthonormal, so the kernel's Cholesky is exact.
+    Returns (pair, swapped)."""
     torch = _torch()
-    n = v.shape[0]
-    return u @ v.mH, torch.eye(n, dtype=u.dtype, device=u.device)
+    if u.shape[0] < v.shape[0]:
+        return (v @ u.mH, torch.eye(u.shape[0], dtype=u.dtype, device=u.device)), True
+    return (u @ v.mH, torch.eye(v.shape[0], dtype=u.dtype, device=u.device)), False
 
 
 def _truncate_batch(ar, items):
@@ -176,29 +206,52 @@ def _truncate_batch(ar, items):
     if not items:
         return []
     res = [None] * len(items)
-    sub, idx = [], []
+    sub, idx, swp = [], [], []
     for i, (u, v) in enumerate(items):
         if u.shape[1] == 0:
             res[i] = (u, v)
             continue
         ar.n_trunc += 1
-        sub.append(_dense_form(u, v) if u.shape[1] >= v.shape[0] else (u, v))
+        if min(u.shape[1], u.shape[0], v.shape[0]) > _CUSOLVER_K:
+            res[i] = _trunc_cusolver(ar, u, v)
+            ar.max_rank = max(ar.max_rank, res[i][0].shape[1])
+            continue
+        if u.shape[1] >= min(u.shape[0], v.shape[0]):
+            pair, sw = _dense_form(u, v)
+        else:
+            pair, sw = (u, v), False
+        sub.append(pair)
+        swp.append(sw)
         idx.append(i)
+    dense_done = [False] * len(idx)
     while idx:
         out = _kernel_batch(ar, sub)
-        redo, ridx = [], []
-        for i, s_, o in zip(idx, sub, out):
+        redo, ridx, rswp, rdone = [], [], [], []
+        for i, s_, sw, dd, o in zip(idx, sub, swp, dense_done, out):
             if o is not None:
-                res[i] = o
+                res[i] = (o[1], o[0]) if sw else o
                 ar.max_rank = max(ar.max_rank, o[0].shape[1])
-            elif s_[0].shape[1] < s_[1].shape[0] and s_[1].shape[0] <= 1020:
-                redo.append(_dense_form(*items[i]))
+            elif not dd and min(items[i][0].shape[0], items[i][1].shape[0]) <= 1020:
+                pair, sw2 = _dense_form(*items[i])
+                redo.append(pair)
+                rswp.append(sw2)
                 ridx.append(i)
+                rdone.append(True)
             else:
                 raise FloatingPointError("hmx_truncate_batch: rank-deficient factor pair with no "
-                                         "well-conditioned form (V rows > 1020)")
-        sub, idx = redo, ridx
+                                         "well-conditioned form (both sides above 1020 rows)")
+        sub, idx, swp, dense_done = redo, ridx, rswp, rdone
     return res
+
+
+def _trunc_cusolver(ar, u, v):
+    torch = _torch()
+    qu, ru = torch.linalg.qr(u)
+    qv, rv = torch.linalg.qr(v)
+    p, s, lh = torch.linalg.svd(ru @ rv.mH, full_matrices=False)
+    r = _trank(s.cpu().numpy(), ar.eps, ar.rule)
+    root = s[:r].sqrt().to(u.dtype)
+    return (qu @ p[:, :r]) * root, (qv @ lh.mH[:, :r]) * root
 
 
 def _trunc(ar, u, v):
@@ -259,6 +312,9 @@ def _mul(ar, x, X):
     if isinstance(x, LowRank):
         _flush(ar, x)
         return x.u @ (x.v.mH @ X)
+    dc = _dense_image(ar, x)
+    if dc is not None:
+        return dc @ X
     out = X.new_zeros((x.r1 - x.r0, X.shape[1]))
     for i, (a, b) in enumerate(x.rs):
         for j, (c, e) in enumerate(x.cs):
@@ -273,6 +329,9 @@ def _mulh(ar, x, X):
     if isinstance(x, LowRank):
         _flush(ar, x)
         return x.v @ (x.u.mH @ X)
+    dc = _dense_image(ar, x)
+    if dc is not None:
+        return dc.mH @ X
     out = X.new_zeros((x.c1 - x.c0, X.shape[1]))
     for i, (a, b) in enumerate(x.rs):
         for j, (c, e) in enumerate(x.cs):
@@ -287,6 +346,8 @@ def _dense(ar, x):
     if isinstance(x, LowRank):
         _flush(ar, x)
         return x.u @ x.v.mH
+    if x.dc is not None:
+        return x.dc
     out = torch.zeros((x.r1 - x.r0, x.c1 - x.c0), dtype=torch.complex128, device=_dev_of(x))
     for i, (a, b) in enumerate(x.rs):
         for j, (c, e) in enumerate(x.cs):
@@ -451,6 +512,9 @@ def _lu(ar, x, path):
             _solve_lower(ar, x.ch[k][k], x.ch[k][j])
         for i in range(k + 1, p):
             _solve_upper_right(ar, x.ch[k][k], x.ch[i][k])
+        for j in range(k + 1, p):
+            _finalize(x.ch[k][j])
+            _finalize(x.ch[j][k])
         for i in range(k + 1, p):
             for j in range(k + 1, p):
                 _addmul(ar, x.ch[i][j], x.ch[i][k], x.ch[k][j], -1.0)

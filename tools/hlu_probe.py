@@ -13,7 +13,8 @@ from paper_1706_09384_b200 import hierarchical_lu as HL  # noqa: E402
 from tests._problems import Problem  # noqa: E402
 
 tag, n = sys.argv[1], int(sys.argv[2])
-epss = [float(e) for e in sys.argv[3:]] or [1e-4]
+prof = "p" in sys.argv[3:]
+epss = [float(e) for e in sys.argv[3:] if e != "p"] or [1e-4]
 pb = Problem(tag, n)
 H, rep = pb.device_h()
 b = pb.rhs(0)
@@ -34,7 +35,7 @@ for eps in epss:
           f"max rank {f.stats['max_rank']}, storage {f.storage() * 16 / 1e6:.1f} MB "
           f"(H {rep.n_stored * 16 / 1e6:.1f} MB); truncate calls {f.stats['truncate_s']:.3f} s, "
           f"call K max p50/p90/max {f.stats['truncate_kmax_p50_p90_max']}", flush=True)
-    if len(sys.argv) > 4 and eps == epss[-1]:
+    if prof and eps == epss[-1]:
         import cProfile
         import pstats
         cProfile.run("HL.hlu(H, eps)", "/tmp/hlu.prof")
