@@ -193,10 +193,44 @@ def run_cpu(tag, steps, warmup, budget_s=None):
             if budget_s is not None and time.perf_counter() - t0 > budget_s:
                 break
         dt = time.perf_counter() - t0
+    pairs = sum((r1 - r0) * (c1 - c0) if k == 0 else int(st) * ((r1 - r0) + (c1 - c0))
+                for (k, r0, r1, c0, c1), st in zip(tab, oh.steps))
     return {"value": bytes_ * done / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
             "sample": f"{desc}; oracle factors (numpy ACA + QR/SVD recompression); {done} threaded "
                       f"oracle H-matvecs of {bytes_ / 1e9:.3f} GB each", "ms_per_step": dt / done * 1e3,
-            "steps": done, "setup_s": t_setup}
+            "steps": done, "setup_s": t_setup,
+            "assembly": {"pooled_s": t_setup, "workers": cores, "pairs": int(pairs),
+                         "green_entries_per_s": d * d * pairs / t_setup,
+                         "sample": f"{desc}, leaf-parallel process pool (SPEC.md:456)"}}
+
+
+def cpu_end_to_end(tag="H4k"):
+    """The reference's own CPU-runnable configuration (BASELINE config 1) end to end on the host:
+    oracle assembly in a process pool, one H-matvec, GMRES(50, 1e-4) -- SURVEY 8(d)'s CPU
+    assembly / matvec / GMRES baseline at full size."""
+    from threadpoolctl import threadpool_limits
+
+    from oracle import hmatrix as OH
+    from oracle import solve as OS
+    from tests._problems import Problem
+
+    cores = os.cpu_count() or 1
+    pb = Problem(tag)
+    t0 = time.perf_counter()
+    oh = pb.oracle_h(workers=cores)
+    t_asm = time.perf_counter() - t0
+    b = pb.rhs(SEED)
+    with threadpool_limits(cores):
+        t0 = time.perf_counter()
+        for _ in range(5):
+            OH.matvec(oh, b)
+        t_mv = (time.perf_counter() - t0) / 5
+        t0 = time.perf_counter()
+        _, it, _, conv = OS.gmres(lambda v: OH.matvec(oh, v), b, 1e-4, 50, 1000)
+        t_gm = time.perf_counter() - t0
+    return {"workload": tag, "cores": cores, "kind": "port", "assembly_pooled_s": t_asm, "matvec_ms": 1e3 * t_mv,
+            "gmres_s": t_gm, "gmres_iterations": it, "converged": bool(conv),
+            "time_to_solve_s": t_asm + t_gm}
 
 
 def reference_arm(args):
@@ -360,6 +394,14 @@ def config_summary(tag, device, dfma_tflops, steps=20):
            "matvec_ms": mv_ms, "matvec_GBps": st["matvec_bytes"] / (mv_ms * 1e-3) / 1e9,
            "matvec_bytes": st["matvec_bytes"], "l2_resident": st["matvec_bytes"] < 100e6,
            "max_rank_after": rep.max_rank_after, "tau": rep.tau}
+    if "gmres" in w.runs:
+        rng = np.random.default_rng(SEED)
+        b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        t0 = time.perf_counter()
+        g = hmx.solve_gmres(H, b, hmx.GmresConfig(tol=1e-4, restart=50))
+        out["gmres_s"] = time.perf_counter() - t0
+        out["gmres_iterations"] = g.iters
+        out["time_to_solve_s"] = t + out["gmres_s"]
     del H
     return out
 
@@ -587,6 +629,8 @@ def hmx_arm(args):
             r = run_cpu(args.config, steps=50, warmup=1, budget_s=15.0)
             line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
             line["cpu_baseline"]["ms_per_step"] = r["ms_per_step"]
+            line["cpu_baseline"]["assembly"] = r["assembly"]
+            line["cpu_baseline"]["end_to_end_H4k"] = cpu_end_to_end("H4k")
         except Exception as exc:  # the baseline is reported, never fatal
             line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
                                     "sample": f"failed: {exc!r}"}

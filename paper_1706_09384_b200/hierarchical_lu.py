@@ -202,7 +202,8 @@ def _truncate_batch(ar, items):
     through ``hmx_truncate_batch`` (Gram pair, scaled Cholesky, Hermitian eigen-solver, truncation
     rule, U' = U W_U, V' = V W_V -- the assembly's recompression kernels), one call per batch.
     A pair with at least as many columns as V has rows, or whose V turns out numerically
-    rank-deficient, is re-submitted as (U V^H, I)."""
+    rank-deficient, is re-submitted as (U V^H, I) (or its adjoint); cuSOLVER QR + SVD only when
+    both sides exceed the kernel's 1020-column limit."""
     if not items:
         return []
     res = [None] * len(items)
@@ -238,8 +239,8 @@ def _truncate_batch(ar, items):
                 ridx.append(i)
                 rdone.append(True)
             else:
-                raise FloatingPointError("hmx_truncate_batch: rank-deficient factor pair with no "
-                                         "well-conditioned form (both sides above 1020 rows)")
+                # both sides above the kernel's 1020 limit: Householder QR + SVD (cuSOLVER)
+                res[i] = _trunc_cusolver(ar, *items[i])
         sub, idx, swp, dense_done = redo, ridx, rswp, rdone
     return res
 
