@@ -148,3 +148,20 @@ def test_source_h_unchanged():
     y0 = hmx.matvec(H, b)
     HL.hlu(H, 1e-4)
     assert np.array_equal(hmx.matvec(H, b), y0)
+
+
+def test_single_leaf_is_dense_lu():
+    """a 1-leaf H-matrix reduces to the pivoted dense LU (machine-precision residual)."""
+    from dataclasses import replace
+
+    pb = Problem("U8k", 40)
+    w = replace(pb.w, n_leaf=64)
+    cl = hmx.make_geometry("sphere", 40, 1.0, d=3)
+    ct = hmx.build_cluster_tree(cl, w.n_leaf)
+    bt = hmx.build_block_tree(ct, ct, w.eta)
+    assert len(bt.table) == 1
+    H, _ = hmx.assemble(w.spec(), cl, ct, bt, hmx.ACAConfig(eps_aca=w.eps))
+    b = _rand(120, 12)
+    x, f = hmx.solve_direct(H, b, 1e-4)
+    assert f.stats["n_getrf"] == 1
+    assert np.linalg.norm(hmx.matvec(H, x) - b) <= 1e-13 * np.linalg.norm(b)
