@@ -142,10 +142,13 @@ _AGGLO_MAX = 512      # agglomerated product columns before an intermediate trun
 # pairs whose kernel problem would have more columns than this are truncated by cuSOLVER QR + SVD
 # instead (the one-CTA eigen-solve of a K x K problem is latency-bound, O(K) dependent phases)
 _CUSOLVER_K = int(os.environ.get("HMX_HLU_CUSOLVER_K", "1021"))
+# dense-form pairs with more columns than this are truncated through a _SKETCH_L-column range sketch
+_SKETCH_K = int(os.environ.get("HMX_HLU_SKETCH_K", "112"))
+_SKETCH_L = 96
 _TRULES = {"frobenius": 0, "spectral": 1}
 
 
-def _kernel_batch(ar, items):
+def _kernel_batch(ar, items, eps=None):
     """One ``hmx_truncate_batch`` call: list of (U, V) -> list of (U', V') or None for items whose
     V was numerically rank-deficient (regularised Cholesky; not formed)."""
     torch = _torch()
@@ -174,7 +177,8 @@ def _kernel_batch(ar, items):
     t0 = time.perf_counter()
     _lib.check(_lib.lib().hmx_truncate_batch(_lib.context(dev.index or 0), n, _lib.ptr(dm), _lib.ptr(dn),
                                               _lib.ptr(K), _lib.ptr(ptr[0]), _lib.ptr(ptr[1]), _lib.ptr(ptr[2]),
-                                              _lib.ptr(ptr[3]), float(ar.eps), _TRULES[ar.rule],
+                                              _lib.ptr(ptr[3]), float(ar.eps if eps is None else eps),
+                                              _TRULES[ar.rule],
                                               _lib.ptr(ranks), _lib.ptr(flags)), "hmx_truncate_batch")
     ar.t_trunc += time.perf_counter() - t0
     res = []
@@ -206,8 +210,10 @@ def _truncate_batch(ar, items):
     both sides exceed the kernel's 1020-column limit."""
     if not items:
         return []
+    torch = _torch()
     res = [None] * len(items)
     sub, idx, swp = [], [], []
+    sk_x, sk_meta = [], []
     for i, (u, v) in enumerate(items):
         if u.shape[1] == 0:
             res[i] = (u, v)
@@ -219,11 +225,30 @@ def _truncate_batch(ar, items):
             continue
         if u.shape[1] >= min(u.shape[0], v.shape[0]):
             pair, sw = _dense_form(u, v)
+            if pair[1].shape[0] > _SKETCH_K and ar.rule == "frobenius":
+                sk_x.append(pair[0])
+                sk_meta.append((i, sw))
+                continue
         else:
             pair, sw = (u, v), False
         sub.append(pair)
         swp.append(sw)
         idx.append(i)
+    if sk_x:
+        # X = Q (Q^H X) on a sketched range basis Q, then the (X^H Q, Q) pair: its V side is
+        # orthonormal and it has at most _SKETCH_L columns (the one-CTA eigen-solve stays small)
+        for X, Q, (i, sw) in zip(sk_x, _sketch_basis(ar, sk_x), sk_meta):
+            if Q is None:   # sketch saturated: the full dense form
+                sub.append((X, torch.eye(X.shape[1], dtype=X.dtype, device=X.device)))
+                swp.append(sw)
+            elif Q.shape[1] == 0:
+                u, v = items[i]
+                res[i] = (u[:, :0], v[:, :0])
+                continue
+            else:
+                sub.append((X.mH @ Q, Q))
+                swp.append(not sw)   # kernel (P, R): X ~ R P^H
+            idx.append(i)
     dense_done = [False] * len(idx)
     while idx:
         out = _kernel_batch(ar, sub)
@@ -243,6 +268,35 @@ def _truncate_batch(ar, items):
                 res[i] = _trunc_cusolver(ar, *items[i])
         sub, idx, swp, dense_done = redo, ridx, rswp, rdone
     return res
+
+
+def _sketch_basis(ar, Xs):
+    """Orthonormal bases of the ranges of the dense X (a x K') from a seeded Gaussian sketch
+    Y = X Omega (K' x _SKETCH_L): the (Y, I) pairs are truncated at max(eps / 10, 1e-8) in one
+    kernel call and the orthogonal columns A = Y W_U normalised.  None where the sketch saturates
+    (kept rank above _SKETCH_L - 8: the range may be larger than the sketch)."""
+    torch = _torch()
+    pairs = []
+    for X in Xs:
+        g = torch.Generator(device=X.device)
+        g.manual_seed(0x5EED + 7 * X.shape[0] + X.shape[1])
+        om = torch.randn((X.shape[1], _SKETCH_L), dtype=X.dtype, device=X.device, generator=g)
+        pairs.append((X @ om, torch.eye(_SKETCH_L, dtype=X.dtype, device=X.device)))
+    out = _kernel_batch(ar, pairs, eps=max(0.1 * ar.eps, 1e-8))
+    qs = []
+    for o in out:
+        if o is None or o[0].shape[1] > _SKETCH_L - 8:
+            qs.append(None)
+        elif o[0].shape[1] == 0:
+            qs.append(o[0])
+        else:
+            # A = Y W_U has orthogonal columns of norms sqrt(s_i), but the Gram route leaves their
+            # trailing directions orthogonal only to ~u s_1 / s_q: one Cholesky-QR pass on the
+            # normalised (well-conditioned) columns restores orthonormality
+            a = o[0] / o[0].norm(dim=0, keepdim=True)
+            r = torch.linalg.cholesky(a.mH @ a).mH
+            qs.append(torch.linalg.solve_triangular(r, a, upper=True, left=False))
+    return qs
 
 
 def _trunc_cusolver(ar, u, v):

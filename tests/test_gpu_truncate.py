@@ -46,3 +46,27 @@ def test_truncate_batch_matches_svd(rule):
         nA = max(np.linalg.norm(A), 1e-300)
         tol = 3 * eps if rule == "frobenius" else 3 * eps * np.sqrt(min(dm, dn))
         assert np.linalg.norm(B - A) <= tol * nA + 1e-300, (dm, dn, K, np.linalg.norm(B - A) / nA)
+
+
+def test_sketched_dense_form():
+    """Dense-form pairs above the sketch threshold (K >= min(dm, dn) > 112) go through the
+    range sketch: same truncation rank (+-1) and error as the SVD truncation, also when the
+    numerical rank is near the sketch width and for the adjoint orientation."""
+    rng = np.random.default_rng(1)
+    eps = 1e-4
+    cases = [(150, 200, 260, 30), (260, 140, 300, 60), (200, 200, 400, 85), (130, 144, 232, 5)]
+    items, ref = [], []
+    for dm, dn, K, r in cases:
+        s = np.exp(-np.arange(K) / (r / 4.0))   # singular-value decay: numerical rank ~ r
+        U = (rng.standard_normal((dm, K)) + 1j * rng.standard_normal((dm, K))) * s
+        V = rng.standard_normal((dn, K)) + 1j * rng.standard_normal((dn, K))
+        items.append((torch.as_tensor(U, device="cuda"), torch.as_tensor(V, device="cuda")))
+        ref.append(U @ V.conj().T)
+    ar = HL.Arith(eps)
+    out = HL._truncate_batch(ar, items)
+    for (u, v), A, c in zip(out, ref, cases):
+        sv = np.linalg.svd(A, compute_uv=False)
+        r_ref = truncation_rank(sv, eps, "frobenius")
+        assert abs(u.shape[1] - r_ref) <= 1, (c, u.shape[1], r_ref)
+        err = np.linalg.norm((u @ v.mH).cpu().numpy() - A) / np.linalg.norm(A)
+        assert err <= 1.5 * eps, (c, err)
