@@ -142,9 +142,9 @@ _AGGLO_MAX = 512      # agglomerated product columns before an intermediate trun
 # pairs whose kernel problem would have more columns than this are truncated by cuSOLVER QR + SVD
 # instead (the one-CTA eigen-solve of a K x K problem is latency-bound, O(K) dependent phases)
 _CUSOLVER_K = int(os.environ.get("HMX_HLU_CUSOLVER_K", "1021"))
-# dense-form pairs with more columns than this are truncated through a _SKETCH_L-column range sketch
+# pairs whose kernel problem would exceed this many columns go through a _SKETCH_L-column range sketch
 _SKETCH_K = int(os.environ.get("HMX_HLU_SKETCH_K", "112"))
-_SKETCH_L = 96
+_SKETCH_L = 112
 _TRULES = {"frobenius": 0, "spectral": 1}
 
 
@@ -223,31 +223,29 @@ def _truncate_batch(ar, items):
             res[i] = _trunc_cusolver(ar, u, v)
             ar.max_rank = max(ar.max_rank, res[i][0].shape[1])
             continue
-        if u.shape[1] >= min(u.shape[0], v.shape[0]):
-            pair, sw = _dense_form(u, v)
-            if pair[1].shape[0] > _SKETCH_K and ar.rule == "frobenius":
-                sk_x.append(pair[0])
-                sk_meta.append((i, sw))
-                continue
-        else:
-            pair, sw = (u, v), False
-        sub.append(pair)
-        swp.append(sw)
+        if min(u.shape[1], u.shape[0], v.shape[0]) > _SKETCH_K and ar.rule == "frobenius":
+            sk_x.append((u, v))
+            sk_meta.append(i)
+            continue
+        sub.append(_direct_form(u, v))
+        swp.append(sub[-1][1])
+        sub[-1] = sub[-1][0]
         idx.append(i)
     if sk_x:
-        # X = Q (Q^H X) on a sketched range basis Q, then the (X^H Q, Q) pair: its V side is
-        # orthonormal and it has at most _SKETCH_L columns (the one-CTA eigen-solve stays small)
-        for X, Q, (i, sw) in zip(sk_x, _sketch_basis(ar, sk_x), sk_meta):
-            if Q is None:   # sketch saturated: the full dense form
-                sub.append((X, torch.eye(X.shape[1], dtype=X.dtype, device=X.device)))
+        # U V^H = Q (Q^H U) V^H on a sketched range basis Q, truncated as the (V (U^H Q), Q) pair:
+        # its V side is orthonormal and it has at most _SKETCH_L columns (the one-CTA eigen-solve
+        # stays small); kernel result (P, R) means U V^H ~ R P^H
+        for (u, v), Q, i in zip(sk_x, _sketch_basis(ar, sk_x), sk_meta):
+            if Q is None:   # sketch saturated: the direct (possibly dense) form
+                pair, sw = _direct_form(u, v)
+                sub.append(pair)
                 swp.append(sw)
             elif Q.shape[1] == 0:
-                u, v = items[i]
                 res[i] = (u[:, :0], v[:, :0])
                 continue
             else:
-                sub.append((X.mH @ Q, Q))
-                swp.append(not sw)   # kernel (P, R): X ~ R P^H
+                sub.append((v @ (u.mH @ Q), Q))
+                swp.append(True)
             idx.append(i)
     dense_done = [False] * len(idx)
     while idx:
@@ -270,18 +268,26 @@ def _truncate_batch(ar, items):
     return res
 
 
-def _sketch_basis(ar, Xs):
-    """Orthonormal bases of the ranges of the dense X (a x K') from a seeded Gaussian sketch
-    Y = X Omega (K' x _SKETCH_L): the (Y, I) pairs are truncated at max(eps / 10, 1e-8) in one
-    kernel call and the orthogonal columns A = Y W_U normalised.  None where the sketch saturates
-    (kept rank above _SKETCH_L - 8: the range may be larger than the sketch)."""
+def _direct_form(u, v):
+    """(pair, swapped) submitted to the kernel without sketching: (U, V) itself, or the dense
+    form when U V^H has no more columns than rows on its smaller side."""
+    if u.shape[1] >= min(u.shape[0], v.shape[0]):
+        return _dense_form(u, v)
+    return (u, v), False
+
+
+def _sketch_basis(ar, pairs_in):
+    """Orthonormal bases of the ranges of U V^H (dm x dn) from a seeded Gaussian sketch
+    Y = U (V^H Omega) (Omega dn x _SKETCH_L): the (Y, I) pairs are truncated at max(eps / 10, 1e-8)
+    in one kernel call and the orthogonal columns A = Y W_U normalised.  None where the sketch
+    saturates (kept rank above _SKETCH_L - 8: the range may be larger than the sketch)."""
     torch = _torch()
     pairs = []
-    for X in Xs:
-        g = torch.Generator(device=X.device)
-        g.manual_seed(0x5EED + 7 * X.shape[0] + X.shape[1])
-        om = torch.randn((X.shape[1], _SKETCH_L), dtype=X.dtype, device=X.device, generator=g)
-        pairs.append((X @ om, torch.eye(_SKETCH_L, dtype=X.dtype, device=X.device)))
+    for u, v in pairs_in:
+        g = torch.Generator(device=u.device)
+        g.manual_seed(0x5EED + 7 * u.shape[0] + v.shape[0])
+        om = torch.randn((v.shape[0], _SKETCH_L), dtype=u.dtype, device=u.device, generator=g)
+        pairs.append((u @ (v.mH @ om), torch.eye(_SKETCH_L, dtype=u.dtype, device=u.device)))
     out = _kernel_batch(ar, pairs, eps=max(0.1 * ar.eps, 1e-8))
     qs = []
     for o in out:
