@@ -47,7 +47,8 @@ def parse():
     ap.add_argument("--no-estimate", action="store_true", help="skip the delta_{H,F} estimator timing")
     ap.add_argument("--solve-config", default="T65k")
     ap.add_argument("--no-direct", action="store_true", help="skip the H-LU direct-solve section")
-    ap.add_argument("--direct-config", default="H4k")
+    ap.add_argument("--direct-config", default="H4k,U8k@2562",
+                    help="H-LU direct-solve workloads (TAG or TAG@points; U8k@2562 = 7,686 dofs, the paper's Table 5 size)")
     ap.add_argument("--extra-configs", default="U131k,U8k,H4k",
                     help="other BASELINE configs measured briefly (assembly + 20 matvecs); '' to skip")
     ap.add_argument("--shard", action="store_true",
@@ -303,7 +304,8 @@ def direct_solve(tag, device, eps_lu=1e-4, cpu=True):
     from paper_1706_09384_b200 import hierarchical_lu as HL
     from paper_1706_09384_b200.configs import WORKLOADS
 
-    w = WORKLOADS[tag]
+    base, _, npts = tag.partition("@")
+    w = WORKLOADS[base] if not npts else WORKLOADS[base].with_points(int(npts))
     cloud = hmx.make_geometry("sphere", w.n_points, 1.0, d=w.d)
     ct = hmx.build_cluster_tree(cloud, w.n_leaf)
     bt = hmx.build_block_tree(ct, ct, w.eta)
@@ -621,7 +623,8 @@ def hmx_arm(args):
         line["time_to_solve"] = time_to_solve(args.solve_config, local)
     if not args.no_direct:
         try:
-            line["direct_solve"] = direct_solve(args.direct_config, local, cpu=(rank == 0 and ws == 1))
+            line["direct_solve"] = {t: direct_solve(t, local, cpu=(rank == 0 and ws == 1))
+                                    for t in args.direct_config.split(",") if t}
         except Exception as exc:  # reported, never fatal for the headline line
             line["direct_solve"] = {"failed": repr(exc)}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
