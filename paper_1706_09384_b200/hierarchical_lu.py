@@ -86,6 +86,7 @@ class Sub:
 
 
 _DC_MAX = 1 << 22      # largest finished block (entries) kept as a dense operand image (64 MB)
+_DC_BUDGET = 16 << 30  # HBM bytes all dense operand images of one factorisation may take
 
 
 def _finalize(x):
@@ -98,11 +99,15 @@ def _finalize(x):
 
 def _dense_image(ar, x):
     """Dense image of a finished hierarchical block (one GEMM per product instead of a recursion
-    over its leaves), or None."""
-    if not x.fin or (x.r1 - x.r0) * (x.c1 - x.c0) > _DC_MAX:
+    over its leaves), or None (block above _DC_MAX entries, or the images' HBM budget spent)."""
+    if not x.fin:
         return None
     if x.dc is None:
+        n = (x.r1 - x.r0) * (x.c1 - x.c0)
+        if n > _DC_MAX or ar.dc_bytes + 16 * n > _DC_BUDGET:
+            return None
         x.dc = _dense(ar, x)
+        ar.dc_bytes += 16 * n
     return x.dc
 
 
@@ -115,6 +120,7 @@ class Arith:
     n_trunc: int = 0
     n_trunc_calls: int = 0
     t_trunc: float = 0.0
+    dc_bytes: int = 0
     k_hist: list = field(default_factory=list)
     n_getrf: int = 0
     max_rank: int = 0
@@ -879,10 +885,11 @@ def hlu(h, eps_lu, rule="frobenius", block_tree=None):
     t2 = time.perf_counter()
     f = LUFactors(lower=_Tri(root, True), upper=_Tri(root, False), eps_lu=float(eps_lu), d=h.d,
                   perm=np.asarray(h.perm), n=h.d * h.n_points)
-    f.stats = {"copy_s": t1 - t0, "factor_s": t2 - t1, "n_truncations": ar.n_trunc, "n_truncate_calls": ar.n_trunc_calls, "truncate_s": ar.t_trunc,
-               "truncate_kmax_p50_p90_max": [int(q) for q in np.percentile(ar.k_hist, [50, 90, 100])] if ar.k_hist else [],
-               "n_getrf": ar.n_getrf,
-               "max_rank": ar.max_rank}
+    f.stats = {"copy_s": t1 - t0, "factor_s": t2 - t1, "n_truncations": ar.n_trunc,
+               "n_truncate_calls": ar.n_trunc_calls, "truncate_s": ar.t_trunc, "dense_image_GB": ar.dc_bytes / 1e9,
+               "truncate_kmax_p50_p90_max": ([int(q) for q in np.percentile(ar.k_hist, [50, 90, 100])]
+                                             if ar.k_hist else []),
+               "n_getrf": ar.n_getrf, "max_rank": ar.max_rank}
     return f
 
 

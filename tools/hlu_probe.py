@@ -34,7 +34,7 @@ for eps in epss:
           f"residual {res:.2e}, truncations {f.stats["n_truncations"]} in {f.stats["n_truncate_calls"]} calls, getrf {f.stats['n_getrf']}, "
           f"max rank {f.stats['max_rank']}, storage {f.storage() * 16 / 1e6:.1f} MB "
           f"(H {rep.n_stored * 16 / 1e6:.1f} MB); truncate calls {f.stats['truncate_s']:.3f} s, "
-          f"call K max p50/p90/max {f.stats['truncate_kmax_p50_p90_max']}", flush=True)
+          f"call K max p50/p90/max {f.stats['truncate_kmax_p50_p90_max']}, dense images {f.stats['dense_image_GB']:.2f} GB", flush=True)
     if prof and eps == epss[-1]:
         import cProfile
         import pstats
