@@ -1,5 +1,6 @@
 """H-matrix snapshots (SPEC.md:563-571 ``snapshot(save|load, path)``; SURVEY
-8(f) row 3): a versioned, checksummed binary image of an assembled H-matrix.
+8(f) row 3): a versioned, checksummed binary image of an assembled H-matrix
+(or, ``save_lu``, of H-LU factors).
 
 Layout (little endian)::
 
@@ -87,7 +88,8 @@ def save(h, path):
 
 
 def load(path, device=0):
-    """Read a snapshot written by :func:`save` back onto ``device``."""
+    """Read a snapshot written by :func:`save` (an HMatrix) or :func:`save_lu` (LUFactors) back onto
+    ``device``."""
     with open(path, "rb") as f:
         raw = f.read()
     if len(raw) < len(MAGIC) + 12 + 32 or raw[:len(MAGIC)] != MAGIC:
@@ -101,6 +103,8 @@ def load(path, device=0):
     buf = io.BytesIO(body)
     buf.seek(len(MAGIC) + 12)
     header = json.loads(buf.read(hlen))
+    if header.get("kind") == "lu":
+        return _load_lu(header, buf, len(body), device)
     arrays = {}
     for k in _ARRAYS:
         meta = header["arrays"][k]
@@ -126,12 +130,106 @@ def load(path, device=0):
     return H
 
 
+# ---- LU factors ("-> HMatrix or LUFactors") ------------------------------------
+# Same envelope (magic, version, JSON header, SHA-256 trailer); header "kind": "lu" carries the
+# factor tree's structure, the payload every leaf in tree order: a factored diagonal leaf as
+# L, U (m x m) and its row permutation (int64), any other dense leaf as its block, a low-rank leaf
+# as U then V -- complex128 row-major.
+
+def _lu_struct(x, leaves):
+    from . import hierarchical_lu as HL
+
+    box = [x.r0, x.r1, x.c0, x.c1]
+    if isinstance(x, HL.Sub):
+        return {"S": box, "rs": x.rs, "cs": x.cs, "ch": [[_lu_struct(c, leaves) for c in row] for row in x.ch]}
+    leaves.append(x)
+    if isinstance(x, HL.Dense):
+        return {"D": box, "f": int(x.L is not None)}
+    return {"R": box, "k": x.rank}
+
+
+def save_lu(f, path):
+    """Write LU factors (``hierarchical_lu.LUFactors``) to ``path``."""
+    from . import hierarchical_lu as HL
+
+    leaves = []
+    tree = _lu_struct(f.root, leaves)
+    perm = np.ascontiguousarray(f.perm, dtype=np.int64)
+    header = {"kind": "lu", "d": f.d, "n": f.n, "eps_lu": f.eps_lu, "n_points": len(perm), "tree": tree}
+    hb = json.dumps(header, sort_keys=True).encode()
+    with open(path, "wb") as fh:
+        w = _HashWriter(fh)
+        w.write(MAGIC)
+        w.write(struct.pack("<IQ", VERSION, len(hb)))
+        w.write(hb)
+        w.write(perm.tobytes())
+        for x in leaves:
+            if isinstance(x, HL.Dense):
+                mats = [x.L, x.U] if x.L is not None else [x.a]
+                for m in mats:
+                    w.write(np.ascontiguousarray(m.cpu().numpy()).tobytes())
+                if x.L is not None:
+                    w.write(np.ascontiguousarray(x.pidx.cpu().numpy().astype(np.int64)).tobytes())
+            else:
+                w.write(np.ascontiguousarray(x.u.cpu().numpy()).tobytes())
+                w.write(np.ascontiguousarray(x.v.cpu().numpy()).tobytes())
+        fh.write(w.h.digest())
+
+
+def _load_lu(header, buf, nbody, device):
+    import torch
+
+    from . import hierarchical_lu as HL
+
+    dev = torch.device("cuda", device)
+    perm = np.frombuffer(buf.read(8 * header["n_points"]), np.int64).copy()
+
+    def arr(shape, dtype=np.complex128):
+        n = int(np.prod(shape))
+        a = np.frombuffer(buf.read(np.dtype(dtype).itemsize * n), dtype)
+        if a.size != n:
+            raise SnapshotCorruptError("snapshot payload size mismatch")
+        return torch.as_tensor(a.reshape(shape).copy(), device=dev)
+
+    def rec(js):
+        if "S" in js:
+            r0, r1, c0, c1 = js["S"]
+            x = HL.Sub(r0, r1, c0, c1, [tuple(q) for q in js["rs"]], [tuple(q) for q in js["cs"]],
+                       [[rec(c) for c in row] for row in js["ch"]])
+            x.fin = True
+            return x
+        if "D" in js:
+            r0, r1, c0, c1 = js["D"]
+            m, n = r1 - r0, c1 - c0
+            if js["f"]:
+                x = HL.Dense(r0, r1, c0, c1, None)
+                x.L, x.U = arr((m, m)), arr((m, m))
+                x.pidx = arr((m,), np.int64)
+                x.pinv = torch.argsort(x.pidx)
+                return x
+            return HL.Dense(r0, r1, c0, c1, arr((m, n)))
+        r0, r1, c0, c1 = js["R"]
+        k = js["k"]
+        return HL.LowRank(r0, r1, c0, c1, arr((r1 - r0, k)), arr((c1 - c0, k)))
+
+    root = rec(header["tree"])
+    if buf.tell() != nbody:
+        raise SnapshotCorruptError("snapshot payload size mismatch")
+    return HL.LUFactors(lower=HL._Tri(root, True), upper=HL._Tri(root, False), eps_lu=header["eps_lu"],
+                        d=header["d"], perm=perm, n=header["n"])
+
+
 def snapshot(op, path, h=None, device=0):
-    """SPEC.md:563 ``snapshot(save|load, path)``."""
+    """SPEC.md:563 ``snapshot(save|load, path) -> HMatrix or LUFactors``."""
     if op == "save":
         if h is None:
-            raise ValueError("snapshot('save', path, h): no H-matrix given")
-        save(h, path)
+            raise ValueError("snapshot('save', path, h): no H-matrix / LU factors given")
+        from .hierarchical_lu import LUFactors
+
+        if isinstance(h, LUFactors):
+            save_lu(h, path)
+        else:
+            save(h, path)
         return h
     if op == "load":
         return load(path, device=device)

@@ -165,3 +165,32 @@ def test_single_leaf_is_dense_lu():
     x, f = hmx.solve_direct(H, b, 1e-4)
     assert f.stats["n_getrf"] == 1
     assert np.linalg.norm(hmx.matvec(H, x) - b) <= 1e-13 * np.linalg.norm(b)
+
+
+def test_lu_snapshot_round_trip(tmp_path):
+    """LU factors saved and loaded hold bitwise the same leaves and solve a new
+    right-hand side with the in-process residual; a flipped payload byte is a checksum error."""
+    pb = Problem("T65k", 600)
+    H, _ = pb.device_h()
+    f = hmx.hlu(H, 1e-6)
+    p = tmp_path / "lu.hmx"
+    hmx.snapshot("save", str(p), f)
+    g = hmx.snapshot("load", str(p))
+    assert isinstance(g, HL.LUFactors)
+    for x, y in zip(HL._walk(f.root), HL._walk(g.root)):
+        assert type(x) is type(y) and (x.r0, x.r1, x.c0, x.c1) == (y.r0, y.r1, y.c0, y.c1)
+        pairs = ([(x.u, y.u), (x.v, y.v)] if isinstance(x, HL.LowRank) else
+                 [(x.L, y.L), (x.U, y.U), (x.pidx, y.pidx)] if x.L is not None else [(x.a, y.a)])
+        for p_, q_ in pairs:
+            assert torch.equal(p_, q_)
+    b = pb.rhs(9)
+    x0, x1 = hmx.triangular_solve(f, b), hmx.triangular_solve(g, b)
+    assert np.linalg.norm(x1 - x0) <= 1e-13 * np.linalg.norm(x0)
+    r0 = np.linalg.norm(hmx.matvec(H, x0) - b)
+    r1 = np.linalg.norm(hmx.matvec(H, x1) - b)
+    assert abs(r1 - r0) <= 1e-3 * r0
+    raw = bytearray(p.read_bytes())
+    raw[len(raw) // 2] ^= 0x40
+    p.write_bytes(bytes(raw))
+    with pytest.raises(hmx.SnapshotCorruptError):
+        hmx.snapshot("load", str(p))
