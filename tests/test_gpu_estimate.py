@@ -113,3 +113,19 @@ def test_every_leaf_within_eps(tag):
     print(f"{tag}: {len(adm)} admissible leaves, worst {ratio.max() / eps:.3f} eps, "
           f"{np.mean(ratio > eps) * 100:.2f}% above eps, {len(over)} above 3 eps (oracle-reproduced), "
           f"delta_HF / ||A||_F = {np.sqrt(err2.sum() / norm2.sum()) / eps:.3f} eps")
+
+
+def test_estimator_with_direct_solve():
+    # SPEC.md:511-515 with x0 from solve_direct: bound >= true residual, and tightening
+    # eps_ACA = eps_LU from 1e-4 to 1e-6 drops both by orders (PAPER Table 5 pairs)
+    pb = Problem("U8k", 1024)
+    b = pb.rhs(3)
+    reps = []
+    for eps in (1e-4, 1e-6):
+        H, _ = hmx.assemble(pb.spec, pb.cloud, pb.ct, pb.bt, hmx.ACAConfig(eps_aca=eps))
+        x0, _ = hmx.solve_direct(H, b, eps)
+        rep = estimate(H, pb.spec, pb.cloud, b, x0, with_dense_oracle=True)
+        assert rep.bound >= rep.true_residual
+        reps.append(rep)
+    assert reps[1].bound < reps[0].bound / 10
+    assert reps[1].true_residual < reps[0].true_residual / 10
