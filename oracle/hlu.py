@@ -27,7 +27,11 @@ Decisions (shared with the device implementation ``paper_1706_09384_b200/hierarc
 7. truncation points: a target holding more than PEND_FLUSH columns; every low-rank leaf
    of the trailing blocks after each elimination step of the LU and of the block
    triangular solves (the device batches each such set into one kernel call); a block
-   read as an operand; the end of hlu / formatted_addmul.
+   read as an operand; the end of hlu / formatted_addmul;
+8. a product (no low-rank operand) landing on a hierarchical target of at most DENSE_T rows and
+   columns is formed exactly as one dense product and scattered into the target's leaves: dense
+   leaves add it, low-rank leaves accumulate it densely and are truncated at their next truncation
+   point as the pair (X, I), X = U V^H + pending addends + the dense addend.
 """
 
 import numpy as np
@@ -38,16 +42,18 @@ from .lowrank import truncation_rank
 DENSE, LOWRANK, SUB = 0, 1, 2
 PEND_FLUSH = 400     # decision 7: pending columns on one target before an early truncation
 AGGLO_MAX = 512      # decision 5: agglomerated product columns before an intermediate truncation
+DENSE_T = 256        # decision 8: hierarchical targets up to this many rows / columns take products densely
 
 
 class Node:
-    __slots__ = ("kind", "r0", "r1", "c0", "c1", "a", "u", "v", "pend", "rs", "cs", "ch",
+    __slots__ = ("kind", "r0", "r1", "c0", "c1", "a", "u", "v", "pend", "acc", "rs", "cs", "ch",
                  "lu", "piv")
 
     def __init__(self, kind, r0, r1, c0, c1):
         self.kind, self.r0, self.r1, self.c0, self.c1 = kind, r0, r1, c0, c1
         self.a = self.u = self.v = self.rs = self.cs = self.ch = self.lu = self.piv = None
         self.pend = []
+        self.acc = None
 
 
 class Ctx:
@@ -77,7 +83,13 @@ def _compress(cx, m):
 
 
 def _flush(cx, x):
-    if x.pend:
+    if x.acc is not None:
+        X = x.acc
+        for u, v in [(x.u, x.v)] + x.pend:
+            X = X + u @ v.conj().T
+        x.acc, x.pend = None, []
+        x.u, x.v = _trunc(cx, X, np.eye(X.shape[1], dtype=np.complex128))
+    elif x.pend:
         u = np.concatenate([x.u] + [p[0] for p in x.pend], axis=1)
         v = np.concatenate([x.v] + [p[1] for p in x.pend], axis=1)
         x.pend = []
@@ -228,6 +240,17 @@ def _add_lr(cx, C, U, V):
                 _add_lr(cx, C.ch[i][j], U[a - C.r0:b - C.r0], V[c - C.c0:e - C.c0])
 
 
+def _add_dense(cx, C, M):
+    if C.kind == DENSE:
+        C.a += M
+    elif C.kind == LOWRANK:
+        C.acc = M.copy() if C.acc is None else C.acc + M
+    else:
+        for i, (a, b) in enumerate(C.rs):
+            for j, (c, e) in enumerate(C.cs):
+                _add_dense(cx, C.ch[i][j], M[a - C.r0:b - C.r0, c - C.c0:e - C.c0])
+
+
 def _prod_lr(cx, A, B):
     if A.kind == LOWRANK:
         _flush(cx, A)
@@ -283,6 +306,9 @@ def addmul(cx, C, A, B, alpha=-1.0):
             _add_lr(cx, C, alpha * mul(cx, A, B.u), B.v)
         return
     if C.kind == SUB:
+        if C.r1 - C.r0 <= DENSE_T and C.c1 - C.c0 <= DENSE_T:
+            _add_dense(cx, C, alpha * (dense(cx, A) @ dense(cx, B)))
+            return
         Kp = A.cs if A.kind == SUB else (B.rs if B.kind == SUB else [(A.c0, A.c1)])
         for i, (ra, rb) in enumerate(C.rs):
             for j, (ca, cb) in enumerate(C.cs):

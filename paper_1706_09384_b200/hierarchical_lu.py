@@ -65,11 +65,12 @@ class Dense:
 
 
 class LowRank:
-    __slots__ = ("r0", "r1", "c0", "c1", "u", "v", "pend")
+    __slots__ = ("r0", "r1", "c0", "c1", "u", "v", "pend", "acc")
 
     def __init__(self, r0, r1, c0, c1, u, v):
         self.r0, self.r1, self.c0, self.c1, self.u, self.v = r0, r1, c0, c1, u, v
-        self.pend = []
+        self.pend = []      # low-rank addends (U_i, V_i) awaiting truncation
+        self.acc = None     # dense addend accumulated from small-target products
 
     @property
     def rank(self):
@@ -87,6 +88,7 @@ class Sub:
 
 _DC_MAX = 1 << 22      # largest finished block (entries) kept as a dense operand image (64 MB)
 _DC_BUDGET = 16 << 30  # HBM bytes all dense operand images of one factorisation may take
+_DENSE_T = int(os.environ.get("HMX_HLU_DENSE_T", "256"))  # hierarchical targets up to this size take products densely
 
 
 def _finalize(x):
@@ -340,18 +342,26 @@ def _cat(x):
     us = [x.u] + [p[0] for p in x.pend]
     vs = [x.v] + [p[1] for p in x.pend]
     x.pend = []
+    if x.acc is not None:
+        # a dense addend is pending: the whole block as the pair (X, I)
+        X = x.acc
+        x.acc = None
+        for u, v in zip(us, vs):
+            if u.shape[1]:
+                X.addmm_(u, v.mH)
+        return X, torch.eye(X.shape[1], dtype=X.dtype, device=X.device)
     # stacked as (K, rows) row-major = the column-major panels the truncation kernel reads
     return torch.cat([t.mT for t in us], 0).mT, torch.cat([t.mT for t in vs], 0).mT
 
 
 def _flush(ar, x):
-    if x.pend:
+    if x.pend or x.acc is not None:
         x.u, x.v = _trunc(ar, *_cat(x))
 
 
 def _pending(x, out):
     if isinstance(x, LowRank):
-        if x.pend:
+        if x.pend or x.acc is not None:
             out.append(x)
     elif isinstance(x, Sub):
         for row in x.ch:
@@ -474,6 +484,30 @@ def _add_lr(ar, C, U, V):
                 _add_lr(ar, C.ch[i][j], U[a - C.r0:b - C.r0], V[c - C.c0:e - C.c0])
 
 
+def _add_dense(ar, C, M):
+    """C += M for a dense M (a low-rank leaf accumulates it densely until its next truncation)."""
+    if isinstance(C, Dense):
+        C.a.add_(M)
+    elif isinstance(C, LowRank):
+        if C.acc is None:
+            C.acc = M.clone()
+        else:
+            C.acc.add_(M)
+    else:
+        for i, (a, b) in enumerate(C.rs):
+            for j, (c, e) in enumerate(C.cs):
+                _add_dense(ar, C.ch[i][j], M[a - C.r0:b - C.r0, c - C.c0:e - C.c0])
+
+
+def _dense_op(ar, x):
+    """Dense image of an operand (cached for finished hierarchical blocks)."""
+    if isinstance(x, Sub):
+        img = _dense_image(ar, x)
+        if img is not None:
+            return img
+    return _dense(ar, x)
+
+
 def _prod_lr(ar, A, B):
     """Low-rank (U, V) with U V^H ~ A B (truncated with eps)."""
     torch = _torch()
@@ -533,6 +567,12 @@ def _addmul(ar, C, A, B, alpha=-1.0):
             _add_lr(ar, C, alpha * _mul(ar, A, B.u), B.v)
         return
     if isinstance(C, Sub):
+        if C.r1 - C.r0 <= _DENSE_T and C.c1 - C.c0 <= _DENSE_T:
+            # small hierarchical target: the exact product by one GEMM on the operands' dense
+            # images, scattered into the target's leaves (oracle decision 8)
+            M = _dense_op(ar, A) @ _dense_op(ar, B)
+            _add_dense(ar, C, M if alpha == 1.0 else M.mul_(alpha))
+            return
         Kp = A.cs if isinstance(A, Sub) else (B.rs if isinstance(B, Sub) else [(A.c0, A.c1)])
         for i, (ra, rb) in enumerate(C.rs):
             for j, (ca, cb) in enumerate(C.cs):
