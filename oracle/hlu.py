@@ -42,7 +42,7 @@ from .lowrank import truncation_rank
 DENSE, LOWRANK, SUB = 0, 1, 2
 PEND_FLUSH = 400     # decision 7: pending columns on one target before an early truncation
 AGGLO_MAX = 512      # decision 5: agglomerated product columns before an intermediate truncation
-DENSE_T = 256        # decision 8: hierarchical targets up to this many rows / columns take products densely
+DENSE_T = 512        # decision 8: hierarchical targets up to this many rows / columns take products densely
 
 
 class Node:

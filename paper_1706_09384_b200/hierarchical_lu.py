@@ -88,7 +88,7 @@ class Sub:
 
 _DC_MAX = 1 << 22      # largest finished block (entries) kept as a dense operand image (64 MB)
 _DC_BUDGET = 16 << 30  # HBM bytes all dense operand images of one factorisation may take
-_DENSE_T = int(os.environ.get("HMX_HLU_DENSE_T", "256"))  # hierarchical targets up to this size take products densely
+_DENSE_T = int(os.environ.get("HMX_HLU_DENSE_T", "512"))  # hierarchical targets up to this size take products densely
 
 
 def _finalize(x):
