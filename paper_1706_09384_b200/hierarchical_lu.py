@@ -45,12 +45,30 @@ from .geometry import AdmissibleLeaf, DenseLeaf, Subdivided
 _RULES = ("frobenius", "spectral")
 
 
-def _torch():
-    import torch
+_TORCH = None
 
-    if not torch.cuda.is_available():
-        raise RuntimeError("hlu: a CUDA device is required (no CPU fallback)")
-    return torch
+
+def _torch():
+    global _TORCH
+    if _TORCH is None:
+        import torch
+
+        if not torch.cuda.is_available():
+            raise RuntimeError("hlu: a CUDA device is required (no CPU fallback)")
+        _TORCH = torch
+    return _TORCH
+
+
+_EYE = {}
+
+
+def _eye(n, like):
+    """Cached identity (the orthonormal side of the dense-form pairs; read-only)."""
+    key = (n, like.device)
+    e = _EYE.get(key)
+    if e is None:
+        e = _EYE[key] = _torch().eye(n, dtype=like.dtype, device=like.device)
+    return e
 
 
 # --------------------------------------------------------------------------------------------
@@ -153,6 +171,8 @@ _CUSOLVER_K = int(os.environ.get("HMX_HLU_CUSOLVER_K", "1021"))
 # pairs whose kernel problem would exceed this many columns go through a _SKETCH_L-column range sketch
 _SKETCH_K = int(os.environ.get("HMX_HLU_SKETCH_K", "112"))
 _SKETCH_L = 112
+_SKETCH_S = 56        # narrow sketch (the K <= 60 recompression class) ...
+_SKETCH_S_RANK = 24   # ... for targets whose rank before the update was at most this
 _TRULES = {"frobenius": 0, "spectral": 1}
 
 
@@ -205,11 +225,11 @@ def _dense_form(u, v):
     Returns (pair, swapped)."""
     torch = _torch()
     if u.shape[0] < v.shape[0]:
-        return (v @ u.mH, torch.eye(u.shape[0], dtype=u.dtype, device=u.device)), True
-    return (u @ v.mH, torch.eye(v.shape[0], dtype=u.dtype, device=u.device)), False
+        return (v @ u.mH, _eye(u.shape[0], u)), True
+    return (u @ v.mH, _eye(v.shape[0], u)), False
 
 
-def _truncate_batch(ar, items):
+def _truncate_batch(ar, items, hints=None):
     """items: list of (U, V) pairs (any strides) -> list of truncated (U', V') pairs, on the device
     through ``hmx_truncate_batch`` (Gram pair, scaled Cholesky, Hermitian eigen-solver, truncation
     rule, U' = U W_U, V' = V W_V -- the assembly's recompression kernels), one call per batch.
@@ -241,9 +261,18 @@ def _truncate_batch(ar, items):
         idx.append(i)
     if sk_x:
         # U V^H = Q (Q^H U) V^H on a sketched range basis Q, truncated as the (V (U^H Q), Q) pair:
-        # its V side is orthonormal and it has at most _SKETCH_L columns (the one-CTA eigen-solve
-        # stays small); kernel result (P, R) means U V^H ~ R P^H
-        for (u, v), Q, i in zip(sk_x, _sketch_basis(ar, sk_x), sk_meta):
+        # its V side is orthonormal and it has at most l columns (the one-CTA eigen-solve stays
+        # small); kernel result (P, R) means U V^H ~ R P^H.  The sketch width follows the rank
+        # the target had before the update (_SKETCH_S columns when it was small, the fast kernel
+        # class), widened to _SKETCH_L where the narrow sketch saturates.
+        ls = [_SKETCH_S if hints is not None and hints[i] is not None and hints[i] <= _SKETCH_S_RANK
+              else _SKETCH_L for i in sk_meta]
+        qs = _sketch_basis(ar, sk_x, ls)
+        wide = [j for j, (q, sl) in enumerate(zip(qs, ls)) if q is None and sl < _SKETCH_L]
+        if wide:
+            for j, q in zip(wide, _sketch_basis(ar, [sk_x[j] for j in wide], [_SKETCH_L] * len(wide))):
+                qs[j] = q
+        for (u, v), Q, i in zip(sk_x, qs, sk_meta):
             if Q is None:   # sketch saturated: the direct (possibly dense) form
                 pair, sw = _direct_form(u, v)
                 sub.append(pair)
@@ -284,22 +313,22 @@ def _direct_form(u, v):
     return (u, v), False
 
 
-def _sketch_basis(ar, pairs_in):
+def _sketch_basis(ar, pairs_in, ls):
     """Orthonormal bases of the ranges of U V^H (dm x dn) from a seeded Gaussian sketch
-    Y = U (V^H Omega) (Omega dn x _SKETCH_L): the (Y, I) pairs are truncated at max(eps / 10, 1e-8)
+    Y = U (V^H Omega) (Omega dn x l, l = ls[i]): the (Y, I) pairs are truncated at max(eps / 10, 1e-8)
     in one kernel call and the orthogonal columns A = Y W_U normalised.  None where the sketch
-    saturates (kept rank above _SKETCH_L - 8: the range may be larger than the sketch)."""
+    saturates (kept rank above l - 8: the range may be larger than the sketch)."""
     torch = _torch()
     pairs = []
-    for u, v in pairs_in:
+    for (u, v), sl in zip(pairs_in, ls):
         g = torch.Generator(device=u.device)
         g.manual_seed(0x5EED + 7 * u.shape[0] + v.shape[0])
-        om = torch.randn((v.shape[0], _SKETCH_L), dtype=u.dtype, device=u.device, generator=g)
-        pairs.append((u @ (v.mH @ om), torch.eye(_SKETCH_L, dtype=u.dtype, device=u.device)))
+        om = torch.randn((v.shape[0], sl), dtype=u.dtype, device=u.device, generator=g)
+        pairs.append((u @ (v.mH @ om), _eye(sl, u)))
     out = _kernel_batch(ar, pairs, eps=max(0.1 * ar.eps, 1e-8))
     qs = []
-    for o in out:
-        if o is None or o[0].shape[1] > _SKETCH_L - 8:
+    for o, sl in zip(out, ls):
+        if o is None or o[0].shape[1] > sl - 8:
             qs.append(None)
         elif o[0].shape[1] == 0:
             qs.append(o[0])
@@ -349,14 +378,15 @@ def _cat(x):
         for u, v in zip(us, vs):
             if u.shape[1]:
                 X.addmm_(u, v.mH)
-        return X, torch.eye(X.shape[1], dtype=X.dtype, device=X.device)
+        return X, _eye(X.shape[1], X)
     # stacked as (K, rows) row-major = the column-major panels the truncation kernel reads
     return torch.cat([t.mT for t in us], 0).mT, torch.cat([t.mT for t in vs], 0).mT
 
 
 def _flush(ar, x):
     if x.pend or x.acc is not None:
-        x.u, x.v = _trunc(ar, *_cat(x))
+        hint = x.u.shape[1]
+        x.u, x.v = _truncate_batch(ar, [_cat(x)], [hint])[0]
 
 
 def _pending(x, out):
@@ -375,7 +405,8 @@ def _flush_batch(ar, nodes):
     for x in nodes:
         _pending(x, todo)
     if todo:
-        for x, (u, v) in zip(todo, _truncate_batch(ar, [_cat(x) for x in todo])):
+        hints = [x.u.shape[1] for x in todo]
+        for x, (u, v) in zip(todo, _truncate_batch(ar, [_cat(x) for x in todo], hints)):
             x.u, x.v = u, v
 
 
