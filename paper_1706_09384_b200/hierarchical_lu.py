@@ -19,13 +19,17 @@ Arithmetic (all complex128 on the device, torch's current stream):
   (low-rank: only U, resp. V, is transformed);
 * ``formatted_addmul`` C <- C + alpha A B over the 27 format cases: a
   low-rank operand multiplies through its thin factors, hierarchical x
-  hierarchical recurses over the cluster children, dense targets accumulate
-  densely; low-rank targets collect addends and are truncated once, with
-  eps_LU, when they are next read (QR of both factor panels, SVD of the K x K
-  core, the Frobenius-tail rule of ``recompress``).  A
-  product landing on a low-rank target without a low-rank operand is formed
-  per child block and agglomerated into one factor pair (padded factors,
-  one truncation).
+  hierarchical recurses over the cluster children (a hierarchical target of
+  at most _DENSE_T rows / columns takes the exact product as one GEMM on the
+  operands' dense images), dense targets accumulate densely; low-rank targets
+  collect addends and are truncated with eps_LU at the truncation points of
+  oracle/hlu.py (decision 7).  A product landing on a low-rank target without
+  a low-rank operand is formed per child block and agglomerated into one
+  factor pair.
+* truncations (the recompress rule): batched on the device by
+  ``hmx_truncate_batch`` (the assembly's Gram / Cholesky / eigen-solver /
+  form kernels), rank-deficient pairs re-submitted as (U V^H, I), problems
+  wider than 112 columns reduced first by a seeded Gaussian range sketch.
 
 The LU is in place: ``LUFactors.lower`` / ``.upper`` are the strictly lower /
 upper blocks plus the unit-lower / upper factors of the diagonal leaves of the
