@@ -948,7 +948,11 @@ def hlu(h, eps_lu, rule="frobenius", block_tree=None):
     if bt.rows is not bt.cols and not np.array_equal(bt.rows.permutation, bt.cols.permutation):
         raise ValueError("hlu: row and column trees differ")
     torch.cuda.set_device(h.device)
-    _lib.release_cached(h.device)
+    free, total = torch.cuda.mem_get_info(h.device)
+    if free < total // 4:
+        # hand the context's cached blocks to torch's allocator (dense images) only when HBM is
+        # short: the cache is what the truncation calls below reuse instead of cudaMalloc / cudaFree
+        _lib.release_cached(h.device)
     t0 = time.perf_counter()
     root = copy_hmatrix(h, bt)
     torch.cuda.synchronize()
