@@ -195,10 +195,19 @@ def _kernel_batch(ar, items, eps=None):
     for i, (u, v) in enumerate(items):
         dm[i], K[i] = u.shape
         dn[i] = v.shape[0]
+    # all outputs in one allocation (one torch call instead of 2n); segments start on 256-byte
+    # boundaries like the allocator's own blocks
+    su = (K * dm + 15) // 16 * 16
+    sv = (K * dn + 15) // 16 * 16
+    offs = np.concatenate(([0], np.cumsum(su + sv)))
+    out = torch.empty(int(offs[-1]), dtype=items[0][0].dtype, device=dev)
+    for i, (u, v) in enumerate(items):
         uc = u.mT.contiguous()          # (K, dm) row-major = dm x K column-major
         vc = v.mT.contiguous()
-        uo = torch.empty_like(uc)
-        vo = torch.empty_like(vc)
+        o = int(offs[i])
+        k, m_, n_ = int(K[i]), int(dm[i]), int(dn[i])
+        uo = out[o:o + k * m_].view(k, m_)
+        vo = out[o + int(su[i]):o + int(su[i]) + k * n_].view(k, n_)
         keep += [uc, vc]
         outs.append((uo, vo))
         ptr[:, i] = (uc.data_ptr(), vc.data_ptr(), uo.data_ptr(), vo.data_ptr())
@@ -460,11 +469,22 @@ def _dense(ar, x):
         return x.u @ x.v.mH
     if x.dc is not None:
         return x.dc
-    out = torch.zeros((x.r1 - x.r0, x.c1 - x.c0), dtype=torch.complex128, device=_dev_of(x))
+    out = torch.empty((x.r1 - x.r0, x.c1 - x.c0), dtype=torch.complex128, device=_dev_of(x))
+    _dense_into(ar, x, out)
+    return out
+
+
+def _dense_into(ar, x, out):
+    """Dense image of Sub ``x`` written in place into ``out`` (the children tile it): nested
+    Subs write straight into their sub-view instead of through a temporary of their own."""
     for i, (a, b) in enumerate(x.rs):
         for j, (c, e) in enumerate(x.cs):
-            out[a - x.r0:b - x.r0, c - x.c0:e - x.c0] = _dense(ar, x.ch[i][j])
-    return out
+            ch = x.ch[i][j]
+            v = out[a - x.r0:b - x.r0, c - x.c0:e - x.c0]
+            if isinstance(ch, Sub) and ch.dc is None:
+                _dense_into(ar, ch, v)
+            else:
+                v.copy_(_dense(ar, ch))
 
 
 def _dev_of(x):
