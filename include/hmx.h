@@ -135,6 +135,10 @@ int hmx_hmatrix_stats(const hmx_hmatrix* h, hmx_stats* st);
  * bit3 fallback, bit4 Cholesky regularised, bit5 QL eigen fallback, bit6 QL not converged) */
 int hmx_hmatrix_block_info(const hmx_hmatrix* h, int64_t* steps, int64_t* rank_before, int64_t* rank_after,
                            int32_t* flags);
+/* restore the per-leaf assembly record of an imported H (snapshot load): ACA steps,
+ * rank before recompression (>= the stored rank) and flags; any pointer may be NULL (left unchanged) */
+int hmx_hmatrix_set_block_info(hmx_hmatrix* h, const int64_t* steps, const int64_t* rank_before,
+                               const int32_t* flags);
 /* copy leaf b out (layouts as in hmx_hmatrix_load) */
 int hmx_hmatrix_get_block(const hmx_hmatrix* h, int64_t b, double* a, double* v);
 /* zero-copy device view of the leaf payloads (input of the H-LU, which the reference's
@@ -180,6 +184,13 @@ int hmx_truncate_batch(hmx_ctx* ctx, int64_t nb, const int64_t* dm, const int64_
                        const uint64_t* U, const uint64_t* V, const uint64_t* Uo, const uint64_t* Vo, double eps,
                        int32_t trunc_rule, int64_t* ranks, int32_t* flags);
 int hmx_matvec(hmx_hmatrix* h, const double* x, double* y, int32_t mem);
+/* the same on an explicit cudaStream_t (0 = legacy default stream).  Concurrency (an
+ * assembled H is immutable and safe for concurrent matvec): the H is only read; every buffer a matvec
+ * writes belongs to a per-stream workspace of the H (created on first use of a stream), so calls on
+ * different streams run concurrently and calls from several host threads on one stream are serialised
+ * by a per-workspace lock while they enqueue.  mem = HMX_DEVICE: asynchronous on `stream`;
+ * HMX_HOST: returns once y is on the host.  hmx_matvec = hmx_matvec_on with the context stream. */
+int hmx_matvec_on(hmx_hmatrix* h, const double* x, double* y, int32_t mem, uint64_t stream);
 /* device pointers; phase_ms[4] = gather, phase 1 (V^H x), phase 2 (row GEMV), finalize */
 int hmx_matvec_profile(hmx_hmatrix* h, const double* x_dev, double* y_dev, float* phase_ms);
 /* live kernel timing: every matvec between begin and end records CUDA events

@@ -65,6 +65,7 @@ SIGNATURES = {
     "hmx_hmatrix_load": (C.c_int, [P, i32, i64, P, P, i64, P, PP, PP, C.POINTER(P)]),
     "hmx_hmatrix_stats": (C.c_int, [P, C.POINTER(HmxStats)]),
     "hmx_hmatrix_block_info": (C.c_int, [P, P, P, P, P]),
+    "hmx_hmatrix_set_block_info": (C.c_int, [P, P, P, P]),
     "hmx_hmatrix_get_block": (C.c_int, [P, i64, P, P]),
     "hmx_hmatrix_device_layout": (C.c_int, [P, P, P, P, P]),
     "hmx_block_errors": (C.c_int, [P, P, P, P, i64, C.c_double, P, P]),
@@ -74,6 +75,7 @@ SIGNATURES = {
     "hmx_truncate_batch": (C.c_int, [P, i64, P, P, P, P, P, P, P, f64, i32, P, P]),
     "hmx_hmatrix_free": (None, [P]),
     "hmx_matvec": (C.c_int, [P, P, P, i32]),
+    "hmx_matvec_on": (C.c_int, [P, P, P, i32, u64]),
     "hmx_matvec_profile": (C.c_int, [P, P, P, C.POINTER(C.c_float)]),
     "hmx_profile_begin": (C.c_int, [P]),
     "hmx_profile_end": (C.c_int, [P, C.POINTER(i64), P]),

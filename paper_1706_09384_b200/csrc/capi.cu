@@ -198,11 +198,12 @@ struct DevBuf {
 };
 
 void free_h(DeviceH& H) {
-  void* ptrs[] = {H.d_perm, H.d_row, H.d_v, H.d_s, H.d_xt, H.d_ylev, H.d_xio, H.d_yio, H.d_job1, H.d_tile2};
+  free_workspaces(H);
+  void* ptrs[] = {H.d_perm, H.d_row, H.d_v, H.d_job1, H.d_tile2};
   for (void* p : ptrs)
     if (p) dev_free(*H.ctx, p);
   H.d_perm = nullptr;
-  H.d_row = H.d_v = H.d_s = H.d_xt = H.d_ylev = H.d_xio = H.d_yio = nullptr;
+  H.d_row = H.d_v = nullptr;
   H.d_job1 = nullptr;
   H.d_tile2 = nullptr;
 }
@@ -1194,6 +1195,25 @@ int hmx_hmatrix_block_info(const hmx_hmatrix* h, int64_t* steps, int64_t* rank_b
   return HMX_OK;
 }
 
+int hmx_hmatrix_set_block_info(hmx_hmatrix* h, const int64_t* steps, const int64_t* rank_before,
+                               const int32_t* flags) {
+  if (!h) return HMX_EINVAL;
+  DeviceH& H = h->H;
+  for (int64_t b = 0; b < H.nb; ++b) {
+    if (rank_before && rank_before[b] < H.rank_after[b]) {
+      hmx_set_error("block %lld: rank before recompression %lld < stored rank %lld", (long long)b,
+                    (long long)rank_before[b], (long long)H.rank_after[b]);
+      return HMX_EINVAL;
+    }
+  }
+  for (int64_t b = 0; b < H.nb; ++b) {
+    if (steps) H.steps[b] = steps[b];
+    if (rank_before) H.rank_before[b] = rank_before[b];
+    if (flags) H.flags[b] = flags[b];
+  }
+  return HMX_OK;
+}
+
 int hmx_hmatrix_device_layout(const hmx_hmatrix* h, int64_t* moff, int64_t* ld, int64_t* voff, uint64_t* bufs) {
   if (!h || !moff || !ld || !voff || !bufs) return HMX_EINVAL;
   const DeviceH& H = h->H;
@@ -1307,29 +1327,38 @@ void hmx_hmatrix_free(hmx_hmatrix* h) {
   if (!h) return;
   cudaSetDevice(h->H.ctx->device);
   cudaStreamSynchronize(h->H.ctx->stream);
-  free_h(h->H);
+  free_h(h->H);  // waits for the last matvec of every workspace stream
   delete h;
 }
 
-int hmx_matvec(hmx_hmatrix* h, const double* x, double* y, int32_t mem) {
-  if (!h || !x || !y) return HMX_EINVAL;
+int hmx_matvec_on(hmx_hmatrix* h, const double* x, double* y, int32_t mem, uint64_t stream) {
+  if (!h || !x || !y || (mem != HMX_HOST && mem != HMX_DEVICE)) return HMX_EINVAL;
   DeviceH& H = h->H;
-  Ctx& c = *H.ctx;
-  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  HMX_CUDA_TRY(cudaSetDevice(H.ctx->device));
+  const cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   if (mem == HMX_DEVICE)
-    return matvec_device(H, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y), nullptr);
-  HMX_CUDA_TRY(cudaMemcpyAsync(H.d_xio, x, sizeof(double2) * H.n, cudaMemcpyHostToDevice, c.stream));
-  int rc = matvec_device(H, H.d_xio, H.d_yio, nullptr);
-  if (rc) return rc;
-  HMX_CUDA_TRY(cudaMemcpyAsync(y, H.d_yio, sizeof(double2) * H.n, cudaMemcpyDeviceToHost, c.stream));
-  HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    return matvec_device(H, reinterpret_cast<const double2*>(x), reinterpret_cast<double2*>(y), nullptr, st);
+  int rc = HMX_OK;
+  MvWorkspace* w = mv_workspace(H, st, &rc);
+  if (!w) return rc;
+  std::lock_guard<std::mutex> lk(w->mu);  // the staging buffers are this call's until y is on the host
+  HMX_CUDA_TRY(cudaMemcpyAsync(w->d_xio, x, sizeof(double2) * H.n, cudaMemcpyHostToDevice, st));
+  if ((rc = matvec_enqueue(H, *w, w->d_xio, w->d_yio, nullptr))) return rc;
+  HMX_CUDA_TRY(cudaMemcpyAsync(y, w->d_yio, sizeof(double2) * H.n, cudaMemcpyDeviceToHost, st));
+  HMX_CUDA_TRY(cudaStreamSynchronize(st));
   return HMX_OK;
+}
+
+int hmx_matvec(hmx_hmatrix* h, const double* x, double* y, int32_t mem) {
+  if (!h) return HMX_EINVAL;
+  return hmx_matvec_on(h, x, y, mem, reinterpret_cast<uint64_t>(h->H.ctx->stream));
 }
 
 int hmx_matvec_profile(hmx_hmatrix* h, const double* x_dev, double* y_dev, float* phase_ms) {
   if (!h || !x_dev || !y_dev || !phase_ms) return HMX_EINVAL;
   HMX_CUDA_TRY(cudaSetDevice(h->H.ctx->device));
-  return matvec_device(h->H, reinterpret_cast<const double2*>(x_dev), reinterpret_cast<double2*>(y_dev), phase_ms);
+  return matvec_device(h->H, reinterpret_cast<const double2*>(x_dev), reinterpret_cast<double2*>(y_dev), phase_ms,
+                       h->H.ctx->stream);
 }
 
 int hmx_profile_begin(hmx_hmatrix* h) {
@@ -1392,7 +1421,7 @@ int hmx_gmres(hmx_hmatrix* h, const double* b, double* x, double tol, int32_t re
   }
   std::vector<double> hist;
   int conv = 0;
-  rc = gmres_device(H, db, dx, tol, restart, max_iters, iters, hist, &conv);
+  rc = gmres_device(H, db, dx, tol, restart, max_iters, iters, hist, &conv, c.stream);
   if (rc) return rc;
   if (mem == HMX_HOST) {
     HMX_CUDA_TRY(cudaMemcpyAsync(x, dx, sizeof(double2) * H.n, cudaMemcpyDeviceToHost, c.stream));

@@ -16,6 +16,7 @@
 
 #include <cstdint>
 #include <map>
+#include <memory>
 #include <mutex>
 #include <unordered_map>
 #include <vector>
@@ -62,6 +63,24 @@ struct MvTile2 {
   int32_t nrows;
 };
 
+// Per-stream scratch of the matvec (an assembled H is immutable and
+// safe for concurrent matvec).  The H itself is read-only during a matvec; every
+// buffer a matvec writes lives here, one workspace per launch stream, so calls on
+// different streams never share memory and calls on one stream are ordered by it.
+// `mu` is held while a call enqueues its kernels (two host threads on one stream
+// cannot interleave their launches) and, for host-pointer calls, until the result
+// is back on the host (the staging buffers).
+struct MvWorkspace {
+  cudaStream_t stream = nullptr;
+  double2* d_s = nullptr;     // source slots
+  double2* d_xt = nullptr;    // x in tree order
+  double2* d_ylev = nullptr;  // nlevels x n partial y (rows no tile writes stay 0)
+  double2* d_xio = nullptr;   // device staging for host x / y
+  double2* d_yio = nullptr;
+  cudaEvent_t done = nullptr;  // recorded after every call (freeing the H waits on it)
+  std::mutex mu;
+};
+
 struct DeviceH {
   Ctx* ctx = nullptr;
   int kind = 0, d = 1;
@@ -79,12 +98,10 @@ struct DeviceH {
   int64_t row_elems = 0;
   double2* d_v = nullptr;  // V stream
   int64_t v_elems = 0;
-  double2* d_s = nullptr;  // source slots
   int64_t s_elems = 0;
-  double2* d_xt = nullptr;  // x in tree order
-  double2* d_ylev = nullptr;  // nlevels x n partial y
-  double2* d_xio = nullptr;  // device staging for host x / y
-  double2* d_yio = nullptr;
+  // matvec scratch, one workspace per launch stream (created on first use)
+  std::mutex ws_mu;
+  std::vector<std::unique_ptr<MvWorkspace>> ws;
   MvJob1* d_job1 = nullptr;
   int64_t njob1 = 0;
   MvTile2* d_tile2 = nullptr;
@@ -102,9 +119,6 @@ struct DeviceH {
   bool profiling = false;
   std::vector<cudaEvent_t> prof_events;  // 5 per profiled call
   double phase1_bytes = 0, phase2_bytes = 0;
-  // pinned host staging for host-pointer matvec
-  double2* h_pin_x = nullptr;
-  double2* h_pin_y = nullptr;
 };
 
 // capi.cu: stream-ordered device memory from the context pool (no device-wide
@@ -134,7 +148,16 @@ struct PlanPre {
 };
 void build_plan_pre(const DeviceH& H, PlanPre& pre);
 int build_matvec_plan(DeviceH& H, const PlanPre* pre = nullptr);
-int matvec_device(DeviceH& H, const double2* x_orig_dev, double2* y_orig_dev, float* phase_ms);
+// the workspace of launch stream s (created on first use); nullptr + error set on failure
+MvWorkspace* mv_workspace(DeviceH& H, cudaStream_t s, int* rc);
+void free_workspaces(DeviceH& H);
+// y = A_H x on stream s (device pointers); takes the stream's workspace lock while enqueueing
+// (gate: optional device flag, the launches do nothing while *gate == 0)
+int matvec_device(DeviceH& H, const double2* x_orig_dev, double2* y_orig_dev, float* phase_ms, cudaStream_t s,
+                  const int* gate = nullptr);
+// same with the workspace already locked by the caller
+int matvec_enqueue(DeviceH& H, MvWorkspace& w, const double2* x_orig_dev, double2* y_orig_dev, float* phase_ms,
+                   const int* gate = nullptr);
 
 // dense.cu
 int launch_dense_fill(Ctx& c, const GreenParams& P, const PointsSoA& pts, const int64_t* d_desc, int64_t ndense,
@@ -211,6 +234,6 @@ int bench_read_bw(Ctx& c, double* gbs);
 
 // gmres.cu
 int gmres_device(DeviceH& H, const double2* b_dev, double2* x_dev, double tol, int restart, int64_t max_iters,
-                 int64_t* iters, std::vector<double>& history, int* converged);
+                 int64_t* iters, std::vector<double>& history, int* converged, cudaStream_t s);
 
 }  // namespace hmx

@@ -28,8 +28,11 @@ namespace {
 
 constexpr int kThreads = 256;
 
+// gate (optional): the launch does nothing when *gate == 0 (device-resident GMRES enqueues
+// matvecs ahead of its convergence test; the ones past convergence are skipped on the device)
 __global__ void mv_gather(const double2* __restrict__ x, const int64_t* __restrict__ perm, int d, int64_t np,
-                          double2* __restrict__ xt) {
+                          double2* __restrict__ xt, const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < np * d; k += (int64_t)gridDim.x * blockDim.x) {
     const int64_t p = k / d, a = k - p * d;
     xt[k] = x[d * perm[p] + a];
@@ -43,7 +46,9 @@ __global__ void mv_gather(const double2* __restrict__ x, const int64_t* __restri
 constexpr int kColsPerJob = 4;  // 8 measured 13% slower (fewer, longer jobs)
 __global__ void __launch_bounds__(kThreads) mv_phase1(const MvJob1* __restrict__ jobs, int64_t njobs,
                                                          const double2* __restrict__ V,
-                                                         const double2* __restrict__ xt, double2* __restrict__ s) {
+                                                         const double2* __restrict__ xt, double2* __restrict__ s,
+                                                         const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   const int lane = threadIdx.x & 31;
   const int64_t wid = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
   const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
@@ -121,7 +126,9 @@ __global__ void __launch_bounds__(kThreads) mv_phase1(const MvJob1* __restrict__
 
 __global__ void __launch_bounds__(kThreads) mv_phase2(const MvTile2* __restrict__ tiles,
                                                       const double2* __restrict__ row,
-                                                      const double2* __restrict__ s, double2* __restrict__ ylev) {
+                                                      const double2* __restrict__ s, double2* __restrict__ ylev,
+                                                      const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   __shared__ double2 red[kThreads];
   const MvTile2 T = tiles[blockIdx.x];
   const int tid = threadIdx.x;
@@ -165,7 +172,8 @@ __global__ void __launch_bounds__(kThreads) mv_phase2(const MvTile2* __restrict_
 }
 
 __global__ void mv_finalize(const double2* __restrict__ ylev, int64_t nlev, int64_t n, const int64_t* __restrict__ perm,
-                            int d, double2* __restrict__ y) {
+                            int d, double2* __restrict__ y, const int* __restrict__ gate) {
+  if (gate && *gate == 0) return;
   for (int64_t k = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; k < n; k += (int64_t)gridDim.x * blockDim.x) {
     double2 t = ylev[k];
     for (int64_t l = 1; l < nlev; ++l) t = cadd(t, ylev[l * n + k]);
@@ -333,12 +341,11 @@ int build_matvec_plan(DeviceH& H, const PlanPre* pre_in) {
   HMX_CUDA_TRY(dev_alloc_t(c, &H.d_row, (size_t)(std::max<int64_t>(H.row_elems, 1))));
   HMX_CUDA_TRY(dev_alloc_t(c, &H.d_v, (size_t)(std::max<int64_t>(H.v_elems, 1))));
   tick("malloc row + V");
-  HMX_CUDA_TRY(dev_alloc_t(c, &H.d_s, (size_t)(std::max<int64_t>(H.s_elems, 1))));
-  HMX_CUDA_TRY(dev_alloc_t(c, &H.d_xt, (size_t)(H.n)));
-  HMX_CUDA_TRY(dev_alloc_t(c, &H.d_ylev, (size_t)(H.n * H.nlevels)));
-  HMX_CUDA_TRY(cudaMemsetAsync(H.d_ylev, 0, sizeof(double2) * H.n * H.nlevels, c.stream));
-  HMX_CUDA_TRY(dev_alloc_t(c, &H.d_xio, (size_t)(H.n)));
-  HMX_CUDA_TRY(dev_alloc_t(c, &H.d_yio, (size_t)(H.n)));
+  // the context stream's matvec workspace up front (other streams get theirs on first use)
+  {
+    int rc = HMX_OK;
+    if (!mv_workspace(H, c.stream, &rc)) return rc;
+  }
   HMX_CUDA_TRY(dev_alloc_t(c, &H.d_job1, (size_t)(std::max<int64_t>(H.njob1, 1))));
   HMX_CUDA_TRY(dev_alloc_t(c, &H.d_tile2, (size_t)(std::max<int64_t>(H.ntile2, 1))));
   if (H.njob1)
@@ -351,29 +358,82 @@ int build_matvec_plan(DeviceH& H, const PlanPre* pre_in) {
   return HMX_OK;
 }
 
-int matvec_device(DeviceH& H, const double2* x, double2* y, float* phase_ms) {
+MvWorkspace* mv_workspace(DeviceH& H, cudaStream_t s, int* rc) {
+  std::lock_guard<std::mutex> lk(H.ws_mu);
+  for (auto& w : H.ws)
+    if (w->stream == s) return w.get();
   Ctx& c = *H.ctx;
+  auto w = std::make_unique<MvWorkspace>();
+  w->stream = s;
+  cudaError_t e = cudaSuccess;
+  if (e == cudaSuccess) e = dev_alloc_t(c, &w->d_s, (size_t)(std::max<int64_t>(H.s_elems, 1)));
+  if (e == cudaSuccess) e = dev_alloc_t(c, &w->d_xt, (size_t)H.n);
+  if (e == cudaSuccess) e = dev_alloc_t(c, &w->d_ylev, (size_t)(H.n * H.nlevels));
+  if (e == cudaSuccess) e = cudaMemsetAsync(w->d_ylev, 0, sizeof(double2) * H.n * H.nlevels, s);
+  if (e == cudaSuccess) e = dev_alloc_t(c, &w->d_xio, (size_t)H.n);
+  if (e == cudaSuccess) e = dev_alloc_t(c, &w->d_yio, (size_t)H.n);
+  if (e == cudaSuccess) e = cudaEventCreateWithFlags(&w->done, cudaEventDisableTiming);
+  if (e != cudaSuccess) {
+    hmx_set_error("matvec workspace: %s", cudaGetErrorString(e));
+    cudaGetLastError();
+    for (void* p : {(void*)w->d_s, (void*)w->d_xt, (void*)w->d_ylev, (void*)w->d_xio, (void*)w->d_yio})
+      dev_free(c, p);
+    *rc = e == cudaErrorMemoryAllocation ? HMX_ENOMEM : HMX_ECUDA;
+    return nullptr;
+  }
+  H.ws.push_back(std::move(w));
+  return H.ws.back().get();
+}
+
+void free_workspaces(DeviceH& H) {
+  std::lock_guard<std::mutex> lk(H.ws_mu);
+  for (auto& w : H.ws) {
+    std::lock_guard<std::mutex> lw(w->mu);  // no call of another thread still enqueueing
+    if (w->done) {
+      cudaEventSynchronize(w->done);
+      cudaEventDestroy(w->done);
+    }
+    for (void* p : {(void*)w->d_s, (void*)w->d_xt, (void*)w->d_ylev, (void*)w->d_xio, (void*)w->d_yio})
+      dev_free(*H.ctx, p);
+  }
+  H.ws.clear();
+}
+
+int matvec_device(DeviceH& H, const double2* x, double2* y, float* phase_ms, cudaStream_t s, const int* gate) {
+  int rc = HMX_OK;
+  MvWorkspace* w = mv_workspace(H, s, &rc);
+  if (!w) return rc;
+  std::lock_guard<std::mutex> lk(w->mu);
+  return matvec_enqueue(H, *w, x, y, phase_ms, gate);
+}
+
+int matvec_enqueue(DeviceH& H, MvWorkspace& W, const double2* x, double2* y, float* phase_ms, const int* gate) {
+  Ctx& c = *H.ctx;
+  const cudaStream_t st = W.stream;
   cudaEvent_t ev[5];
-  const bool timed = phase_ms != nullptr || H.profiling;
+  const bool prof = H.profiling;  // diagnostic (hmx_profile_begin/end): one stream at a time
+  const bool timed = phase_ms != nullptr || prof;
   if (timed) {
     for (int i = 0; i < 5; ++i) HMX_CUDA_TRY(cudaEventCreate(&ev[i]));
-    HMX_CUDA_TRY(cudaEventRecord(ev[0], c.stream));
+    HMX_CUDA_TRY(cudaEventRecord(ev[0], st));
   }
   const int eg = std::max<int64_t>(1, std::min<int64_t>(hmx_cdiv(H.n, kThreads), 4 * c.num_sms));
-  mv_gather<<<eg, kThreads, 0, c.stream>>>(x, H.d_perm, H.d, H.np, H.d_xt);
-  if (timed) HMX_CUDA_TRY(cudaEventRecord(ev[1], c.stream));
+  mv_gather<<<eg, kThreads, 0, st>>>(x, H.d_perm, H.d, H.np, W.d_xt, gate);
+  if (timed) HMX_CUDA_TRY(cudaEventRecord(ev[1], st));
   if (H.njob1) {
     const int64_t warps = std::min<int64_t>(H.njob1, (int64_t)c.num_sms * 64);  // 8 CTAs x 8 warps per SM
-    mv_phase1<<<(unsigned)hmx_cdiv(warps * 32, kThreads), kThreads, 0, c.stream>>>(H.d_job1, H.njob1, H.d_v, H.d_xt,
-                                                                                   H.d_s);
+    mv_phase1<<<(unsigned)hmx_cdiv(warps * 32, kThreads), kThreads, 0, st>>>(H.d_job1, H.njob1, H.d_v, W.d_xt,
+                                                                             W.d_s, gate);
   }
-  if (timed) HMX_CUDA_TRY(cudaEventRecord(ev[2], c.stream));
-  if (H.ntile2) mv_phase2<<<(unsigned)H.ntile2, kThreads, 0, c.stream>>>(H.d_tile2, H.d_row, H.d_s, H.d_ylev);
-  if (timed) HMX_CUDA_TRY(cudaEventRecord(ev[3], c.stream));
-  mv_finalize<<<eg, kThreads, 0, c.stream>>>(H.d_ylev, H.nlevels, H.n, H.d_perm, H.d, y);
+  if (timed) HMX_CUDA_TRY(cudaEventRecord(ev[2], st));
+  if (H.ntile2) mv_phase2<<<(unsigned)H.ntile2, kThreads, 0, st>>>(H.d_tile2, H.d_row, W.d_s, W.d_ylev, gate);
+  if (timed) HMX_CUDA_TRY(cudaEventRecord(ev[3], st));
+  mv_finalize<<<eg, kThreads, 0, st>>>(W.d_ylev, H.nlevels, H.n, H.d_perm, H.d, y, gate);
   HMX_CUDA_TRY(cudaGetLastError());
-  if (timed) HMX_CUDA_TRY(cudaEventRecord(ev[4], c.stream));
-  if (H.profiling && !phase_ms) {
+  HMX_CUDA_TRY(cudaEventRecord(W.done, st));
+  if (timed) HMX_CUDA_TRY(cudaEventRecord(ev[4], st));
+  if (prof && !phase_ms) {
+    std::lock_guard<std::mutex> lk(H.ws_mu);
     H.prof_events.insert(H.prof_events.end(), ev, ev + 5);
   } else if (phase_ms) {
     HMX_CUDA_TRY(cudaEventSynchronize(ev[4]));

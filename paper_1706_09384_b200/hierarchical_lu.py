@@ -171,7 +171,7 @@ _PEND_FLUSH = 400     # pending columns on one low-rank target before it is trun
 _AGGLO_MAX = 512      # agglomerated product columns before an intermediate truncation
 # pairs whose kernel problem would have more columns than this are truncated by cuSOLVER QR + SVD
 # instead (the one-CTA eigen-solve of a K x K problem is latency-bound, O(K) dependent phases)
-_CUSOLVER_K = int(os.environ.get("HMX_HLU_CUSOLVER_K", "1021"))
+_CUSOLVER_K = 1020   # hmx_truncate_batch accepts K <= 1020 (capi.cu hmx_truncate_batch)
 # pairs whose kernel problem would exceed this many columns go through a _SKETCH_L-column range sketch
 _SKETCH_K = int(os.environ.get("HMX_HLU_SKETCH_K", "112"))
 _SKETCH_L = 112
@@ -222,13 +222,24 @@ def _kernel_batch(ar, items, eps=None):
                                               _TRULES[ar.rule],
                                               _lib.ptr(ranks), _lib.ptr(flags)), "hmx_truncate_batch")
     ar.t_trunc += time.perf_counter() - t0
-    res = []
-    for i, (uo, vo) in enumerate(outs):
-        if flags[i] & 1:
-            res.append(None)
-            continue
+    # compact copy of the kept columns (one allocation sized sum r (dm + dn)): the truncated
+    # leaves then keep only their final-rank storage alive, not the K-column batch buffer
+    kept = [i for i in range(n) if not flags[i] & 1]
+    pieces = []
+    for i in kept:
         r = int(ranks[i])
-        res.append((uo[:r].mT, vo[:r].mT))
+        pieces += [outs[i][0][:r].reshape(-1), outs[i][1][:r].reshape(-1)]
+    flat = torch.cat(pieces) if pieces else None
+    del out, outs[:]
+    res = [None] * n
+    o = 0
+    for i in kept:
+        r, m_, n_ = int(ranks[i]), int(dm[i]), int(dn[i])
+        u = flat[o:o + r * m_].view(r, m_).mT
+        o += r * m_
+        v = flat[o:o + r * n_].view(r, n_).mT
+        o += r * n_
+        res[i] = (u, v)
     return res
 
 
@@ -800,6 +811,14 @@ def _umul(ar, U, X):
     return out
 
 
+def _drop_images(x):
+    if isinstance(x, Sub):
+        x.dc = None
+        for row in x.ch:
+            for c in row:
+                _drop_images(c)
+
+
 def _walk(x):
     if isinstance(x, Sub):
         for row in x.ch:
@@ -837,6 +856,15 @@ def _leaf_index(bt):
     return {(int(t[5]), int(t[6])): b for b, t in enumerate(bt.table)}
 
 
+def _own_copy(view):
+    """A private contiguous copy of a view of the assembly's HBM streams.  ``.contiguous()`` is not
+    enough: torch returns the view itself when it is already contiguous (a 1-row or 1-column block),
+    and the in-place Schur updates would then write into the immutable source H."""
+    out = _torch().empty(view.shape, dtype=view.dtype, device=view.device)
+    out.copy_(view)
+    return out
+
+
 def copy_hmatrix(h, block_tree=None):
     """Device node tree holding a private copy of every leaf of the assembled H
     (zero-copy views of the HBM streams, cloned)."""
@@ -863,16 +891,16 @@ def copy_hmatrix(h, block_tree=None):
         dm, dn = d * (r1 - r0), d * (c1 - c0)
         o, l = int(moff[b]), int(ld[b])
         if k == 0:
-            a = R[o:o + l * dn].view(dn, l)[:, :dm].transpose(0, 1).contiguous()
+            a = _own_copy(R[o:o + l * dn].view(dn, l)[:, :dm].transpose(0, 1))
             return Dense(d * r0, d * r1, d * c0, d * c1, a)
         r = int(ranks[b])
         if r == 0:
             u = torch.zeros((dm, 0), dtype=torch.complex128, device=dev)
             v = torch.zeros((dn, 0), dtype=torch.complex128, device=dev)
         else:
-            u = R[o:o + l * r].view(r, l)[:, :dm].transpose(0, 1).contiguous()
+            u = _own_copy(R[o:o + l * r].view(r, l)[:, :dm].transpose(0, 1))
             vo = int(voff[b])
-            v = Vs[vo:vo + dn * r].view(r, dn).transpose(0, 1).contiguous()
+            v = _own_copy(Vs[vo:vo + dn * r].view(r, dn).transpose(0, 1))
         return LowRank(d * r0, d * r1, d * c0, d * c1, u, v)
 
     return _build(bt.root, d, _leaf_index(bt), make_leaf)
@@ -980,6 +1008,7 @@ def hlu(h, eps_lu, rule="frobenius", block_tree=None):
     ar = Arith(float(eps_lu), rule)
     _lu(ar, root, ())
     _flush_batch(ar, [root])
+    _drop_images(root)   # the dense operand images were factorisation workspace, not factor storage
     torch.cuda.synchronize()
     t2 = time.perf_counter()
     f = LUFactors(lower=_Tri(root, True), upper=_Tri(root, False), eps_lu=float(eps_lu), d=h.d,

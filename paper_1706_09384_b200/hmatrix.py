@@ -95,8 +95,10 @@ class HMatrix:
         return LowRankFactor(u, v)
 
     def use_stream(self, stream_ptr):
-        """Launch on an external cudaStream_t (e.g. torch.cuda.current_stream().cuda_stream)."""
-        _lib.bind_stream(self.device, stream_ptr)
+        """Default launch stream of this H's matvecs (a cudaStream_t such as
+        torch.cuda.current_stream().cuda_stream); a per-H setting, not process state.
+        ``matvec(h, x, stream=...)`` overrides it per call."""
+        self._stream = None if stream_ptr is None else int(stream_ptr)
 
     @classmethod
     def from_factors(cls, d, n_points, perm, table, payload, device=0):
@@ -206,24 +208,33 @@ def _is_cuda_tensor(x):
     return hasattr(x, "is_cuda") and bool(getattr(x, "is_cuda", False))
 
 
-def matvec(h, x, out=None):
+def matvec(h, x, out=None, stream=None):
     """y = A_H x; x in original point order.  numpy in ->
     numpy out (host copies inside); a CUDA complex128 torch tensor in -> a
-    CUDA tensor out (no host round trip)."""
+    CUDA tensor out (no host round trip), launched on ``stream`` (a
+    cudaStream_t; default: torch's current stream, so the result is ordered
+    with the caller's torch work).  Safe to call concurrently on one H from
+    several threads / streams (``hmx_matvec_on``)."""
     n = h.d * h.n_points
+    if stream is None:
+        stream = getattr(h, "_stream", None)
     if _is_cuda_tensor(x):
         import torch
 
         if x.dtype != torch.complex128 or x.numel() != n or not x.is_contiguous():
             raise ValueError("dimension mismatch")
         y = torch.empty_like(x) if out is None else out
-        _lib.bind_torch_stream(h.device)  # stream-ordered with the caller's torch work
-        _lib.check(_lib.lib().hmx_matvec(h.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), DEVICE),
-                   "hmx_matvec")
+        if stream is None:
+            stream = torch.cuda.current_stream(x.device).cuda_stream
+        _lib.check(_lib.lib().hmx_matvec_on(h.handle, C.c_void_p(x.data_ptr()), C.c_void_p(y.data_ptr()), DEVICE,
+                                            int(stream)), "hmx_matvec")
         return y
     x = np.ascontiguousarray(x, dtype=np.complex128)
     if x.shape != (n,):
         raise ValueError("dimension mismatch")
     y = np.empty_like(x) if out is None else out
-    _lib.check(_lib.lib().hmx_matvec(h.handle, _lib.ptr(x), _lib.ptr(y), HOST), "hmx_matvec")
+    if stream is None:
+        _lib.check(_lib.lib().hmx_matvec(h.handle, _lib.ptr(x), _lib.ptr(y), HOST), "hmx_matvec")
+    else:
+        _lib.check(_lib.lib().hmx_matvec_on(h.handle, _lib.ptr(x), _lib.ptr(y), HOST, int(stream)), "hmx_matvec")
     return y

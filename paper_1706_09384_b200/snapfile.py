@@ -5,14 +5,21 @@
 Layout (little endian)::
 
     b"HMXSNAP\\0" | u32 version | u64 header length | header (JSON)
-    | arrays: perm, table (nb x 5), steps, rank_before, rank_after, flags
+    | arrays: perm, table (nb x 7: kind, r0, r1, c0, c1, row node, col node),
+      steps, rank_before, rank_after, flags
+      [+ version 2 with a block tree: the cluster tree (nodes nn x 5, boxes nn x 6)
+       and the cloud (points N x 3, normals N x 3 when present)]
     | payload: every leaf in leaves() order -- dense (d m) x (d n), or
       U (d m) x r then V (d n) x r, complex128 row-major
     | SHA-256 of everything before it (32 bytes)
 
 ``load`` rebuilds the device H-matrix through ``hmx_hmatrix_load`` with the
 same leaf table and ranks, so the streams, the matvec plan and therefore the
-matvec output are bitwise identical to the saved H-matrix's.  Errors
+matvec output are bitwise identical to the saved H-matrix's; the per-leaf
+assembly record (ACA steps, rank before recompression, flags) is restored
+through ``hmx_hmatrix_set_block_info`` and, for version 2, the block tree is
+rebuilt so ``storage_report`` and ``hlu`` work on a loaded H.  Version 1
+files (no tree) still load.  Errors
 (``errors.py:23-32``): wrong magic / version -> ``SnapshotVersionError``,
 checksum or size mismatch -> ``SnapshotCorruptError``.
 """
@@ -29,8 +36,10 @@ from .hmatrix import HMatrix
 from .kernels import KernelSpec, Material
 
 MAGIC = b"HMXSNAP\0"
-VERSION = 1
+VERSION = 2
+_READS = (1, 2)
 _ARRAYS = ("perm", "table", "steps", "rank_before", "rank_after", "flags")
+_TREE_ARRAYS = ("nodes", "boxes", "points", "normals")
 
 
 def _spec_json(spec):
@@ -62,12 +71,26 @@ class _HashWriter:
 def save(h, path):
     """Write ``h`` to ``path``."""
     info = h.block_info()
-    table = np.ascontiguousarray(np.asarray(h.table)[:, :5], dtype=np.int64)
+    table = np.asarray(h.table)
+    if table.shape[1] < 7:   # no node columns (an imported H without a tree)
+        table = np.concatenate([table[:, :5], np.full((len(table), 2), -1, np.int64)], axis=1)
+    table = np.ascontiguousarray(table[:, :7], dtype=np.int64)
     perm = np.ascontiguousarray(h.perm, dtype=np.int64)
     arrays = {"perm": perm, "table": table, "steps": info["steps"], "rank_before": info["rank_before"],
               "rank_after": info["rank_after"], "flags": info["flags"]}
+    bt = h.block_tree
+    tree = None
+    if bt is not None and (bt.rows is bt.cols or np.array_equal(bt.rows.permutation, bt.cols.permutation)):
+        ct = bt.rows
+        tree = {"n_leaf": int(ct.n_leaf), "eta": float(bt.eta), "has_normals": ct.cloud.normals is not None,
+                "cloud_d": int(ct.cloud.d)}
+        arrays["nodes"] = np.ascontiguousarray(ct.nodes_array, dtype=np.int64)
+        arrays["boxes"] = np.ascontiguousarray(ct.boxes_array, dtype=np.float64)
+        arrays["points"] = np.ascontiguousarray(ct.cloud.points, dtype=np.float64)
+        if ct.cloud.normals is not None:
+            arrays["normals"] = np.ascontiguousarray(ct.cloud.normals, dtype=np.float64)
     header = {"d": h.d, "n_points": h.n_points, "n_blocks": len(table), "self_shift": h.self_shift,
-              "spec": _spec_json(h.spec),
+              "spec": _spec_json(h.spec), "tree": tree,
               "arrays": {k: {"dtype": str(v.dtype), "shape": list(v.shape)} for k, v in arrays.items()}}
     hb = json.dumps(header, sort_keys=True).encode()
     with open(path, "wb") as f:
@@ -75,8 +98,9 @@ def save(h, path):
         w.write(MAGIC)
         w.write(struct.pack("<IQ", VERSION, len(hb)))
         w.write(hb)
-        for k in _ARRAYS:
-            w.write(np.ascontiguousarray(arrays[k]).tobytes())
+        for k in _ARRAYS + _TREE_ARRAYS:
+            if k in arrays:
+                w.write(np.ascontiguousarray(arrays[k]).tobytes())
         for b in range(len(table)):
             p = h.block(b)
             if table[b, 0] == 0:
@@ -95,8 +119,8 @@ def load(path, device=0):
     if len(raw) < len(MAGIC) + 12 + 32 or raw[:len(MAGIC)] != MAGIC:
         raise SnapshotVersionError("not an hmx snapshot")
     version, hlen = struct.unpack_from("<IQ", raw, len(MAGIC))
-    if version != VERSION:
-        raise SnapshotVersionError(f"snapshot version {version}, this build reads {VERSION}")
+    if version not in _READS:
+        raise SnapshotVersionError(f"snapshot version {version}, this build reads {_READS}")
     body, digest = raw[:-32], raw[-32:]
     if hashlib.sha256(body).digest() != digest:
         raise SnapshotCorruptError("snapshot checksum mismatch")
@@ -106,11 +130,16 @@ def load(path, device=0):
     if header.get("kind") == "lu":
         return _load_lu(header, buf, len(body), device)
     arrays = {}
-    for k in _ARRAYS:
-        meta = header["arrays"][k]
+    for k in _ARRAYS + _TREE_ARRAYS:
+        meta = header["arrays"].get(k)
+        if meta is None:
+            continue
         dt = np.dtype(meta["dtype"])
         n = int(np.prod(meta["shape"])) if meta["shape"] else 1
-        arrays[k] = np.frombuffer(buf.read(n * dt.itemsize), dtype=dt).reshape(meta["shape"])
+        raw_k = buf.read(n * dt.itemsize)
+        if len(raw_k) != n * dt.itemsize:
+            raise SnapshotCorruptError("snapshot payload size mismatch")
+        arrays[k] = np.frombuffer(raw_k, dtype=dt).reshape(meta["shape"])
     d, table, ranks = header["d"], arrays["table"], arrays["rank_after"]
     payload = []
     for b in range(len(table)):
@@ -125,8 +154,25 @@ def load(path, device=0):
     if buf.tell() != len(body):
         raise SnapshotCorruptError("snapshot payload size mismatch")
     H = HMatrix.from_factors(d, header["n_points"], arrays["perm"], table, payload, device=device)
+    from . import _lib
+
+    steps = np.ascontiguousarray(arrays["steps"], dtype=np.int64)
+    rb = np.ascontiguousarray(arrays["rank_before"], dtype=np.int64)
+    fl = np.ascontiguousarray(arrays["flags"], dtype=np.int32)
+    _lib.check(_lib.lib().hmx_hmatrix_set_block_info(H.handle, _lib.ptr(steps), _lib.ptr(rb), _lib.ptr(fl)),
+               "hmx_hmatrix_set_block_info")
     H.spec = _spec_from(header["spec"])
     H.self_shift = header["self_shift"]
+    tree = header.get("tree")
+    if tree is not None and table.shape[1] >= 7:
+        from .geometry import BlockTree, PointCloud, cluster_tree_from_arrays
+
+        cloud = PointCloud(np.array(arrays["points"]), None if "normals" not in arrays else np.array(arrays["normals"]),
+                           d=tree["cloud_d"])
+        ct = cluster_tree_from_arrays(cloud, np.array(arrays["perm"]), np.array(arrays["nodes"]),
+                                      np.array(arrays["boxes"]), tree["n_leaf"])
+        H.block_tree = BlockTree(rows=ct, cols=ct, table=np.ascontiguousarray(table, dtype=np.int64), eta=tree["eta"])
+        H.table = H.block_tree.table
     return H
 
 

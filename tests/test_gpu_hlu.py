@@ -150,6 +150,21 @@ def test_source_h_unchanged():
     assert np.array_equal(hmx.matvec(H, b), y0)
 
 
+def test_source_h_unchanged_one_point_leaves():
+    """d = 1 with one-point leaves: 1 x n / m x 1 leaf views of the HBM streams are already contiguous,
+    and the H-LU must still copy them (in-place Schur updates would otherwise write into H)."""
+    cl = hmx.make_geometry("sphere", 96, 1.0, d=1)
+    ct = hmx.build_cluster_tree(cl, 1)
+    bt = hmx.build_block_tree(ct, ct, 3.0)
+    H, _ = hmx.assemble(hmx.KernelSpec.helmholtz(2.0), cl, ct, bt, hmx.ACAConfig(eps_aca=1e-6))
+    b = _rand(96, 21)
+    y0 = hmx.matvec(H, b)
+    f = HL.hlu(H, 1e-6)
+    assert np.array_equal(hmx.matvec(H, b), y0)
+    x = hmx.triangular_solve(f, b)
+    assert np.linalg.norm(hmx.matvec(H, x) - b) <= 1e-4 * np.linalg.norm(b)
+
+
 def test_single_leaf_is_dense_lu():
     """a 1-leaf H-matrix reduces to the pivoted dense LU (machine-precision residual)."""
     from dataclasses import replace

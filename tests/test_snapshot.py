@@ -54,6 +54,12 @@ def test_round_trip_bitwise(tmp_path, tag, n):
             np.testing.assert_array_equal(p1.u, p2.u)
             np.testing.assert_array_equal(p1.v, p2.v)
     assert H2.stats()["n_stored"] == H.stats()["n_stored"]
+    # the assembly record and the block tree travel with the snapshot
+    i1, i2 = H.block_info(), H2.block_info()
+    for k in ("steps", "rank_before", "rank_after", "flags"):
+        np.testing.assert_array_equal(i1[k], i2[k])
+    assert hmx.storage_report(H2) == hmx.storage_report(H)
+    np.testing.assert_array_equal(H2.block_tree.table, H.block_tree.table)
     # the loaded H carries its kernel: the estimator regenerates the same leaves
     e1, _ = hmx.block_errors(H, pb.spec, pb.cloud)
     e2, _ = hmx.block_errors(H2, H2.spec, pb.cloud)
@@ -63,3 +69,17 @@ def test_round_trip_bitwise(tmp_path, tag, n):
     r2 = hmx.solve_gmres(H2, pb.rhs(4), hmx.GmresConfig(tol=1e-6))
     assert r1.iters == r2.iters
     np.testing.assert_array_equal(r1.x, r2.x)
+
+
+@pytest.mark.gpu
+def test_loaded_h_factorises(tmp_path):
+    """hlu needs the block tree: a snapshot carries it (version 2)."""
+    pb = Problem("H4k", 1024)
+    H, _ = pb.device_h()
+    path = str(tmp_path / "h.hmx")
+    hmx.snapshot("save", path, H)
+    H2 = hmx.snapshot("load", path)
+    f1 = hmx.hlu(H, 1e-6)
+    f2 = hmx.hlu(H2, 1e-6)
+    b = pb.rhs(5)
+    np.testing.assert_array_equal(hmx.triangular_solve(f1, b), hmx.triangular_solve(f2, b))
