@@ -7,6 +7,9 @@ travel to the GPU box, the reference does not).
 * geometry_<case>.npz : permutation + leaf table (kind, r0, r1, c0, c1) of the
   reference ``build_cluster_tree`` / ``build_block_tree`` / ``leaves()``
   (geometry.py:182-295) for a few clouds;
+* config_partitions.json : SHA-256 of the reference permutation and leaf table
+  at every BASELINE.json configuration (H4k, U8k, U32k, U131k, T65k), with the
+  leaf counts (the full tables are too large to commit);
 * kernels.npz : outputs of the reference kernel core
   (_kernelcore_np.py:37-130) on seeded points, with and without coincident
   pairs / self shift.
@@ -36,6 +39,30 @@ def leaf_table(bt):
                       l.col.stop) for l in bt.leaves()], dtype=np.int64)
 
 
+def config_partitions():
+    """Reference tree + partition at the five BASELINE sizes (geometry.py:182-295)."""
+    import hashlib
+    import json
+
+    cases = {"H4k": (4096, 32), "U8k": (8192, 32), "U32k": (32768, 32), "U131k": (131072, 64),
+             "T65k": (65536, 32)}
+    out = {}
+    for tag, (n, leaf) in cases.items():
+        cl = G.make_geometry("sphere", n, 1.0)
+        ct = G.build_cluster_tree(cl, leaf)
+        bt = G.build_block_tree(ct, ct, 3.0)
+        perm = np.ascontiguousarray(ct.permutation.astype("<i8"))
+        tab = np.ascontiguousarray(leaf_table(bt).astype("<i8"))
+        out[tag] = {"n_points": n, "n_leaf": leaf, "eta": 3.0,
+                    "perm_sha256": hashlib.sha256(perm.tobytes()).hexdigest(),
+                    "table_sha256": hashlib.sha256(tab.tobytes()).hexdigest(),
+                    "n_leaves": int(len(tab)), "n_admissible": int((tab[:, 0] == 1).sum()),
+                    "depth": int(ct.depth), "c_sp": int(G.sparsity_pattern(bt))}
+        print(tag, out[tag])
+    with open(os.path.join(HERE, "config_partitions.json"), "w") as f:
+        json.dump(out, f, indent=1)
+
+
 def main():
     for name, (kind, n, leaf, eta) in GEOMETRY_CASES.items():
         cl = G.make_geometry(kind, n, 1.0)
@@ -58,6 +85,7 @@ def main():
     out["T"] = R.elasto_t_block(26.197, 45.375, 1.0, 1.0, 1 / 45.375**2, X, Y, NY, self_shift=65536.0)
     out["H_none_is_none"] = np.array(R.scalar_block(11.3, X, Y) is None)
     np.savez_compressed(os.path.join(HERE, "kernels.npz"), **out)
+    config_partitions()
     print("golden fixtures written to", HERE)
 
 

@@ -116,3 +116,29 @@ def test_errors():
         hmx.PointCloud(np.zeros((0, 3)))
     with pytest.raises(ValueError):
         hmx.make_geometry("cube", 10)
+
+
+def _config_partitions():
+    import json
+
+    with open(os.path.join(GOLD, "config_partitions.json")) as f:
+        return json.load(f)
+
+
+@pytest.mark.parametrize("tag", ["H4k", "U8k", "U32k", "U131k", "T65k"])
+def test_native_partition_matches_reference_at_baseline_configs(tag):
+    """Permutation and full leaf list at every BASELINE.json size are bit-exact with the
+    reference build_cluster_tree / build_block_tree / leaves() (geometry.py:182-295): SHA-256
+    of the reference's arrays, generated by tests/golden/make_golden.py."""
+    import hashlib
+
+    g = _config_partitions()[tag]
+    cl = hmx.make_geometry("sphere", g["n_points"], 1.0)
+    ct = hmx.build_cluster_tree(cl, g["n_leaf"])
+    bt = hmx.build_block_tree(ct, ct, g["eta"])
+    perm = np.ascontiguousarray(np.asarray(ct.permutation).astype("<i8"))
+    tab = np.ascontiguousarray(np.asarray(bt.leaf_table).astype("<i8"))
+    assert len(tab) == g["n_leaves"] and int((tab[:, 0] == 1).sum()) == g["n_admissible"]
+    assert hashlib.sha256(perm.tobytes()).hexdigest() == g["perm_sha256"]
+    assert hashlib.sha256(tab.tobytes()).hexdigest() == g["table_sha256"]
+    assert ct.depth == g["depth"] and hmx.sparsity_pattern(bt) == g["c_sp"]
