@@ -30,13 +30,13 @@
 extern "C" {
 #endif
 
-#define HMX_ABI_VERSION 1
+#define HMX_ABI_VERSION 2
 
 /* status codes */
 #define HMX_OK 0
 #define HMX_EINVAL 1    /* invalid argument / dimension mismatch (ValueError)          */
 #define HMX_ECUDA 2     /* CUDA runtime failure                                        */
-#define HMX_EPIVOT 3    /* FallbackNeeded with no device fallback (PivotExhaustionError) */
+#define HMX_EPIVOT 3    /* pivot exhaustion after the randomized-SVD fallback also failed (PivotExhaustionError) */
 #define HMX_ESINGULAR 4 /* r == 0 pair without a self rule (SingularEvaluationError)     */
 #define HMX_ENOMEM 5    /* device memory budget exceeded                               */
 
@@ -48,6 +48,10 @@ extern "C" {
 /* recompression truncation rules (oracle/lowrank.py decision 8) */
 #define HMX_TRUNC_FROBENIUS 0
 #define HMX_TRUNC_SPECTRAL 1
+
+/* ACA kernel selection for the wide (m + n >= 320 points) d = 3 leaves */
+#define HMX_ACA_KERNEL_AUTO 0      /* tensor-core (DMMA) ACA, CUDA-core when its ring does not fit */
+#define HMX_ACA_KERNEL_CUDA_CORE 1 /* CUDA-core ACA only                                          */
 
 /* memory location of vector arguments */
 #define HMX_HOST 0
@@ -72,8 +76,12 @@ typedef struct {
   int64_t max_rank;      /* <= 0: min(d m, d n) per block */
   double sigma3_floor;   /* relative sigma_3 floor, default 1e-12 */
   int32_t trunc_rule;    /* HMX_TRUNC_* */
-  int32_t pad;
+  int32_t aca_kernel;    /* HMX_ACA_KERNEL_* */
   double mem_budget_gb;  /* ACA workspace budget; <= 0: 70% of free (+ cached) device memory */
+  int32_t tc_stages;     /* tensor-core ACA copy ring depth: 0 = deepest that fits, 2 or 3 */
+  int32_t certify;       /* 1: after assembly, regenerate every admissible leaf, re-compress the
+                            ones above eps until ||A_b - U V^H||_F <= eps ||A_b||_F (north_star) */
+  int64_t rsvd_seed;     /* seed of the Gaussian test matrices of the randomized-SVD fallback */
 } hmx_aca_cfg;
 
 typedef struct {
@@ -167,6 +175,15 @@ int hmx_aca_block(hmx_ctx* ctx, const hmx_kernel* k, const double* X, int64_t m,
  * Vout (dn x K) row-major with leading dimension *rank <= K */
 int hmx_recompress(hmx_ctx* ctx, int64_t dm, int64_t dn, int64_t K, const double* U, const double* V, double eps,
                    int32_t trunc_rule, int64_t* rank, double* Uout, double* Vout);
+
+/* randomized_svd(dense, eps, oversample) (the FallbackNeeded path of aca_vector,
+ * SPEC.md:302, 384-385): adaptive Gaussian range finder on a dense (m x n) complex row-major block A,
+ * columns 8 + oversample, doubling until ||A - Q Q^H A||_F <= eps ||A||_F or the cap
+ * min(max_rank, m, n) is reached (*converged = 0, a flagged result).  Writes U = Q (m x *k) and
+ * V = (Q^H A)^H (n x *k), row-major with leading dimension *k; U and V hold cap columns.  The same
+ * device routine compresses the flagged leaves inside hmx_assemble. */
+int hmx_rsvd(hmx_ctx* ctx, const double* A, int64_t m, int64_t n, double eps, int32_t oversample, int64_t max_rank,
+             int64_t seed, double* U, double* V, int64_t* k, int32_t* converged);
 
 /* ---- H-matvec / GMRES ---------------------------------------------------------- */
 /* y = A_H x, x and y in ORIGINAL point order (d N complex each) */

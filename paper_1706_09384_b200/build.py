@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "libhmx.so")
-SOURCES = ["capi.cu", "aca.cu", "recompress.cu", "dense.cu", "matvec.cu", "gmres.cu", "estimate.cu", "geometry.cpp"]
+SOURCES = ["capi.cu", "aca.cu", "recompress.cu", "dense.cu", "matvec.cu", "gmres.cu", "estimate.cu", "rsvd.cu", "geometry.cpp"]
 HEADERS = ["hmx_common.cuh", "green.cuh", "hmatrix.h", "hmx_host.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
@@ -45,7 +45,7 @@ def build(force=False, verbose=True):
     with ThreadPoolExecutor(max_workers=len(SOURCES)) as ex:
         objs = list(ex.map(lambda s: _compile(s, force), SOURCES))
     if force or not os.path.exists(LIB) or os.path.getmtime(LIB) < max(os.path.getmtime(o) for o in objs):
-        cmd = [NVCC, "-shared", *ARCH, "-o", LIB, *objs]
+        cmd = [NVCC, "-shared", *ARCH, "-o", LIB, *objs, "-lcublas", "-lcusolver"]
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stderr}")

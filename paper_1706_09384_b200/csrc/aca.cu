@@ -48,7 +48,7 @@ constexpr int kGramGroup = HMX_GRAM_GROUP;  // factor columns per warp in the Gr
 #ifndef HMX_GRAM_BATCH
 #define HMX_GRAM_BATCH 1
 #endif
-constexpr int kGramBatch = HMX_GRAM_BATCH;  // steps per Gram pass (max; HMX_ACA_GRAM_BATCH lowers it)
+constexpr int kGramBatch = HMX_GRAM_BATCH;  // steps per Gram pass (max)
 
 // sigma_1 and sigma_3 of a 3x3 complex matrix from the characteristic
 // polynomial of R^H R: c2 = ||R||_F^2, c1 = sum |2x2 minors|^2 (Cauchy-Binet),
@@ -1196,20 +1196,18 @@ void warm_aca() {
 
 int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const AcaDesc* d_desc, const int32_t* d_order,
                int64_t nblk, int kcap_max, int m_max, double eps, double sigma3_floor, double2* U, double2* V,
-               double2* G, AcaOut* d_out, int variant) {
+               double2* G, AcaOut* d_out, int variant, int tc_stages) {
   if (nblk == 0) return HMX_OK;
   // variant: kAcaWide (512 threads, one CTA per SM: 2-3 CTAs/SM measured
   // 1.4-1.8x slower), kAcaNarrow (128 threads, 4 CTAs per SM: small leaves
   // are latency bound and use few threads per step).
   const int nt = variant == kAcaNarrow ? 128 : 512;
-  const char* e_b = std::getenv("HMX_ACA_GRAM_BATCH");
-  const int batch = e_b ? std::atoi(e_b) : kGramBatch;
+  const int batch = kGramBatch;
   if (variant == kAcaTensor) {
     // 3-stage ring when it fits in shared memory, else 2 stages, else the CUDA-core kernel
     int smem_max = 0;
     HMX_CUDA_TRY(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
-    const char* e_st = std::getenv("HMX_TC_STAGES");
-    const int want = e_st ? std::atoi(e_st) : 3;
+    const int want = tc_stages > 0 ? tc_stages : 3;
     const int stages = want >= 3 && aca_tc_smem(kcap_max, m_max, 3) <= (size_t)smem_max ? 3
                        : aca_tc_smem(kcap_max, m_max, 2) <= (size_t)smem_max ? 2
                                                                                : 0;

@@ -111,6 +111,7 @@ namespace {
 using namespace hmx;
 
 constexpr int kMaxAcaCols = 1020;  // per-leaf ACA column limit (recompress.cu vector sizes)
+constexpr int kRsvdOversample = 10;  // oversampling of the randomized-SVD fallback (oracle/lowrank.py)
 // share of (free + cached) HBM for the ACA workspaces U, V, G: the Grams are released
 // before the final streams are allocated, so U + V + streams stay well inside 180 GB
 constexpr double kAcaBudgetFrac = 0.7;
@@ -197,6 +198,9 @@ struct DevBuf {
   }
 };
 
+int recompress_device(Ctx& c, DevBuf& mem, const double2* dU, const double2* dV, int64_t dm, int64_t dn, int K,
+                      double2* G, double eps, int rule, int* r_out, double2** Uo, double2** Vo);
+
 void free_h(DeviceH& H) {
   free_workspaces(H);
   void* ptrs[] = {H.d_perm, H.d_row, H.d_v, H.d_job1, H.d_tile2};
@@ -280,17 +284,6 @@ int hmx_ctx_create(int32_t device, hmx_ctx** out) {
     HMX_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
     HMX_CUDA_TRY(cudaStreamCreateWithPriority(&c->c.rerun, cudaStreamNonBlocking, hi));
   }
-  // HMX_POOL=1: stream-ordered pool allocations (measured slower for the first
-  // assembly and for T65k on this driver; off by default)
-  if (const char* ep = std::getenv("HMX_POOL"); ep && ep[0] == '1') {
-    cudaMemPoolProps props = {};
-    props.allocType = cudaMemAllocationTypePinned;
-    props.location.type = cudaMemLocationTypeDevice;
-    props.location.id = device;
-    HMX_CUDA_TRY(cudaMemPoolCreate(&c->c.pool, &props));
-    uint64_t keep = UINT64_MAX;
-    HMX_CUDA_TRY(cudaMemPoolSetAttribute(c->c.pool, cudaMemPoolAttrReleaseThreshold, &keep));
-  }
   warm_aca();
   warm_recompress();
   warm_dense();
@@ -334,6 +327,7 @@ int hmx_ctx_destroy(hmx_ctx* ctx) {
   if (ctx->c.aux) cudaStreamDestroy(ctx->c.aux);
   if (ctx->c.rerun) cudaStreamDestroy(ctx->c.rerun);
   if (ctx->c.pool) cudaMemPoolDestroy(ctx->c.pool);
+  linalg_destroy(ctx->c);
   release_cache(ctx->c);
   delete ctx;
   return HMX_OK;
@@ -539,12 +533,10 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   double avail = (double)free_b + (double)c.cached_bytes;
   double budget = cfg->mem_budget_gb > 0 ? cfg->mem_budget_gb * 1e9 : kAcaBudgetFrac * avail;
   auto round_d = [&](int64_t v) { return std::max<int64_t>(d, (v / d) * d); };
-  const char* e_nm0 = std::getenv("HMX_ACA_NARROW_MAX");
-  const int64_t nmax0 = e_nm0 ? std::atoll(e_nm0) : kAcaNarrowMax;
-  const char* e_tc = std::getenv("HMX_ACA_TC");
-  // tensor-core ACA for the wide d = 3 leaves (default; HMX_ACA_TC=0 selects the CUDA-core kernel)
-  const bool use_tc = d == 3 && !(e_tc && std::atoi(e_tc) == 0);
-  auto is_tc = [&](int64_t b) { return use_tc && rows_of(b) + cols_of(b) >= nmax0; };
+  // one routing decision feeds both the workspace plan (tensor-core Gram scratch) and the
+  // launch split (wide prefix of the size-sorted pass): aca_route, hmatrix.h
+  const AcaRoute route = aca_route(d, cfg);
+  auto is_tc = [&](int64_t b) { return route.use_tc && rows_of(b) + cols_of(b) >= route.wide_min; };
   auto ws_bytes = [&](int64_t b, int64_t kc) {
     return 16.0 * ((double)d * (rows_of(b) + cols_of(b)) * kc + 2.0 * kc * kc +
                    (is_tc(b) ? (double)aca_tc_scratch(kc) : 0.0));
@@ -641,8 +633,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   std::deque<AcaPass> passes;  // stable addresses (Pending keeps pointers)
   std::vector<int64_t> todo = adm;
   const double s3f = cfg->sigma3_floor > 0 ? cfg->sigma3_floor : 1e-12;
-  const char* e_nm = std::getenv("HMX_ACA_NARROW_MAX");
-  const int64_t nmax = e_nm ? std::atoll(e_nm) : kAcaNarrowMax;
+  const int64_t nmax = route.wide_min;
   // recompression results read back once at the end
   struct Pending {
     AcaPass* ps;
@@ -695,54 +686,26 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     const int classes[] = {kMaxAcaCols, kRecompressSmemMax, 88, 72, 60, 48, 39, 30, 21};
     const int ncls = (int)(sizeof(classes) / sizeof(classes[0]));
     size_t q0 = 0;
-    // when issued on the auxiliary stream, only the large-K class stays there;
-    // the shared-memory classes go to the main stream (ordered after this
-    // point by an event) so they overlap the long large-K CTAs
-    // HMX_RC_FORK=1: the wide leaves' shared-memory classes go to the main stream
-    // (behind the narrow leaves' classes); default: they stay on aux after the
-    // large-K class, so the two streams' class sequences run side by side
-    const char* e_fk = std::getenv("HMX_RC_FORK");
-    const bool on_aux = c.stream == c.aux && e_fk && e_fk[0] == '1';
-    bool forked = false;
     for (int ci = 0; ci < ncls && q0 < rd.size(); ++ci) {
       const int lim_lo = ci + 1 < ncls ? classes[ci + 1] : 0;
       size_t q1 = q0;
       while (q1 < rd.size() && (rd[q1].K > lim_lo || ci == ncls - 1)) ++q1;
       if (q1 > q0) {
-        const cudaStream_t saved = c.stream;
-        if (on_aux && ci > 0) {
-          if (!forked) {
-            cudaEvent_t ev_f;
-            HMX_CUDA_TRY(cudaEventCreateWithFlags(&ev_f, cudaEventDisableTiming));
-            HMX_CUDA_TRY(cudaEventRecord(ev_f, c.aux));
-            HMX_CUDA_TRY(cudaStreamWaitEvent(main_stream, ev_f, 0));
-            cudaEventDestroy(ev_f);
-            forked = true;
-          }
-          c.stream = main_stream;
-        }
         e = launch_recompress_core(c, d_rd + q0, (int64_t)(q1 - q0), rd[q0].K, cfg->eps, cfg->trunc_rule, ps.G, W,
                                    d_rank + q0, d_flag + q0);
         mark("  rc class K<=" + std::to_string(rd[q0].K) + " n=" + std::to_string(q1 - q0));
-        c.stream = saved;
         if (e) return e;
       }
       q0 = q1;
     }
     mark("recompress issued");
-    if (forked) {
-      const cudaStream_t sv = c.stream;
-      c.stream = main_stream;
-      mark("recompress small classes issued");
-      c.stream = sv;
-    }
     pending.push_back(Pending{&ps, std::move(live), d_rank, d_flag});
     return HMX_OK;
   };
   // ACA outputs of positions [q0, q1) of the pass (already on the host):
   // bookkeeping, overflow -> next pass, recompression of the rest
   std::vector<int64_t> next;
-  int64_t nfb = 0;
+  std::vector<int64_t> fb_leaves;  // leaves whose sigma_3 pivots all fell below the floor
   auto consume = [&](AcaPass& ps, size_t q0, size_t q1) -> int {
     std::vector<int64_t> live;
     for (size_t i = q0; i < q1; ++i) {
@@ -758,14 +721,16 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
         ps.out[i].rank = -1;  // superseded
         continue;
       }
-      if (o.status & 8) ++nfb;
       H.steps[b] = o.steps;
       H.rank_before[b] = o.rank;
       H.flags[b] = o.status & 0xB;
       H.pairs_evaluated += (int64_t)o.steps * (rows_of(b) + cols_of(b)) + (int64_t)o.zero_rows * cols_of(b);
+      if (o.status & 8) {  // FallbackNeeded: randomized SVD after the passes (section 1b)
+        fb_leaves.push_back(b);
+        continue;
+      }
       live.push_back((int64_t)i);
     }
-    if (nfb) return HMX_OK;
     return recompress_subset(ps, std::move(live));
   };
   // Capacity-overflow reruns (passes after the first) depend only on the
@@ -877,7 +842,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       if (nwide) {
         sub_max(0, nwide, kc, mm);
         if ((rc = launch_aca(c, d, P, pts.soa, d_desc, d_order, (int64_t)nwide, kc, mm, cfg->eps, s3f, ps.U, ps.V,
-                             ps.G, d_out, use_tc ? kAcaTensor : kAcaWide)))
+                             ps.G, d_out, route.use_tc ? kAcaTensor : kAcaWide, route.tc_stages)))
           return fail(rc);
       }
       mark("aca wide done");
@@ -888,7 +853,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     if (todo.size() > nwide) {
       sub_max(nwide, todo.size(), kc, mm);
       if ((rc = launch_aca(c, d, P, pts.soa, d_desc, d_order + nwide, (int64_t)(todo.size() - nwide), kc, mm,
-                           cfg->eps, s3f, ps.U, ps.V, ps.G, d_out, kAcaNarrow)))
+                           cfg->eps, s3f, ps.U, ps.V, ps.G, d_out, kAcaNarrow, 0)))
         return fail(rc);
       mark("aca narrow done");
       HMX_CUDA_TRY(cudaMemcpyAsync(ps.out.data() + nwide, d_out + nwide, sizeof(AcaOut) * (todo.size() - nwide),
@@ -896,31 +861,19 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     }
     // the rank-independent half of the matvec plan, while the ACA runs
     if (pre.segs.empty()) build_plan_pre(H, pre);
-    // HMX_WIDE_FIRST=1: consume the wide leaves (aux, finished first) before
-    // the narrow ones so their large-K recompression is queued behind the
-    // narrow ACA instead of after it (measured 2-5% slower: off by default)
-    const char* e_wf = std::getenv("HMX_WIDE_FIRST");
-    const bool wide_first = e_wf && e_wf[0] == '1';
-    auto consume_wide = [&]() -> int {
-      if (!nwide) return HMX_OK;
-      HMX_CUDA_TRY(cudaStreamSynchronize(c.aux));
-      OnAux on(c);
-      return consume(ps, 0, nwide);
-    };
-    if (wide_first && (rc = consume_wide())) return fail(rc);
+    // narrow leaves (main stream) first, then the wide ones (aux stream): the wide leaves'
+    // large-K recompression classes then queue on aux behind the wide ACA and overlap the
+    // narrow leaves' recompression on the main stream
     if (todo.size() > nwide) {
       HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
       if ((rc = consume(ps, nwide, todo.size()))) return fail(rc);
     }
-    if (!wide_first && (rc = consume_wide())) return fail(rc);
-    H.aca_passes++;
-    if (nfb) {
-      H.n_fallback += nfb;
-      hmx_set_error("FallbackNeeded on %lld admissible blocks (all sigma_3 pivots below the floor); the device "
-                    "randomized-SVD fallback is not implemented",
-                    (long long)nfb);
-      return fail(HMX_EPIVOT);
+    if (nwide) {
+      HMX_CUDA_TRY(cudaStreamSynchronize(c.aux));
+      OnAux on(c);
+      if ((rc = consume(ps, 0, nwide))) return fail(rc);
     }
+    H.aca_passes++;
     // join the auxiliary stream before the next pass / the layout
     cudaEvent_t join;
     HMX_CUDA_TRY(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
@@ -939,6 +892,50 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     HMX_CUDA_TRY(cudaEventRecord(join, c.rerun));
     HMX_CUDA_TRY(cudaStreamWaitEvent(c.stream, join, 0));
     cudaEventDestroy(join);
+  }
+  // ---- 1b. randomized-SVD fallback -------------------------------
+  // each flagged leaf is regenerated densely, compressed by the adaptive range finder and
+  // recompressed like an ACA factor pair; its factors are copied into the streams after the
+  // layout (section 3).  Pivot exhaustion is reported only if the fallback itself fails.
+  struct FbOut {
+    int64_t b;
+    int r;
+    double2 *U, *V;
+  };
+  std::vector<FbOut> fbo;
+  DevBuf fb_mem(c);
+  for (int64_t b : fb_leaves) {
+    const int64_t m = rows_of(b), n = cols_of(b), dm = d * m, dn = d * n;
+    const int64_t cap = std::min<int64_t>(maxr[b], kMaxAcaCols);
+    DevBuf t(c);
+    double2 *A, *U, *V, *G;
+    int64_t* dd;
+    int32_t* derr;
+    if ((rc = t.alloc(&A, dm * dn)) || (rc = t.alloc(&U, dm * cap)) || (rc = t.alloc(&V, dn * cap)) ||
+        (rc = t.alloc(&G, 2 * cap * cap)) || (rc = t.alloc(&dd, 6)) || (rc = t.alloc(&derr, 1)))
+      return fail(rc);
+    const int64_t desc[6] = {table[5 * b + 1], m, table[5 * b + 3], n, 0, dm};
+    HMX_CUDA_TRY(cudaMemcpyAsync(dd, desc, sizeof(desc), cudaMemcpyHostToDevice, c.stream));
+    HMX_CUDA_TRY(cudaMemsetAsync(derr, 0, sizeof(int32_t), c.stream));
+    if ((rc = launch_dense_fill(c, P, pts.soa, dd, 1, A, derr))) return fail(rc);
+    int K = 0, conv = 0;
+    const uint64_t seed = (uint64_t)cfg->rsvd_seed * 0x9E3779B97F4A7C15ull + (uint64_t)b;
+    if ((rc = rsvd_dense(c, A, dm, dn, cfg->eps, kRsvdOversample, cap, seed, U, V, G, &K, &conv))) {
+      const std::string why = g_last_error;
+      hmx_set_error("block %lld: FallbackNeeded and the randomized-SVD fallback failed (%s)", (long long)b,
+                    why.c_str());
+      return fail(HMX_EPIVOT);
+    }
+    int r = 0;
+    double2 *Uo = nullptr, *Vo = nullptr;
+    if (K > 0 && (rc = recompress_device(c, fb_mem, U, V, dm, dn, K, G, cfg->eps, cfg->trunc_rule, &r, &Uo, &Vo)))
+      return fail(rc);
+    H.rank_before[b] = K;
+    H.rank_after[b] = r;
+    H.flags[b] = (H.flags[b] & ~1) | (conv ? 1 : 0) | 8 | 128;  // bit 7: factors from the rSVD fallback
+    H.n_fallback++;
+    H.pairs_evaluated += m * n;
+    fbo.push_back(FbOut{b, r, Uo, Vo});
   }
   HMX_CUDA_TRY(cudaEventRecord(ev[1], c.stream));
   tick("aca done");
@@ -979,6 +976,14 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   // ---- 3. layout + matvec plan ----------------------------------------------------------------
   if (verbose) setenv("HMX_VERBOSE_PLAN", "1", 1);
   if ((rc = build_matvec_plan(H, &pre))) return fail(rc);
+  for (const FbOut& f : fbo) {
+    if (f.r == 0) continue;
+    const int64_t dm = d * rows_of(f.b), dn = d * cols_of(f.b);
+    HMX_CUDA_TRY(cudaMemcpyAsync(H.d_row + H.leaf_moff[f.b], f.U, sizeof(double2) * dm * f.r,
+                                 cudaMemcpyDeviceToDevice, c.stream));
+    HMX_CUDA_TRY(cudaMemcpyAsync(H.d_v + H.leaf_voff[f.b], f.V, sizeof(double2) * dn * f.r,
+                                 cudaMemcpyDeviceToDevice, c.stream));
+  }
 
   // ---- 4a. dense leaves ---------------------------------------------------------------------
   HMX_CUDA_TRY(cudaEventRecord(ev[3], c.stream));
@@ -1615,7 +1620,7 @@ int hmx_aca_block(hmx_ctx* ctx, const hmx_kernel* k, const double* X, int64_t m,
     HMX_CUDA_TRY(cudaMemcpyAsync(d_order, &zero, sizeof(int32_t), cudaMemcpyHostToDevice, c.stream));
     const int variant = m + n < kAcaNarrowMax ? kAcaNarrow : kAcaWide;
     if ((rc = launch_aca(c, d, P, P3.soa, d_desc, d_order, 1, (int)kc, (int)m, cfg->eps, s3f, dU, dV, G, d_out,
-                         variant)))
+                         variant, 0)))
       return rc;
     AcaOut o;
     HMX_CUDA_TRY(cudaMemcpyAsync(&o, d_out, sizeof(AcaOut), cudaMemcpyDeviceToHost, c.stream));
@@ -1708,6 +1713,44 @@ int hmx_recompress(hmx_ctx* ctx, int64_t dm, int64_t dn, int64_t K, const double
     HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
     from_colmajor(ou, dm, r, r, reinterpret_cast<double2*>(Uout));
     from_colmajor(ov, dn, r, r, reinterpret_cast<double2*>(Vout));
+  }
+  return HMX_OK;
+}
+
+int hmx_rsvd(hmx_ctx* ctx, const double* A, int64_t m, int64_t n, double eps, int32_t oversample, int64_t max_rank,
+             int64_t seed, double* U, double* V, int64_t* k, int32_t* converged) {
+  if (!ctx || !A || !U || !V || !k || !converged || m <= 0 || n <= 0 || oversample < 0) return HMX_EINVAL;
+  if (!(eps > 0 && eps < 1)) {
+    hmx_set_error("hmx_rsvd: eps must be in (0, 1)");
+    return HMX_EINVAL;
+  }
+  Ctx& c = ctx->c;
+  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  const int64_t cap = std::min<int64_t>(max_rank > 0 ? max_rank : std::min(m, n), std::min(m, n));
+  if (cap > kMaxAcaCols) {
+    hmx_set_error("hmx_rsvd: column cap %lld above the device limit %d", (long long)cap, kMaxAcaCols);
+    return HMX_EINVAL;
+  }
+  DevBuf mem(c);
+  std::vector<double2> ha;
+  to_colmajor(reinterpret_cast<const double2*>(A), m, n, ha);
+  double2 *dA, *dU, *dV, *G;
+  int rc;
+  if ((rc = mem.alloc(&dA, m * n)) || (rc = mem.alloc(&dU, m * cap)) || (rc = mem.alloc(&dV, n * cap)) ||
+      (rc = mem.alloc(&G, 2 * cap * cap)))
+    return rc;
+  HMX_CUDA_TRY(cudaMemcpyAsync(dA, ha.data(), sizeof(double2) * ha.size(), cudaMemcpyHostToDevice, c.stream));
+  int K = 0, conv = 0;
+  if ((rc = rsvd_dense(c, dA, m, n, eps, oversample, cap, (uint64_t)seed, dU, dV, G, &K, &conv))) return rc;
+  *k = K;
+  *converged = conv;
+  if (K > 0) {
+    std::vector<double2> ou((size_t)(m * K)), ov((size_t)(n * K));
+    HMX_CUDA_TRY(cudaMemcpyAsync(ou.data(), dU, sizeof(double2) * ou.size(), cudaMemcpyDeviceToHost, c.stream));
+    HMX_CUDA_TRY(cudaMemcpyAsync(ov.data(), dV, sizeof(double2) * ov.size(), cudaMemcpyDeviceToHost, c.stream));
+    HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+    from_colmajor(ou, m, K, K, reinterpret_cast<double2*>(U));
+    from_colmajor(ov, n, K, K, reinterpret_cast<double2*>(V));
   }
   return HMX_OK;
 }

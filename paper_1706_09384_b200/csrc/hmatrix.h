@@ -40,6 +40,8 @@ struct Ctx {
   std::multimap<size_t, void*> cache;  // size -> free block
   std::unordered_map<void*, size_t> live;  // block -> size
   size_t cached_bytes = 0;
+  void* blas = nullptr;    // cublasHandle_t of the randomized-SVD fallback (rsvd.cu), lazy
+  void* solver = nullptr;  // cusolverDnHandle_t, lazy
 };
 
 // phase-1 job: one warp computes s[soff] = V[voff : voff+len]^H x_tree[xoff : xoff+len]
@@ -191,7 +193,23 @@ constexpr int kAcaTensor = 2;
 inline int64_t aca_tc_scratch(int64_t kcap) { return 16 * ((kcap + 7) / 8) * 64; }
 int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const AcaDesc* d_desc, const int32_t* d_order,
                int64_t nblk, int kcap_max, int m_max, double eps, double sigma3_floor, double2* U, double2* V,
-               double2* G, AcaOut* d_out, int variant);
+               double2* G, AcaOut* d_out, int variant, int tc_stages);
+// Routing of the admissible leaves between the ACA kernels: leaves with m + n >= wide_min points
+// are "wide" (auxiliary stream; tensor-core kernel with its Gram scratch when use_tc, else the
+// 512-thread CUDA-core kernel), the rest narrow.  hmx_assemble derives BOTH the workspace plan and
+// the launch split from this one value.
+struct AcaRoute {
+  int64_t wide_min;
+  bool use_tc;
+  int tc_stages;  // 0: deepest ring that fits in shared memory
+};
+inline AcaRoute aca_route(int d, const hmx_aca_cfg* cfg) {
+  AcaRoute r;
+  r.wide_min = kAcaNarrowMax;
+  r.use_tc = d == 3 && cfg->aca_kernel != HMX_ACA_KERNEL_CUDA_CORE;
+  r.tc_stages = cfg->tc_stages;
+  return r;
+}
 
 // recompress.cu
 // recompress_core keeps E and the QL eigenvector matrix in shared memory up to this ACA rank
@@ -231,6 +249,13 @@ int64_t err_tiles_of(int64_t m, int64_t n);
 // dense.cu: FP64 peak microbenchmark
 int bench_dfma(Ctx& c, double* tflops);
 int bench_read_bw(Ctx& c, double* gbs);
+
+// rsvd.cu: randomized-SVD fallback of the vector ACA.  A: m x n column-major
+// dense block; U (m x cap), V (n x cap), G (2 cap^2) outputs: K columns, Gram pair at ld = K.
+int rsvd_dense(Ctx& c, const double2* A, int64_t m, int64_t n, double eps, int oversample, int64_t cap, uint64_t seed,
+               double2* U, double2* V, double2* G, int* K_out, int* converged);
+int linalg_handles(Ctx& c, void** blas, void** solver);
+void linalg_destroy(Ctx& c);
 
 // gmres.cu
 int gmres_device(DeviceH& H, const double2* b_dev, double2* x_dev, double tol, int restart, int64_t max_iters,

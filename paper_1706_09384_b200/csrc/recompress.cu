@@ -1078,16 +1078,14 @@ int launch_recompress_core(Ctx& c, const RecDesc* d_desc, int64_t nblk, int kmax
     return HMX_EINVAL;
   }
   const size_t vec = sizeof(double2) * 3 * (size_t)kmax + sizeof(double) * 6 * kmax + sizeof(int) * (kmax + 4) + 32;
-  const char* e_all = std::getenv("HMX_RC_ALLSMEM_MAX");
-  const int all_max = e_all ? std::atoi(e_all) : kRecompressAllSmemMax;
+  const int all_max = kRecompressAllSmemMax;
   if (kmax <= all_max) {
     const size_t smem = vec + sizeof(double2) * ((size_t)kmax * (kmax + 1) / 2 + 2 * (size_t)kmax * kmax);
     HMX_CUDA_TRY(cudaFuncSetAttribute(recompress_core<2, 128>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     recompress_core<2, 128><<<(unsigned)nblk, 128, smem, c.stream>>>(d_desc, eps, rule, G, W, d_rank, d_flags);
   } else if (kmax <= kRecompressSmemMax) {
     const size_t smem = vec + sizeof(double2) * ((size_t)kmax * (kmax + 1) / 2);  // packed E
-    const char* e_64 = std::getenv("HMX_RC_NT64_MAX");
-    const int nt64_max = e_64 ? std::atoi(e_64) : kRecompressNt64Max;
+    const int nt64_max = kRecompressNt64Max;
     if (kmax <= nt64_max) {
       // small K: 2-warp CTAs (cheaper barriers, twice the leaves per SM)
       HMX_CUDA_TRY(
@@ -1105,8 +1103,7 @@ int launch_recompress_core(Ctx& c, const RecDesc* d_desc, int64_t nblk, int kmax
   } else {
     // large K: few long CTAs whose O(K^3) phases are L2-latency bound -> more warps
     const size_t smem = vec + sizeof(double2) * kGemmTile;
-    const char* e_nt = std::getenv("HMX_RC_NT");
-    const int nt = e_nt ? std::atoi(e_nt) : 512;
+    constexpr int nt = 512;
     if (nt == 1024) {
       HMX_CUDA_TRY(cudaFuncSetAttribute(recompress_core<0, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                         (int)smem));

@@ -13,7 +13,7 @@ import numpy as np
 
 from . import _lib
 from .geometry import sparsity_pattern
-from .lowrank import TRUNC_RULES, ACAConfig, LowRankFactor
+from .lowrank import ACAConfig, LowRankFactor
 
 HOST, DEVICE = 0, 1
 
@@ -146,12 +146,7 @@ def assemble(spec, cloud, ct, bt, cfg=ACAConfig(), self_shift=None, device=0):
         raise ValueError("ElastoT requires normals on the cloud")
     perm = np.ascontiguousarray(ct.permutation, dtype=np.int64)
     table = bt.leaf_table
-    c = _lib.HmxAcaCfg()
-    c.eps = cfg.eps_aca
-    c.max_rank = cfg.max_rank or 0
-    c.sigma3_floor = cfg.sigma3_floor
-    c.trunc_rule = TRUNC_RULES[cfg.trunc_rule]
-    c.mem_budget_gb = cfg.mem_budget_gb
+    c = cfg.c_struct()
     kern = _spec_kernel(spec)
     shift = float(cloud.size) if self_shift is None else float(self_shift)
     h = C.c_void_p()

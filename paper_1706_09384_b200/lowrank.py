@@ -8,6 +8,7 @@ from dataclasses import dataclass
 import numpy as np
 
 TRUNC_RULES = {"frobenius": 0, "spectral": 1}
+ACA_KERNELS = {"auto": 0, "cuda_core": 1}
 
 
 @dataclass(frozen=True)
@@ -20,6 +21,14 @@ class ACAConfig:
     sigma3_floor: float = 1e-12
     trunc_rule: str = "frobenius"
     mem_budget_gb: float = 0.0
+    # device-path options (no reference counterpart): ACA kernel for the wide d = 3 leaves
+    # ("auto" = tensor-core DMMA, "cuda_core"), its copy-ring depth (0 = deepest that fits),
+    # opt-in per-leaf certification ||A_b - U V^H||_F <= eps ||A_b||_F, and the seed of the
+    # randomized-SVD fallback's Gaussian test matrices
+    aca_kernel: str = "auto"
+    tc_stages: int = 0
+    certify: bool = False
+    rsvd_seed: int = 0
 
     def __post_init__(self):
         if not (0.0 < self.eps_aca < 1.0):
@@ -28,6 +37,24 @@ class ACAConfig:
             raise ValueError("max_rank must be >= 1")
         if self.trunc_rule not in TRUNC_RULES:
             raise ValueError(f"trunc_rule must be one of {sorted(TRUNC_RULES)}")
+        if self.aca_kernel not in ACA_KERNELS:
+            raise ValueError(f"aca_kernel must be one of {sorted(ACA_KERNELS)}")
+        if self.tc_stages not in (0, 2, 3):
+            raise ValueError("tc_stages must be 0, 2 or 3")
+
+    def c_struct(self, mem_budget_gb=None):
+        """The hmx_aca_cfg of include/hmx.h."""
+        c = _lib.HmxAcaCfg()
+        c.eps = self.eps_aca
+        c.max_rank = self.max_rank or 0
+        c.sigma3_floor = self.sigma3_floor
+        c.trunc_rule = TRUNC_RULES[self.trunc_rule]
+        c.aca_kernel = ACA_KERNELS[self.aca_kernel]
+        c.mem_budget_gb = self.mem_budget_gb if mem_budget_gb is None else mem_budget_gb
+        c.tc_stages = self.tc_stages
+        c.certify = int(bool(self.certify))
+        c.rsvd_seed = int(self.rsvd_seed)
+        return c
 
 
 @dataclass
@@ -116,13 +143,7 @@ class ACAResult(LowRankFactor):
 
 
 def _c_cfg(cfg):
-    c = _lib.HmxAcaCfg()
-    c.eps = cfg.eps_aca
-    c.max_rank = cfg.max_rank or 0
-    c.sigma3_floor = cfg.sigma3_floor
-    c.trunc_rule = TRUNC_RULES[cfg.trunc_rule]
-    c.mem_budget_gb = 0.0
-    return c
+    return cfg.c_struct(mem_budget_gb=0.0)
 
 
 def _aca_block(gen, cfg, recompress_too, device=0):
@@ -232,34 +253,25 @@ def aca_full(a, cfg=ACAConfig()):
     return ACAResult(U, V, steps=len(us), converged=converged)
 
 
-def randomized_svd(a, eps, oversample=10, max_rank=None, seed=0):
-    """Gaussian range finder with rank doubling until the
-    estimated residual is below eps ||A||_2, on the GPU; a is a dense matrix or
-    a BlockGenerator (densified)."""
-    torch, dev = _torch_dev()
+def randomized_svd(a, eps, oversample=10, max_rank=None, seed=0, device=0):
+    """SPEC.md:308-316 on the device (hmx_rsvd, csrc/rsvd.cu): Gaussian range finder with
+    8 + oversample columns, doubling until ||A - Q Q^H A||_F <= eps ||A||_F; ``a`` is a dense
+    matrix or a BlockGenerator (densified on the device).  Returns the un-truncated factors
+    U = Q, V = (Q^H A)^H (``recompress`` trims them, as after ACA); ``converged`` is False when
+    the column cap min(max_rank, m, n) stopped the doubling (a flagged result)."""
     A = a.dense() if isinstance(a, BlockGenerator) else np.asarray(a, dtype=np.complex128)
-    At = torch.as_tensor(A, device=dev)
-    m, n = At.shape
-    cap = min(m, n) if max_rank is None else min(max_rank, m, n)
-    s_all = torch.linalg.svdvals(At) if min(m, n) <= 2048 else None
-    norm2 = float(s_all[0]) if s_all is not None and s_all.numel() else float(torch.linalg.norm(At))
-    if norm2 == 0.0:
-        return ACAResult(np.zeros((m, 0), np.complex128), np.zeros((n, 0), np.complex128), steps=0, converged=True)
-    g = torch.Generator(device=dev).manual_seed(seed)
-    k = min(cap, 8)
-    while True:
-        Om = torch.complex(torch.randn(n, k + oversample, generator=g, device=dev, dtype=torch.float64),
-                           torch.randn(n, k + oversample, generator=g, device=dev, dtype=torch.float64))
-        Q, _ = torch.linalg.qr(At @ Om)
-        B = Q.conj().T @ At
-        Ub, s, Vh = torch.linalg.svd(B, full_matrices=False)
-        resid = float(torch.linalg.norm(At - Q @ B, ord=2)) if min(m, n) <= 2048 else float(
-            torch.linalg.norm(At - Q @ B))
-        if resid <= eps * norm2 or k >= cap:
-            break
-        k = min(cap, 2 * k)
-    r = int((s > eps * s[0]).sum()) if s.numel() else 0
-    r = min(r, cap)
-    U = (Q @ Ub[:, :r]) * s[:r]
-    V = Vh[:r].conj().T
-    return ACAResult(U.cpu().numpy(), V.cpu().numpy(), steps=0, converged=resid <= eps * norm2)
+    A = np.ascontiguousarray(A, dtype=np.complex128)
+    if A.ndim != 2 or A.size == 0:
+        raise ValueError("randomized_svd needs a non-empty 2-D block")
+    m, n = A.shape
+    cap = min(m, n) if max_rank is None else min(int(max_rank), m, n)
+    U = np.zeros((m, cap), np.complex128)
+    V = np.zeros((n, cap), np.complex128)
+    k = _C.c_int64()
+    conv = _C.c_int32()
+    _lib.check(_lib.lib().hmx_rsvd(_lib.context(device), _lib.ptr(A), m, n, float(eps), int(oversample), cap,
+                                   int(seed), _lib.ptr(U), _lib.ptr(V), _C.byref(k), _C.byref(conv)), "hmx_rsvd")
+    K = int(k.value)
+    U = U.reshape(-1)[: m * K].reshape(m, K).copy()
+    V = V.reshape(-1)[: n * K].reshape(n, K).copy()
+    return ACAResult(U, V, steps=0, converged=bool(conv.value))

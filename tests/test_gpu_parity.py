@@ -153,8 +153,13 @@ def test_gmres_iterations_vs_oracle(tag, n):
     b = pb.rhs(0)
     res = hmx.solve_gmres(H, b, hmx.GmresConfig(tol=1e-4, restart=50))
     assert res.converged
-    xo, it_o, hist_o, conv_o = OS.gmres(lambda v: hmx.matvec(H, v), b, 1e-4, 50, 1000)
-    assert abs(res.iters - it_o) <= 1
+    # the oracle's GMRES on the oracle's own H-matrix (assembly + matvec all on the host)
+    oh = pb.oracle_h()
+    xo, it_o, hist_o, conv_o = OS.gmres(lambda v: OH.matvec(oh, v), b, 1e-4, 50, 1000)
+    assert conv_o and abs(res.iters - it_o) <= 1
+    # the Krylov recurrence alone: the oracle GMRES driven by the device matvec
+    _, it_d, _, _ = OS.gmres(lambda v: hmx.matvec(H, v), b, 1e-4, 50, 1000)
+    assert abs(res.iters - it_d) <= 1
     r = b - hmx.matvec(H, res.x)
     assert np.linalg.norm(r) <= 1e-4 * np.linalg.norm(b) * 1.0001
     assert all(h1 <= h0 * (1 + 1e-12) for h0, h1 in zip(res.history, res.history[1:]))
@@ -163,12 +168,12 @@ def test_gmres_iterations_vs_oracle(tag, n):
 
 
 @pytest.mark.parametrize("tag,n", [("U8k", 4096), ("T65k", 4096)])
-def test_aca_kernel_variants_agree(tag, n, monkeypatch):
+def test_aca_kernel_variants_agree(tag, n):
     """The three ACA kernels for large d = 3 leaves (m + n >= 320 points) --
     tensor-core with a 3-stage ring (default), tensor-core with a 2-stage
-    ring, CUDA-core (HMX_ACA_TC=0) -- each reproduce the oracle's steps /
-    ranks (+-1) and the compression bar on every leaf, and agree with each
-    other."""
+    ring, CUDA-core (aca_kernel="cuda_core") -- each reproduce the oracle's
+    steps / ranks (+-1) and the compression bar on every leaf, and agree with
+    each other."""
     from paper_1706_09384_b200.hmatrix import block_errors
 
     pb = Problem(tag, n)
@@ -177,12 +182,8 @@ def test_aca_kernel_variants_agree(tag, n, monkeypatch):
     assert (sizes[adm] >= 320).sum() >= 100, "too few large leaves at this size"
     oh = pb.oracle_h()
     infos = []
-    for env in ({}, {"HMX_TC_STAGES": "2"}, {"HMX_ACA_TC": "0"}):
-        for k in ("HMX_TC_STAGES", "HMX_ACA_TC"):
-            monkeypatch.delenv(k, raising=False)
-        for k, v in env.items():
-            monkeypatch.setenv(k, v)
-        H, _ = pb.device_h()
+    for env in ({}, {"tc_stages": 2}, {"aca_kernel": "cuda_core"}):
+        H, _ = pb.device_h(**env)
         info = H.block_info()
         assert np.abs(info["steps"][adm] - oh.steps[adm]).max() <= 1, env
         assert np.abs(info["rank_after"][adm] - oh.rank_after[adm]).max() <= 1, env
