@@ -9,12 +9,16 @@ algorithmic H-matvec traffic of all ranks divided by the device time of the K
 steps (max over ranks): GB/s.  The packed H streams (10.5 GB at U32k) are far
 larger than the 126 MB L2, so no L2 flush is needed between steps.
 
-Multi-GPU (torchrun): replicas only -- every rank assembles and applies its own
-copy, value = sum over ranks, scaling "weak".
+Multi-GPU (N > 1; ``--gpus N`` outside torchrun re-launches itself as N
+ranks): the row-sharded H of SURVEY 8(e) -- rank p assembles the leaves of
+its owned row range, a step is the local matvec plus one all-gather of the
+owned y segments; value = full-H bytes x K / max-over-ranks device time,
+scaling "strong".  ``--replicas`` runs independent full copies instead.
 
 ``--impl reference`` times the reference's CPU implementation of the same
-path (the oracle restatement, oracle/hmatrix.py, all host threads) on a
-bounded sample of the same workload and prints the same JSON line shape.
+path (the oracle restatement, oracle/hmatrix.py, all host threads) on the
+same workload -- every U32k leaf assembled in a process pool, then full
+oracle H-matvecs -- and prints the same JSON line shape.
 """
 
 import argparse
@@ -49,11 +53,14 @@ def parse():
     ap.add_argument("--no-direct", action="store_true", help="skip the H-LU direct-solve section")
     ap.add_argument("--direct-config", default="H4k,U8k@2562",
                     help="H-LU direct-solve workloads (TAG or TAG@points; U8k@2562 = 7,686 dofs, the paper's Table 5 size)")
-    ap.add_argument("--extra-configs", default="U131k,U8k,H4k",
+    ap.add_argument("--extra-configs", default="U32k45,U131k,U8k,H4k",
                     help="other BASELINE configs measured briefly (assembly + 20 matvecs); '' to skip")
     ap.add_argument("--shard", action="store_true",
-                    help="block-row sharded H (SURVEY 8(e)): each rank assembles 1/N of the leaves, one "
-                         "all-reduce of y per matvec, strong scaling (default: independent replicas)")
+                    help="row-sharded H (SURVEY 8(e)) even at N = 1 (the default for N > 1): each rank "
+                         "assembles the leaves of its owned row range, one all-gather of y per matvec, "
+                         "strong scaling")
+    ap.add_argument("--replicas", action="store_true",
+                    help="N > 1: independent full replicas instead of the row-sharded H (weak scaling)")
     return ap.parse_args()
 
 
@@ -131,47 +138,62 @@ def dist_setup(args):
 
 
 # ----------------------------------------------------------------------------------------------
-def cpu_sample_problem(tag, stripe=8):
-    """Bounded CPU sample: every leaf whose row cluster lies in the first 1/stripe
-    of the tree-ordered rows (a block-row stripe keeps the workload's leaf mix)."""
+def cpu_model():
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def cpu_problem(tag, stripe=None):
+    """The oracle's inputs for workload ``tag``: every leaf (stripe None, the same
+    configuration as the device run) or, for a quick bounded sample, the leaves whose row
+    cluster lies in the first 1/stripe of the tree-ordered rows (keeps the leaf mix)."""
     from oracle import geometry as OG
     from paper_1706_09384_b200.configs import WORKLOADS
-    import paper_1706_09384_b200 as hmx
-    from tests._problems import oracle_params, spec_for  # noqa: F401
+    from tests._problems import oracle_params, spec_for
 
     w = WORKLOADS[tag]
     pts, nrm = OG.sphere_cloud(w.n_points)
     ct = OG.cluster_tree(pts, w.n_leaf)
     lv = OG.block_leaves(ct, ct, w.eta)
     tab = OG.leaf_table(ct, ct, lv)
+    params = oracle_params(spec_for(w))
+    if stripe is None:
+        return w, ct, nrm, tab, params, f"all {len(tab)} leaves of {tag} (same configuration as the device run)"
     cut = w.n_points // stripe
     sel = np.flatnonzero(tab[:, 2] <= cut)
-    params = oracle_params(spec_for(w))
     return w, ct, nrm, tab[sel], params, f"rows [0, {cut}) of {tag} (1/{stripe} block-row stripe, {len(sel)} leaves)"
 
 
-def run_cpu(tag, steps, warmup, budget_s=None):
-    """Oracle H-matvec throughput on the bounded sample; returns dict."""
+def run_cpu(tag, steps, warmup, budget_s=None, stripe=None):
+    """The oracle (oracle/hmatrix.py) on the host cores: leaf-parallel assembly in a fork pool
+    (SPEC.md:456), then ``steps`` threaded H-matvecs (permutation to tree order, every leaf,
+    permutation back), each timed; returns throughput (bytes of all steps / their total time)
+    and the median step."""
     from concurrent.futures import ThreadPoolExecutor
+
+    from threadpoolctl import threadpool_limits
 
     from oracle import hmatrix as OH
 
-    w, ct, nrm, tab, params, desc = cpu_sample_problem(tag)
+    w, ct, nrm, tab, params, desc = cpu_problem(tag, stripe)
     cores = os.cpu_count() or 1
     t0 = time.perf_counter()
     oh = OH.assemble(w.kind, params, ct.points_tree, None if w.kind != "T" else nrm[ct.perm], ct.perm, tab, w.eps,
                      self_shift=float(w.n_points), workers=cores)
     t_setup = time.perf_counter() - t0
     d = w.d
-    bytes_ = 0.0
-    for (k, r0, r1, c0, c1), ra in zip(tab, oh.rank_after):
-        m, n = r1 - r0, c1 - c0
-        bytes_ += 16.0 * (d * d * m * n if k == 0 else ra * d * (m + n))
-    bytes_ += 32.0 * d * w.n_points
-    # balanced contiguous chunks of leaves by bytes
-    cost = np.array([(d * d * (r1 - r0) * (c1 - c0) if k == 0 else ra * d * ((r1 - r0) + (c1 - c0)))
-                     for (k, r0, r1, c0, c1), ra in zip(tab, oh.rank_after)], float)
-    order = np.argsort(-cost)
+    m = (tab[:, 2] - tab[:, 1]).astype(np.float64)
+    n = (tab[:, 4] - tab[:, 3]).astype(np.float64)
+    cost = np.where(tab[:, 0] == 0, d * d * m * n, oh.rank_after * d * (m + n))
+    bytes_ = 16.0 * float(cost.sum()) + 32.0 * d * w.n_points
+    # balanced leaf chunks (LPT on the leaf bytes), one per thread
+    order = np.argsort(-cost, kind="stable")
     chunks = [[] for _ in range(cores)]
     load = np.zeros(cores)
     for b in order:
@@ -179,28 +201,33 @@ def run_cpu(tag, steps, warmup, budget_s=None):
         chunks[i].append(int(b))
         load[i] += cost[b]
     rng = np.random.default_rng(SEED)
-    n = d * w.n_points
-    xs = [rng.standard_normal(n) + 1j * rng.standard_normal(n) for _ in range(4)]
-    from threadpoolctl import threadpool_limits
+    nd = d * w.n_points
+    xs = [rng.standard_normal(nd) + 1j * rng.standard_normal(nd) for _ in range(4)]
 
+    def step(x, pool):
+        return OH.from_tree(oh, OH.matvec_tree_threads(oh, OH.to_tree(oh, x), pool, chunks))
+
+    times = []
     with ThreadPoolExecutor(cores) as pool, threadpool_limits(1):
         for j in range(warmup):
-            OH.matvec_tree_threads(oh, xs[j % 4], pool, chunks)
-        t0 = time.perf_counter()
-        done = 0
+            step(xs[j % 4], pool)
+        t_all = time.perf_counter()
         for j in range(steps):
-            OH.matvec_tree_threads(oh, xs[j % 4], pool, chunks)
-            done += 1
-            if budget_s is not None and time.perf_counter() - t0 > budget_s:
+            t0 = time.perf_counter()
+            step(xs[j % 4], pool)
+            times.append(time.perf_counter() - t0)
+            if budget_s is not None and time.perf_counter() - t_all > budget_s:
                 break
-        dt = time.perf_counter() - t0
-    pairs = sum((r1 - r0) * (c1 - c0) if k == 0 else int(st) * ((r1 - r0) + (c1 - c0))
-                for (k, r0, r1, c0, c1), st in zip(tab, oh.steps))
+    dt = float(sum(times))
+    done = len(times)
+    pairs = int(np.sum(np.where(tab[:, 0] == 0, m * n, oh.steps * (m + n))))
     return {"value": bytes_ * done / dt / 1e9, "unit": "GB/s", "cores": cores, "kind": "port",
+            "cpu_model": cpu_model(), "same_config": stripe is None,
             "sample": f"{desc}; oracle factors (numpy ACA + QR/SVD recompression); {done} threaded "
                       f"oracle H-matvecs of {bytes_ / 1e9:.3f} GB each", "ms_per_step": dt / done * 1e3,
-            "steps": done, "setup_s": t_setup,
-            "assembly": {"pooled_s": t_setup, "workers": cores, "pairs": int(pairs),
+            "ms_per_step_median": float(np.median(times)) * 1e3, "steps": done, "setup_s": t_setup,
+            "max_rank_after": int(oh.rank_after.max()),
+            "assembly": {"pooled_s": t_setup, "workers": cores, "pairs": pairs,
                          "green_entries_per_s": d * d * pairs / t_setup,
                          "sample": f"{desc}, leaf-parallel process pool (SPEC.md:456)"}}
 
@@ -235,18 +262,21 @@ def cpu_end_to_end(tag="H4k"):
 
 
 def reference_arm(args):
+    """BASELINE config 3 on the host: the oracle assembles every U32k leaf, then times
+    ``--steps`` full oracle H-matvecs (bounded at ~3 minutes of steps)."""
     ws, rank, local = dist_setup(args)
     if rank != 0:
         return
-    r = run_cpu(args.config, args.steps, args.warmup)
+    r = run_cpu(args.config, args.steps, args.warmup, budget_s=180.0)
     line = {
         "impl": "reference", "metric": f"{args.config} H-matvec algorithmic HBM throughput (elasto U)",
         "value": r["value"], "unit": "GB/s", "n_gpus": args.gpus, "steps": r["steps"], "warmup": args.warmup,
         "ms_per_step": r["ms_per_step"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
         "dtype": "c128", "data": "synthetic (Fibonacci sphere, seeded complex Gaussian x)",
-        "config": {"workload": f"{args.config} H-matvec", "sample": r["sample"]},
+        "config": {"workload": f"{args.config} H-matvec", "sample": r["sample"], "same_config": r["same_config"]},
         "cpu_baseline": {"value": r["value"], "unit": "GB/s", "cores": r["cores"], "kind": "port",
-                         "sample": r["sample"]},
+                         "cpu_model": r["cpu_model"], "sample": r["sample"],
+                         "ms_per_step_median": r["ms_per_step_median"], "assembly": r["assembly"]},
         "e2e": {"value": r["value"], "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -288,7 +318,18 @@ def time_to_solve(tag, device):
            "time_to_solve_with_tree_s": st["t_total_ms"] * 1e-3 + t_gm + t_tree,
            "max_rank_before": rep.max_rank_before, "max_rank_after": rep.max_rank_after,
            "matvec_bytes": st["matvec_bytes"], "aca_passes": st["aca_passes"],
-           "free_gb_before_assembly": free_before / 1e9}
+           "free_gb_before_assembly": free_before / 1e9, "n_fallback": st["n_fallback"]}
+    # warm: the same job again in the same process (workspaces from the context cache)
+    del H
+    H, rep = hmx.assemble(w.spec(), cloud, ct, bt, hmx.ACAConfig(eps_aca=w.eps), device=device)
+    st = H.stats()
+    t0 = time.perf_counter()
+    res = hmx.solve_gmres(H, b, hmx.GmresConfig(tol=1e-4, restart=50))
+    t_gm = time.perf_counter() - t0
+    out["warm"] = {"assembly_ms": st["t_total_ms"], "gmres_s": t_gm, "iterations": res.iters,
+                   "time_to_solve_s": st["t_total_ms"] * 1e-3 + t_gm}
+    out["note"] = ("time_to_solve_s: first assembly of this workload in the process (after the other "
+                   "sections released their workspaces); warm: the same job repeated")
     del H
     return out
 
@@ -629,10 +670,10 @@ def hmx_arm(args):
             line["direct_solve"] = {"failed": repr(exc)}
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
-            r = run_cpu(args.config, steps=50, warmup=1, budget_s=15.0)
-            line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample")}
-            line["cpu_baseline"]["ms_per_step"] = r["ms_per_step"]
-            line["cpu_baseline"]["assembly"] = r["assembly"]
+            r = run_cpu(args.config, steps=5, warmup=1)
+            line["cpu_baseline"] = {k: r[k] for k in ("value", "unit", "cores", "kind", "sample", "cpu_model",
+                                                      "same_config", "ms_per_step", "ms_per_step_median",
+                                                      "max_rank_after", "assembly")}
             line["cpu_baseline"]["end_to_end_H4k"] = cpu_end_to_end("H4k")
         except Exception as exc:  # the baseline is reported, never fatal
             line["cpu_baseline"] = {"value": None, "unit": "GB/s", "cores": os.cpu_count(), "kind": "port",
@@ -646,10 +687,11 @@ def hmx_arm(args):
 
 # ----------------------------------------------------------------------------------------------
 def shard_arm(args):
-    """--shard: block-row sharded U32k H-matvec (strong scaling).  Rank p
-    assembles its stripe of the leaves (no collective); a step is the sharded
-    matvec: local stripe matvec + one NCCL all-reduce of y (d N complex128).
-    value = full-H algorithmic bytes x K / device time (max over ranks)."""
+    """Row-sharded U32k H-matvec (strong scaling; the N > 1 default).  Rank p
+    assembles the leaves of its owned row range (no collective); a step is the
+    sharded matvec: local matvec + one NCCL all-gather of the owned y segments
+    (d N complex128 in total).  value = full-H algorithmic bytes x K / device
+    time (max over ranks)."""
     import torch
 
     import paper_1706_09384_b200 as hmx
@@ -719,12 +761,13 @@ def shard_arm(args):
         "dtype": "c128", "data": "synthetic (Fibonacci sphere, seeded complex Gaussian x, seed 0)",
         "config": {"workload": f"{args.config} H-matvec", "kernel": "elasto U", "n_points": w.n_points,
                    "n_leaf": w.n_leaf, "eta": w.eta, "eps_aca": w.eps, "ks": w.ks,
-                   "parallelism": f"block-row shards x{ws} (one all-reduce of y per matvec)",
+                   "parallelism": f"row-range shards x{ws} (one all-gather of y per matvec)",
                    "l2": "inputs larger than L2, no flush"},
         "gpu_launches": 4 * K,
         "e2e": {"value": mv_bytes * K / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 16 * n,
                 "d2h_bytes_per_step": 16 * n, "ms_per_step": e2e_ms / K},
-        "assembly": {"wall_s_max_over_ranks": t_asm, "leaves_this_rank": int(len(sh.part_idx))},
+        "assembly": {"wall_s_max_over_ranks": t_asm, "leaves_this_rank": int(len(sh.part_idx)),
+                     "row_bounds": [int(v) for v in sh.bounds]},
         "clocks": clk.summary(),
     }
     if rank == 0:
@@ -734,11 +777,30 @@ def shard_arm(args):
         tdist.destroy_process_group()
 
 
+def relaunch_under_torchrun(args):
+    """``python bench.py --gpus N`` (N > 1) outside torchrun: re-run this command as N ranks, one per
+    GPU, through torch.distributed.run on 127.0.0.1 (the NCCL INIT lines go to stderr)."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd, env=env)
+
+
 if __name__ == "__main__":
     a = parse()
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    if a.impl != "reference" and a.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(a))
     if a.impl == "reference":
         reference_arm(a)
-    elif a.shard:
+    elif a.shard or (world > 1 and not a.replicas):
         shard_arm(a)
     else:
         hmx_arm(a)

@@ -79,9 +79,9 @@ typedef struct {
   int32_t aca_kernel;    /* HMX_ACA_KERNEL_* */
   double mem_budget_gb;  /* ACA workspace budget; <= 0: 70% of free (+ cached) device memory */
   int32_t tc_stages;     /* tensor-core ACA copy ring depth: 0 = deepest that fits, 2 or 3 */
-  int32_t certify;       /* 1: after assembly, regenerate every admissible leaf, re-compress the
-                            ones above eps until ||A_b - U V^H||_F <= eps ||A_b||_F (north_star) */
+  int32_t pad;
   int64_t rsvd_seed;     /* seed of the Gaussian test matrices of the randomized-SVD fallback */
+  double eps_recompress; /* truncation tolerance of the recompression; <= 0: eps (the reference) */
 } hmx_aca_cfg;
 
 typedef struct {
@@ -175,6 +175,11 @@ int hmx_aca_block(hmx_ctx* ctx, const hmx_kernel* k, const double* X, int64_t m,
  * Vout (dn x K) row-major with leading dimension *rank <= K */
 int hmx_recompress(hmx_ctx* ctx, int64_t dm, int64_t dn, int64_t K, const double* U, const double* V, double eps,
                    int32_t trunc_rule, int64_t* rank, double* Uout, double* Vout);
+
+/* New H-matrix = base with leaf idx[j] replaced by leaf j of sub (same leaf, e.g. re-compressed at
+ * a tighter tolerance by the certification pass of ACAConfig(certify=True)); both inputs unchanged.
+ * Device-side copy of every payload into a freshly laid out stream pair. */
+int hmx_hmatrix_splice(const hmx_hmatrix* base, const hmx_hmatrix* sub, const int64_t* idx, hmx_hmatrix** out);
 
 /* randomized_svd(dense, eps, oversample) (the FallbackNeeded path of aca_vector,
  * SPEC.md:302, 384-385): adaptive Gaussian range finder on a dense (m x n) complex row-major block A,

@@ -26,8 +26,8 @@ class HmxKernel(C.Structure):
 
 class HmxAcaCfg(C.Structure):
     _fields_ = [("eps", f64), ("max_rank", i64), ("sigma3_floor", f64), ("trunc_rule", i32),
-                ("aca_kernel", i32), ("mem_budget_gb", f64), ("tc_stages", i32), ("certify", i32),
-                ("rsvd_seed", i64)]
+                ("aca_kernel", i32), ("mem_budget_gb", f64), ("tc_stages", i32), ("pad", i32),
+                ("rsvd_seed", i64), ("eps_recompress", f64)]
 
 
 class HmxStats(C.Structure):
@@ -73,6 +73,7 @@ SIGNATURES = {
     "hmx_aca_block": (C.c_int, [P, C.POINTER(HmxKernel), P, i64, P, i64, P, i32, f64, C.POINTER(HmxAcaCfg), i32,
                                 i64, P, P, C.POINTER(i64), C.POINTER(i64), C.POINTER(i32)]),
     "hmx_recompress": (C.c_int, [P, i64, i64, i64, P, P, f64, i32, C.POINTER(i64), P, P]),
+    "hmx_hmatrix_splice": (C.c_int, [P, P, P, C.POINTER(P)]),
     "hmx_rsvd": (C.c_int, [P, P, i64, i64, f64, i32, i64, i64, P, P, C.POINTER(i64), C.POINTER(i32)]),
     "hmx_truncate_batch": (C.c_int, [P, i64, P, P, P, P, P, P, P, f64, i32, P, P]),
     "hmx_hmatrix_free": (None, [P]),

@@ -86,6 +86,8 @@ WORKLOADS = {
     "U8k": Workload("U8k", "U", 8192, 32, ks=ks_ten_per_wavelength(8192)),
     "U32k": Workload("U32k", "U", 32768, 32, ks=ks_ten_per_wavelength(32768),
                      runs=("assemble", "matvec")),
+    # the other reading of config 3's "kappa_s about 45" (the N_c = 65,536 ten-points rule value)
+    "U32k45": Workload("U32k45", "U", 32768, 32, ks=ks_ten_per_wavelength(65536), runs=("assemble", "matvec")),
     "U131k": Workload("U131k", "U", 131072, 64, ks=2.0, runs=("assemble", "matvec")),
     "T65k": Workload("T65k", "T", 65536, 32, ks=ks_ten_per_wavelength(65536),
                      runs=("assemble", "gmres")),

@@ -229,6 +229,21 @@ int validate_table(const int64_t* table, int64_t nb, int64_t np) {
   return HMX_OK;
 }
 
+// batched strided copy (hmx_hmatrix_splice): one CTA per column block of a leaf payload
+struct Copy2D {
+  const double2* src;
+  double2* dst;
+  int64_t lds, ldd, rows, cols;
+};
+__global__ void __launch_bounds__(256) copy2d_batch(const Copy2D* __restrict__ items) {
+  const Copy2D it = items[blockIdx.x];
+  const int64_t total = it.rows * it.cols;
+  for (int64_t e = threadIdx.x; e < total; e += blockDim.x) {
+    const int64_t i = e % it.rows, j = e / it.rows;
+    it.dst[i + j * it.ldd] = it.src[i + j * it.lds];
+  }
+}
+
 // launches issued inside this scope go to the context's auxiliary stream
 struct OnAux {
   Ctx& c;
@@ -460,6 +475,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   }
   int rc = validate_table(table, nb, np);
   if (rc) return rc;
+  const double eps_rc = cfg->eps_recompress > 0 ? cfg->eps_recompress : cfg->eps;
   Ctx& c = ctx->c;
   HMX_CUDA_TRY(cudaSetDevice(c.device));
   const auto t_start = std::chrono::steady_clock::now();
@@ -691,7 +707,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       size_t q1 = q0;
       while (q1 < rd.size() && (rd[q1].K > lim_lo || ci == ncls - 1)) ++q1;
       if (q1 > q0) {
-        e = launch_recompress_core(c, d_rd + q0, (int64_t)(q1 - q0), rd[q0].K, cfg->eps, cfg->trunc_rule, ps.G, W,
+        e = launch_recompress_core(c, d_rd + q0, (int64_t)(q1 - q0), rd[q0].K, eps_rc, cfg->trunc_rule, ps.G, W,
                                    d_rank + q0, d_flag + q0);
         mark("  rc class K<=" + std::to_string(rd[q0].K) + " n=" + std::to_string(q1 - q0));
         if (e) return e;
@@ -928,7 +944,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     }
     int r = 0;
     double2 *Uo = nullptr, *Vo = nullptr;
-    if (K > 0 && (rc = recompress_device(c, fb_mem, U, V, dm, dn, K, G, cfg->eps, cfg->trunc_rule, &r, &Uo, &Vo)))
+    if (K > 0 && (rc = recompress_device(c, fb_mem, U, V, dm, dn, K, G, eps_rc, cfg->trunc_rule, &r, &Uo, &Vo)))
       return fail(rc);
     H.rank_before[b] = K;
     H.rank_after[b] = r;
@@ -1138,6 +1154,100 @@ int hmx_hmatrix_load(hmx_ctx* ctx, int32_t d, int64_t np, const int64_t* perm, c
   }
   HMX_CUDA_TRY(cudaMemcpy(H.d_row, row.data(), sizeof(double2) * row.size(), cudaMemcpyHostToDevice));
   if (!vs.empty()) HMX_CUDA_TRY(cudaMemcpy(H.d_v, vs.data(), sizeof(double2) * vs.size(), cudaMemcpyHostToDevice));
+  *out = holder;
+  return HMX_OK;
+}
+
+int hmx_hmatrix_splice(const hmx_hmatrix* base, const hmx_hmatrix* sub, const int64_t* idx, hmx_hmatrix** out) {
+  if (!base || !sub || !idx || !out) return HMX_EINVAL;
+  const DeviceH& B = base->H;
+  const DeviceH& S = sub->H;
+  if (B.ctx != S.ctx || B.d != S.d || B.np != S.np) {
+    hmx_set_error("hmx_hmatrix_splice: the two H-matrices differ in context, d or point count");
+    return HMX_EINVAL;
+  }
+  std::vector<int64_t> src((size_t)B.nb, -1);  // base leaf -> sub leaf (or -1: keep the base leaf)
+  for (int64_t j = 0; j < S.nb; ++j) {
+    const int64_t b = idx[j];
+    if (b < 0 || b >= B.nb || src[(size_t)b] >= 0 ||
+        !std::equal(S.table.begin() + 5 * j, S.table.begin() + 5 * j + 5, B.table.begin() + 5 * b)) {
+      hmx_set_error("hmx_hmatrix_splice: sub leaf %lld does not match base leaf %lld", (long long)j, (long long)b);
+      return HMX_EINVAL;
+    }
+    src[(size_t)b] = j;
+  }
+  Ctx& c = *B.ctx;
+  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  auto holder = new hmx_hmatrix;
+  DeviceH& H = holder->H;
+  H.ctx = &c;
+  H.kind = B.kind;
+  H.d = B.d;
+  H.np = B.np;
+  H.n = B.n;
+  H.nb = B.nb;
+  H.table = B.table;
+  H.steps = B.steps;
+  H.rank_before = B.rank_before;
+  H.rank_after = B.rank_after;
+  H.flags = B.flags;
+  H.pairs_evaluated = B.pairs_evaluated + S.pairs_evaluated;
+  H.aca_passes = B.aca_passes;
+  H.n_fallback = B.n_fallback;
+  H.n_unconverged = B.n_unconverged;
+  H.n_regularized = B.n_regularized;
+  H.flops_assembly = B.flops_assembly + S.flops_assembly;
+  H.t_dense_ms = B.t_dense_ms;
+  H.t_aca_ms = B.t_aca_ms + S.t_aca_ms;
+  H.t_recomp_ms = B.t_recomp_ms + S.t_recomp_ms;
+  H.t_form_ms = B.t_form_ms + S.t_form_ms;
+  H.t_total_ms = B.t_total_ms + S.t_total_ms;
+  for (int64_t b = 0; b < H.nb; ++b) {
+    const int64_t j = src[(size_t)b];
+    if (j < 0) continue;
+    H.steps[b] = S.steps[j];
+    H.rank_before[b] = S.rank_before[j];
+    H.rank_after[b] = S.rank_after[j];
+    H.flags[b] = S.flags[j] | 256;  // bit 8: re-compressed by the certification pass
+    H.n_fallback += (S.flags[j] & 128) ? 1 : 0;
+  }
+  auto fail = [&](int code) {
+    free_h(H);
+    delete holder;
+    return code;
+  };
+  int rc;
+  {
+    std::vector<int64_t> p((size_t)H.np);
+    HMX_CUDA_TRY(cudaMemcpy(p.data(), B.d_perm, sizeof(int64_t) * H.np, cudaMemcpyDeviceToHost));
+    if ((rc = dev_upload(c, &H.d_perm, p))) return fail(rc);
+  }
+  if ((rc = build_matvec_plan(H))) return fail(rc);
+  std::vector<Copy2D> cp;
+  cp.reserve(2 * (size_t)H.nb);
+  for (int64_t b = 0; b < H.nb; ++b) {
+    const int64_t j = src[(size_t)b];
+    const DeviceH& F = j < 0 ? B : S;
+    const int64_t fb = j < 0 ? b : j;
+    const int64_t dm = H.d * (H.table[5 * b + 2] - H.table[5 * b + 1]);
+    const int64_t dn = H.d * (H.table[5 * b + 4] - H.table[5 * b + 3]);
+    if (H.table[5 * b] == 0) {
+      cp.push_back(Copy2D{F.d_row + F.leaf_moff[fb], H.d_row + H.leaf_moff[b], F.leaf_ld[fb], H.leaf_ld[b], dm, dn});
+    } else if (H.rank_after[b] > 0) {
+      const int64_t r = H.rank_after[b];
+      cp.push_back(Copy2D{F.d_row + F.leaf_moff[fb], H.d_row + H.leaf_moff[b], F.leaf_ld[fb], H.leaf_ld[b], dm, r});
+      cp.push_back(Copy2D{F.d_v + F.leaf_voff[fb], H.d_v + H.leaf_voff[b], dn, dn, dn, r});
+    }
+  }
+  if (!cp.empty()) {
+    DevBuf t(c);
+    Copy2D* d_cp;
+    if ((rc = t.alloc(&d_cp, (int64_t)cp.size()))) return fail(rc);
+    HMX_CUDA_TRY(cudaMemcpyAsync(d_cp, cp.data(), sizeof(Copy2D) * cp.size(), cudaMemcpyHostToDevice, c.stream));
+    copy2d_batch<<<(unsigned)cp.size(), 256, 0, c.stream>>>(d_cp);
+    HMX_CUDA_TRY(cudaGetLastError());
+    HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  }
   *out = holder;
   return HMX_OK;
 }
@@ -1655,7 +1765,8 @@ int hmx_aca_block(hmx_ctx* ctx, const hmx_kernel* k, const double* X, int64_t m,
                                      sizeof(double2) * K, K, cudaMemcpyDeviceToDevice, c.stream));
       int r = 0;
       double2 *Uo = nullptr, *Vo = nullptr;
-      if ((rc = recompress_device(c, mem, dU, dV, d * m, d * n, K, G2, cfg->eps, cfg->trunc_rule, &r, &Uo, &Vo)))
+      if ((rc = recompress_device(c, mem, dU, dV, d * m, d * n, K, G2, cfg->eps_recompress > 0 ? cfg->eps_recompress : cfg->eps,
+                                     cfg->trunc_rule, &r, &Uo, &Vo)))
         return rc;
       K = r;
       srcU = Uo;

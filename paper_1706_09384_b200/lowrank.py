@@ -23,12 +23,15 @@ class ACAConfig:
     mem_budget_gb: float = 0.0
     # device-path options (no reference counterpart): ACA kernel for the wide d = 3 leaves
     # ("auto" = tensor-core DMMA, "cuda_core"), its copy-ring depth (0 = deepest that fits),
-    # opt-in per-leaf certification ||A_b - U V^H||_F <= eps ||A_b||_F, and the seed of the
-    # randomized-SVD fallback's Gaussian test matrices
+    # the seed of the randomized-SVD fallback's Gaussian test matrices, a separate recompression
+    # tolerance (0: eps_aca, the reference), and opt-in per-leaf certification: after assembly
+    # every admissible leaf is regenerated and the ones with ||A_b - U V^H||_F > eps ||A_b||_F are
+    # re-compressed at tighter tolerances until none is (hmatrix.assemble)
     aca_kernel: str = "auto"
     tc_stages: int = 0
-    certify: bool = False
     rsvd_seed: int = 0
+    eps_recompress: float = 0.0
+    certify: bool = False
 
     def __post_init__(self):
         if not (0.0 < self.eps_aca < 1.0):
@@ -52,8 +55,8 @@ class ACAConfig:
         c.aca_kernel = ACA_KERNELS[self.aca_kernel]
         c.mem_budget_gb = self.mem_budget_gb if mem_budget_gb is None else mem_budget_gb
         c.tc_stages = self.tc_stages
-        c.certify = int(bool(self.certify))
         c.rsvd_seed = int(self.rsvd_seed)
+        c.eps_recompress = self.eps_recompress
         return c
 
 

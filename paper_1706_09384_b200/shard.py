@@ -1,13 +1,16 @@
-"""Block-row sharded H-matrix over several processes.
+"""Row-sharded H-matrix over several processes.
 
-One process per GPU.  The admissible and dense leaves are independent
-(SPEC.md:344, 456), so the assembly shards with no collective at all: rank p
-assembles only the leaves of its block-row stripe.  The H-matvec has one
-exchange step: every rank applies its own leaves to the replicated x and the
-partial products are summed with one all-reduce of y (d N complex128, 1.5 MB
-at U32k).  GMRES runs replicated on every rank on top of that matvec; the
-all-reduce hands every rank the same y, so all ranks take the same Krylov
-steps and stop together without further collectives.
+One process per GPU.  The rows [0, N) (tree order) are cut at points no leaf
+straddles into one contiguous owned range per rank, balanced on the leaf
+cost; rank p owns every leaf whose row range lies in its range.  The
+admissible and dense leaves are independent, so the
+assembly shards with no collective at all.  The H-matvec has one exchange
+step: every rank applies its own leaves to the replicated x, which fills
+exactly its owned rows of y, and one all-gather of the owned segments (d N
+complex128 in total, 1.5 MB at U32k) hands every rank the full y.  GMRES runs
+replicated on every rank on top of that matvec; every rank holds the same y,
+so all ranks take the same Krylov steps and stop together without further
+collectives.
 
 The collective goes through ``torch.distributed`` (NCCL on the GPUs, gloo in
 the CPU tests); the per-rank compute is the C-ABI (``hmx_assemble`` on a leaf
@@ -31,24 +34,52 @@ def leaf_cost(table, d, rank_est=None):
     return cost
 
 
-def partition_block_rows(table, n_parts, cost=None, d=3):
-    """Split the leaf list into ``n_parts`` block-row stripes: leaves ordered by
-    (row start, row stop desc, column start), cut into contiguous runs of
-    near-equal cumulative cost.  Returns a list of sorted leaf-index arrays
-    (together a partition of range(len(table)))."""
+def safe_row_cuts(table, n_points):
+    """Tree-order row positions p in [0, N] that no leaf straddles (no leaf has r0 < p < r1):
+    cutting the rows there gives every leaf to exactly one owner of its whole row range."""
     t = np.asarray(table)
-    nb = len(t)
+    diff = np.zeros(int(n_points) + 2, np.int64)
+    np.add.at(diff, t[:, 1] + 1, 1)
+    np.add.at(diff, t[:, 2], -1)
+    inside = np.cumsum(diff)[: int(n_points) + 1]
+    return np.flatnonzero(inside == 0)
+
+
+def partition_row_ranges(table, n_parts, n_points, cost=None, d=3):
+    """Split the rows [0, N) (tree order) into ``n_parts`` contiguous owned ranges at safe cut
+    points, each near an equal share of the cumulative leaf cost; every leaf goes to the owner of
+    its row range.  Returns (parts, bounds): sorted leaf-index arrays (together a partition of
+    range(len(table))) and the n_parts + 1 row bounds."""
+    t = np.asarray(table)
     if n_parts < 1:
         raise ValueError("n_parts must be >= 1")
     if cost is None:
         cost = leaf_cost(t, d)
-    order = np.lexsort((t[:, 3], -t[:, 2], t[:, 1]))
-    cum = np.cumsum(np.asarray(cost, np.float64)[order])
-    total = cum[-1] if nb else 0.0
-    # part p takes the leaves whose cumulative cost ends in (p/P, (p+1)/P] of the total
-    bounds = np.searchsorted(cum, total * np.arange(1, n_parts) / n_parts, side="left")
-    parts = np.split(order, bounds)
-    return [np.sort(p) for p in parts]
+    cost = np.asarray(cost, np.float64)
+    N = int(n_points)
+    safe = safe_row_cuts(t, N)
+    # cumulative cost of the leaves lying entirely below each safe point
+    per_row_end = np.zeros(N + 1)
+    np.add.at(per_row_end, t[:, 2], cost)
+    cum = np.cumsum(per_row_end)[safe]
+    total = float(cost.sum())
+    bounds = [0]
+    for k in range(1, n_parts):
+        target = total * k / n_parts
+        j = int(np.argmin(np.abs(cum - target)))
+        bounds.append(max(int(safe[j]), bounds[-1]))
+    bounds.append(N)
+    bounds = np.asarray(bounds, np.int64)
+    owner = np.searchsorted(bounds, t[:, 1], side="right") - 1
+    parts = [np.flatnonzero(owner == k) for k in range(n_parts)]
+    return parts, bounds
+
+
+def partition_block_rows(table, n_parts, cost=None, d=3, n_points=None):
+    """The leaf parts of :func:`partition_row_ranges` (n_points defaults to the table's extent)."""
+    t = np.asarray(table)
+    N = int(t[:, 2].max()) if n_points is None else int(n_points)
+    return partition_row_ranges(t, n_parts, N, cost=cost, d=d)[0]
 
 
 class LeafSubset:
@@ -62,33 +93,53 @@ class LeafSubset:
         self.rows, self.cols, self.eta = bt.rows, bt.cols, bt.eta
 
 
-def allreduce_sum(y, group=None):
-    """In-place sum of a complex128 torch tensor over the process group (the
-    matvec's exchange step); identity on a single process."""
-    import torch
-    import torch.distributed as dist
+class RowExchange:
+    """The matvec's exchange step: rank k computed the rows it owns (tree rows
+    [bounds[k], bounds[k+1]), i.e. original dofs d perm[t] + a); one all-gather of the owned
+    segments hands every rank the full y (d N complex128, half the bytes of an all-reduce)."""
 
-    if not (dist.is_available() and dist.is_initialized()) or dist.get_world_size(group) == 1:
+    def __init__(self, bounds, perm, d, rank, world, device="cpu", group=None):
+        import torch
+
+        perm = np.asarray(perm, np.int64)
+        self.world, self.rank, self.group = world, rank, group
+        dofs = [(d * perm[bounds[k]:bounds[k + 1]][:, None] + np.arange(d)[None, :]).ravel() for k in range(world)]
+        self.counts = [len(x) for x in dofs]
+        self.L = max(max(self.counts), 1)
+        self.own = torch.as_tensor(dofs[rank], device=device)
+        self.all = torch.as_tensor(np.concatenate(dofs), device=device)
+
+    def __call__(self, y_local):
+        import torch
+        import torch.distributed as dist
+
+        if self.world == 1:
+            return y_local
+        seg = torch.zeros(self.L, dtype=y_local.dtype, device=y_local.device)
+        seg[: self.counts[self.rank]] = y_local[self.own]
+        outs = [torch.empty_like(seg) for _ in range(self.world)]
+        dist.all_gather([torch.view_as_real(o) for o in outs], torch.view_as_real(seg), group=self.group)
+        y = torch.empty_like(y_local)
+        y[self.all] = torch.cat([o[:c] for o, c in zip(outs, self.counts)])
         return y
-    v = torch.view_as_real(y)  # NCCL / gloo reduce real tensors
-    dist.all_reduce(v, op=dist.ReduceOp.SUM, group=group)
-    return y
 
 
-def sharded_matvec(local_apply, x, group=None):
-    """y = sum_p A_p x: ``local_apply(x)`` returns this rank's partial product
-    (a torch tensor), summed over the group."""
-    return allreduce_sum(local_apply(x), group)
+def sharded_matvec(local_apply, x, exchange):
+    """y = sum_p A_p x: ``local_apply(x)`` returns this rank's product (non-zero only on its
+    owned rows); ``exchange`` (a RowExchange) assembles the full y on every rank."""
+    return exchange(local_apply(x))
 
 
 class ShardedHMatrix:
-    """This rank's stripe of a block-row sharded H-matrix."""
+    """This rank's row range of a row-sharded H-matrix."""
 
-    def __init__(self, local, part_idx, n_points, d, group=None):
+    def __init__(self, local, part_idx, n_points, d, bounds=None, exchange=None, group=None):
         self.local = local  # HMatrix of this rank's leaves (None: no leaves)
         self.part_idx = part_idx
         self.n_points = n_points
         self.d = d
+        self.bounds = bounds
+        self.exchange = exchange
         self.group = group
 
     def apply_local(self, x):
@@ -102,19 +153,20 @@ class ShardedHMatrix:
 
     def matvec(self, x):
         """x: CUDA complex128 tensor in original point order (replicated)."""
-        return sharded_matvec(self.apply_local, x, self.group)
+        return sharded_matvec(self.apply_local, x, self.exchange)
 
 
 def assemble_sharded(spec, cloud, ct, bt, cfg, rank, world, group=None, device=0, cost=None):
-    """Assemble rank ``rank``'s block-row stripe (no collective)."""
+    """Assemble rank ``rank``'s owned row range (no collective)."""
     from .hmatrix import assemble
 
-    parts = partition_block_rows(bt.leaf_table, world, cost=cost, d=spec.d)
+    parts, bounds = partition_row_ranges(bt.leaf_table, world, cloud.size, cost=cost, d=spec.d)
     idx = parts[rank]
     local = None
     if len(idx):
         local, _ = assemble(spec, cloud, ct, LeafSubset(bt, idx), cfg, device=device)
-    return ShardedHMatrix(local, idx, cloud.size, spec.d, group)
+    ex = RowExchange(bounds, ct.permutation, spec.d, rank, world, device=f"cuda:{device}", group=group)
+    return ShardedHMatrix(local, idx, cloud.size, spec.d, bounds=bounds, exchange=ex, group=group)
 
 
 def _givens(a, b):

@@ -43,7 +43,7 @@ def test_host_error_paths():
 def test_struct_layouts_match_header():
     # hmx_kernel: int32 kind, int32 pad, 6 doubles
     assert C.sizeof(_lib.HmxKernel) == 8 + 6 * 8
-    assert C.sizeof(_lib.HmxAcaCfg) == 8 + 8 + 8 + 4 + 4 + 8 + 4 + 4 + 8
+    assert C.sizeof(_lib.HmxAcaCfg) == 8 + 8 + 8 + 4 + 4 + 8 + 4 + 4 + 8 + 8
     text = open(os.path.join(ROOT, "include", "hmx.h")).read()
     body = re.search(r"typedef struct \{([^{}]*)\} hmx_stats;", text).group(1)
     n_i64 = sum(len(re.findall(r"\w+", l.split("int64_t", 1)[1].split(";")[0]))

@@ -1,4 +1,4 @@
-"""Block-row sharding on one GPU: every stripe of a 2- and 4-way partition is
+"""Row-range sharding on one GPU: every part of a 2-, 3- and 4-way partition is
 assembled through the C-ABI on its leaf subset; the stripes' device matvecs sum
 to the full H-matvec, and the replicated torch GMRES over the (world-size-1)
 sharded operator takes the device GMRES's iteration count."""

@@ -12,7 +12,8 @@ import torch.distributed as dist
 import torch.multiprocessing as mp
 
 import paper_1706_09384_b200 as hmx
-from paper_1706_09384_b200.shard import gmres, leaf_cost, partition_block_rows, sharded_matvec
+from paper_1706_09384_b200.shard import (RowExchange, gmres, leaf_cost, partition_row_ranges, safe_row_cuts,
+                                         sharded_matvec)
 
 
 def _tree(n=400, leaf=16):
@@ -25,18 +26,32 @@ def _tree(n=400, leaf=16):
 @pytest.mark.parametrize("parts", [1, 2, 3, 8])
 def test_partition_covers_and_balances(parts):
     t = _tree()
+    n = int(t[:, 2].max())
     cost = leaf_cost(t, 1)
-    ps = partition_block_rows(t, parts, cost=cost, d=1)
-    assert len(ps) == parts
+    ps, bounds = partition_row_ranges(t, parts, n, cost=cost, d=1)
+    assert len(ps) == parts and bounds[0] == 0 and bounds[-1] == n and np.all(np.diff(bounds) >= 0)
     allidx = np.concatenate(ps)
     assert np.array_equal(np.sort(allidx), np.arange(len(t)))  # a partition of the leaves
+    safe = set(safe_row_cuts(t, n).tolist())
+    assert all(int(b) in safe for b in bounds)
+    for k, p in enumerate(ps):  # each part owns whole leaves inside its row range
+        assert np.all(t[p, 1] >= bounds[k]) and np.all(t[p, 2] <= bounds[k + 1])
     loads = np.array([cost[p].sum() for p in ps])
-    # contiguous cuts of a cost-ordered list: each stripe within one leaf of the mean
-    assert loads.max() - loads.sum() / parts <= cost.max() + 1e-9
-    # block-row stripes: row starts of stripe p never exceed those of stripe p + 1
-    for a, b in zip(ps[:-1], ps[1:]):
-        if len(a) and len(b):
-            assert t[a, 1].min() <= t[b, 1].min()
+    # cuts only at safe points: a part can be off the mean by at most the cost between two
+    # neighbouring safe cuts
+    per_end = np.zeros(n + 1)
+    np.add.at(per_end, t[:, 2], cost)
+    cum = np.cumsum(per_end)[sorted(safe)]
+    assert loads.max() - loads.sum() / parts <= np.diff(cum).max() + 1e-9
+
+
+def test_safe_cuts_are_cluster_boundaries():
+    t = _tree()
+    n = int(t[:, 2].max())
+    safe = safe_row_cuts(t, n)
+    assert safe[0] == 0 and safe[-1] == n
+    for p in safe:
+        assert not np.any((t[:, 1] < p) & (p < t[:, 2]))
 
 
 def _operator(n, seed=3):
@@ -64,13 +79,25 @@ def _worker(rank, world, port, q):
     t = _tree()
     n = int(t[:, 2].max())
     a = _operator(n)
-    idx = partition_block_rows(t, world, d=1)[rank]
+    parts, bounds = partition_row_ranges(t, world, n, d=1)
+    idx = parts[rank]
     local = _local_apply(a, t, idx)
+    ex = RowExchange(bounds, np.arange(n), 1, rank, world)  # identity permutation: tree = original order
     rng = np.random.default_rng(11)
     x = torch.from_numpy(rng.standard_normal(n) + 1j * rng.standard_normal(n))
-    y = sharded_matvec(local, x)
-    res = gmres(lambda v: sharded_matvec(local, v), x, hmx.GmresConfig(tol=1e-10, restart=7))
-    q.put((rank, len(idx), y.numpy(), res.iters, res.x.numpy(), res.converged))
+    y = sharded_matvec(local, x, ex)
+    res = gmres(lambda v: sharded_matvec(local, v, ex), x, hmx.GmresConfig(tol=1e-10, restart=7))
+    # a non-trivial permutation: rows owned in tree order, y gathered in original order
+    perm = np.random.default_rng(5).permutation(n)
+    ex2 = RowExchange(bounds, perm, 1, rank, world)
+    inv = np.argsort(perm)
+
+    def local_perm(x):  # y_orig[perm[i]] = (A x_tree)[i] restricted to this rank's leaves
+        yt = local(torch.from_numpy(x.numpy()[perm]))
+        return torch.from_numpy(yt.numpy()[inv])
+
+    y2 = sharded_matvec(local_perm, x, ex2)
+    q.put((rank, len(idx), y.numpy(), res.iters, res.x.numpy(), res.converged, y2.numpy()))
     dist.barrier()
     dist.destroy_process_group()
 
@@ -92,8 +119,11 @@ def test_sharded_matvec_and_gmres_world2():
     rng = np.random.default_rng(11)
     x = rng.standard_normal(n) + 1j * rng.standard_normal(n)
     assert res[0][1] > 0 and res[1][1] > 0 and res[0][1] + res[1][1] == len(t)
-    for _, _, y, _, _, _ in res:
+    perm = np.random.default_rng(5).permutation(n)
+    y_perm = (a @ x[perm])[np.argsort(perm)]
+    for _, _, y, _, _, _, y2 in res:
         np.testing.assert_allclose(y, a @ x, rtol=0, atol=1e-12 * np.abs(a @ x).max())
+        np.testing.assert_allclose(y2, y_perm, rtol=0, atol=1e-12 * np.abs(y_perm).max())
     # both ranks got the same y bit for bit, hence the same Krylov steps
     assert np.array_equal(res[0][2], res[1][2])
     assert res[0][3] == res[1][3] and np.array_equal(res[0][4], res[1][4])
