@@ -755,7 +755,7 @@ def shard_arm(args):
     torch.cuda.synchronize()
     e2e_ms = max_over_ranks(f0.elapsed_time(f1), f"cuda:{local}")
     line = {
-        "metric": f"{args.config} H-matvec algorithmic HBM throughput (elasto U), block-row sharded",
+        "metric": f"{args.config} H-matvec algorithmic HBM throughput (elasto U), row-sharded",
         "value": mv_bytes * K / (ms * 1e-3) / 1e9, "unit": "GB/s", "n_gpus": ws, "steps": K, "warmup": W,
         "ms_per_step": ms / K, "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
         "dtype": "c128", "data": "synthetic (Fibonacci sphere, seeded complex Gaussian x, seed 0)",
