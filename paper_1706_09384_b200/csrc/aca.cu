@@ -661,61 +661,58 @@ HMX_D void dmma(double& c0, double& c1, double a, double b) {
                : "d"(a), "d"(b));
 }
 
-// B fragment of a pivot row piv (3 x lds complex) for column l: n < 3 real,
-// 3 <= n < 6 imaginary part of piv(n mod 3, l), else 0
-HMX_D double piv_frag(const double2* piv, int lds, int l, int n) {
-  if (n >= 6) return 0.0;
-  const double2 v = piv[(n < 3 ? n : n - 3) * lds + l];
-  return n < 3 ? v.x : v.y;
+// ---- Blackwell bulk-copy plumbing (TMA engine, async proxy) ------------------------
+// cp.async.bulk moves one contiguous run global -> shared and signals completion as
+// transaction bytes on an mbarrier (SASS UBLKCP / SYNCS); the issuing lane needs no
+// registers for the data and no per-element address arithmetic.
+HMX_D void mbar_init(unsigned a, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
 }
-
-// 16-byte asynchronous global -> shared copy (zero fill when !valid)
-HMX_D void tc_cp16(double2* smem, const double2* gmem, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0));
+HMX_D void mbar_expect_tx(unsigned a, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
 }
-HMX_D void tc_cp16s(unsigned sa, const double2* gmem) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(gmem));
+HMX_D void mbar_wait(unsigned a, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
 }
-HMX_D void tc_cp16sz(unsigned sa, const double2* gmem, bool valid) {
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gmem), "r"(valid ? 16 : 0));
+HMX_D void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
 }
+// generic-proxy accesses of this thread before -> async-proxy accesses after
+HMX_D void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+HMX_D void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
 
 // Fused pass over panel F (rows = 3 npts, ld = rows, K columns) for the row
 // blocks of this warp.  Each column octet of a row block is brought into the
-// warp's shared-memory ring with cp.async kTcStages - 1 octets ahead (no
-// registers held by loads in flight), then feeds both contractions from shared
-// memory.  Residual fragments of each row block are left in resb (aliases the
-// ring: kTcRows x 12 doubles, C1 n = 0..5 then C2 n = 0..5) and `epi(rb_row0)`
-// is called by the whole warp; with pend, the Gram partials of the pending
-// columns [Pc, Pc + 3) go to scr (this warp's slice: noct x 32 lanes x 4).
-// Copy slots: lane element e = lane + 32 i is (column e / kTcRows, row
-// e % kTcRows) of an octet; its shared address and its global offset from the
-// octet's first element are fixed for the pass, only the octet base moves.
-// The Gram B operand (the pending columns of the row block) is read into
-// registers once per row block.
+// warp's shared-memory ring by eight bulk copies (one 48-row column run each,
+// issued by lanes 0-7 on the stage's mbarrier) kTcStages - 1 octets ahead, then
+// feeds both contractions from shared memory.  Residual fragments of each row
+// block are left in resb (aliases the ring: kTcRows x 12 doubles, C1 n = 0..5
+// then C2 n = 0..5) and `epi(rb_row0)` is called by the whole warp; with pend,
+// the Gram partials of the pending columns [Pc, Pc + 3) go to scr (this warp's
+// slice: noct x 32 lanes x 4); the pending columns of the row block ride on the
+// first octet's mbarrier.  `phase` holds the parity of the next wait on each
+// ring stage (bit s), carried across passes.  Rows past the panel's end (last
+// row block) are zeroed in shared memory after the copy lands (the bulk copy
+// writes only the valid rows, so the two proxies never touch the same bytes).
 template <int kTcStages, class Epi>
 HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const double2* piv, int lds, bool pend,
-                   int Pc, double* __restrict__ scr, int noct, double2* ring, double2* nfs, Epi&& epi) {
+                   int Pc, double* __restrict__ scr, int noct, double2* ring, double2* nfs, unsigned bar_sa,
+                   unsigned& phase, Epi&& epi) {
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int fr = lane >> 2, fk = lane & 3;
   double* resb = reinterpret_cast<double*>(ring);
-  constexpr int kSlots = (8 * kTcRows) / 32;
   constexpr unsigned kStageBytes = sizeof(double2) * kTcStage;
   const unsigned ring_sa = (unsigned)__cvta_generic_to_shared(ring);
-  unsigned sa[kSlots];  // shared address in stage 0
-  int goff[kSlots];     // element offset from the octet's (row r0, column 0)
-  int srow[kSlots];     // row within the block
-  int scol[kSlots];     // column within the octet
-#pragma unroll
-  for (int i = 0; i < kSlots; ++i) {
-    const int e = lane + 32 * i;
-    const int col = e / kTcRows, row = e - col * kTcRows;
-    sa[i] = ring_sa + (unsigned)(sizeof(double2) * (col * kTcCol + row));
-    goff[i] = row + col * (int)rows;
-    srow[i] = row;
-    scol[i] = col;
-  }
+  const unsigned nfs_sa = (unsigned)__cvta_generic_to_shared(nfs);
   // B fragment of the residual for column l (pivot row staged with zeros past K)
   const bool bre = fr < 3, bon = fr < 6;
   const int bcol = bre ? fr : (bon ? fr - 3 : 0);  // lanes fr >= 6 read row 0 and use 0
@@ -726,36 +723,28 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
 #endif
   for (int64_t r0 = (int64_t)warp * kTcRows; r0 < rows; r0 += (int64_t)kTcWarps * kTcRows) {
     const int rlim = rows - r0 < (int64_t)kTcRows ? (int)(rows - r0) : kTcRows;  // valid rows of this block
+    const unsigned run = (unsigned)rlim * (unsigned)sizeof(double2);
     const double2* Fr = F + r0;
     auto stage = [&](int co, int buf) {
-      const double2* Fo = Fr + (int64_t)co * 8 * rows;
-      const unsigned so = (unsigned)buf * kStageBytes;
-      const int clim = K - co * 8;  // columns of this octet inside the panel
-      if (rlim == kTcRows && clim >= 8) {
-#pragma unroll
-        for (int i = 0; i < kSlots; ++i) tc_cp16s(sa[i] + so, Fo + goff[i]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < kSlots; ++i) {
-          const bool v = srow[i] < rlim && scol[i] < clim;
-          tc_cp16sz(sa[i] + so, v ? Fo + goff[i] : F, v);
-        }
-      }
-      asm volatile("cp.async.commit_group;");
+      const int clim = min(8, K - co * 8);  // columns of this octet inside the panel
+      const unsigned mb = bar_sa + 8u * (unsigned)buf;
+      const bool with_pend = pend && co == 0;
+      if (lane == 0) mbar_expect_tx(mb, run * (unsigned)(clim + (with_pend ? 3 : 0)));
+      __syncwarp();
+      if (lane < clim)
+        bulk_g2s(ring_sa + (unsigned)buf * kStageBytes + (unsigned)(lane * kTcCol) * (unsigned)sizeof(double2),
+                 Fr + (int64_t)(co * 8 + lane) * rows, run, mb);
+      else if (with_pend && lane >= 8 && lane < 11)
+        bulk_g2s(nfs_sa + (unsigned)((lane - 8) * kTcRows) * (unsigned)sizeof(double2),
+                 Fr + (int64_t)(Pc + lane - 8) * rows, run, mb);
     };
-    // pending columns of this row block (Gram B operand) ride along with stage 0
-    if (pend) {
-      for (int e = lane; e < 3 * kTcRows; e += 32) {
-        const int c = e / kTcRows, row = e - c * kTcRows;
-        const bool v = row < rlim;
-        tc_cp16(nfs + c * kTcRows + row, v ? Fr + row + (int64_t)(Pc + c) * rows : F, v);
-      }
-    }
+    auto wait = [&](int buf) {
+      mbar_wait(bar_sa + 8u * (unsigned)buf, (phase >> buf) & 1u);
+      phase ^= 1u << buf;
+    };
 #pragma unroll
-    for (int sidx = 0; sidx < kTcStages - 1; ++sidx) {
+    for (int sidx = 0; sidx < kTcStages - 1; ++sidx)
       if (sidx < noct) stage(sidx, sidx);
-      else asm volatile("cp.async.commit_group;");
-    }
     double c1[kTcOct][2], c2[kTcOct][2];
 #pragma unroll
     for (int o = 0; o < kTcOct; ++o) c1[o][0] = c1[o][1] = c2[o][0] = c2[o][1] = 0.0;
@@ -776,7 +765,6 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
     }
     for (int co = 0; co < noct; ++co) {
       if (co + kTcStages - 1 < noct) stage(co + kTcStages - 1, (co + kTcStages - 1) % kTcStages);
-      else asm volatile("cp.async.commit_group;");
       double* d = scr + ((int64_t)co * 32 + lane) * 4;
       double g3[2] = {nx[0][0], nx[0][1]}, g4[2] = {nx[0][2], nx[0][3]};
 #pragma unroll
@@ -790,8 +778,21 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
         nx[kTcPf - 1][2] = dn[2];
         nx[kTcPf - 1][3] = dn[3];
       }
-      asm volatile("cp.async.wait_group %0;" ::"n"(kTcStages - 1) : "memory");
-      __syncwarp();
+      const int buf = co % kTcStages;
+      wait(buf);
+      double2* T = ring + buf * kTcStage;  // T[col * kTcCol + row]
+      if (rlim < kTcRows) {  // rows past the panel: zeros (bytes the bulk copy did not write)
+        for (int e = lane; e < 8 * (kTcRows - rlim); e += 32) {
+          const int c = e / (kTcRows - rlim), row = rlim + e % (kTcRows - rlim);
+          T[c * kTcCol + row] = cmk(0.0, 0.0);
+        }
+        if (pend && co == 0)
+          for (int e = lane; e < 3 * (kTcRows - rlim); e += 32) {
+            const int c = e / (kTcRows - rlim), row = rlim + e % (kTcRows - rlim);
+            nfs[c * kTcRows + row] = cmk(0.0, 0.0);
+          }
+        __syncwarp();
+      }
       if (pend && co == 0) {
 #pragma unroll
         for (int j = 0; j < kTcKs; ++j) {
@@ -799,7 +800,6 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
           bj[j] = bon ? (bre ? x.x : x.y) : 0.0;
         }
       }
-      const double2* T = ring + (co % kTcStages) * kTcStage;  // T[col * kTcCol + row]
       const int l0 = co * 8;
       // residual: two k-steps of 4 columns
 #pragma unroll
@@ -834,10 +834,11 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
         d[2] = (h4[0][0] + h4[1][0]) + (h4[2][0] + h4[3][0]);
         d[3] = (h4[0][1] + h4[1][1]) + (h4[2][1] + h4[3][1]);
       }
-      __syncwarp();  // this buffer is refilled by the next iteration's prefetch
+      // this buffer is refilled by the next iteration's prefetch (async proxy): order
+      // this iteration's generic shared-memory accesses before it
+      fence_async_smem();
+      __syncwarp();
     }
-    asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncwarp();
     // residual fragments -> shared memory (rows of this block; the ring is idle now)
 #pragma unroll
     for (int o = 0; o < kTcOct; ++o)
@@ -852,6 +853,10 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
     __syncwarp();
     TC_WMARK(8);
     epi(r0);
+    // the epilogue's panel-column stores (generic proxy) are read back by later bulk copies;
+    // its shared-memory accesses precede the next row block's copies into the ring
+    fence_async_global();
+    fence_async_smem();
     __syncwarp();
     TC_WMARK(9);
     first = false;
@@ -896,6 +901,7 @@ __global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
   extern __shared__ double2 dyn[];
   __shared__ Shared sh;
   __shared__ int s_pend;
+  __shared__ __align__(8) unsigned long long tc_bar[kTcWarps][STAGES];  // per-warp ring mbarriers
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int b = order[blockIdx.x];
   const AcaDesc ds = desc[b];
@@ -919,6 +925,14 @@ __global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
   const int nwork_u = min(NW, (int)((ldu + kTcRows - 1) / kTcRows));
 
   for (int i = tid; i < m; i += NT) visited[i] = 0;
+  // ring stages start zeroed (copies past a short last octet leave earlier, finite data)
+  for (int t = lane; t < kTcRing; t += 32) ring[t] = cmk(0.0, 0.0);
+  const unsigned bar_sa = (unsigned)__cvta_generic_to_shared(&tc_bar[warp][0]);
+  if (lane == 0)
+    for (int st = 0; st < STAGES; ++st) mbar_init(bar_sa + 8u * st, 1);
+  unsigned phase = 0;
+  fence_async_smem();
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   if (tid == 0) {
     sh.ipiv = 0;
     sh.K = 0;
@@ -966,7 +980,7 @@ __global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
     // ---- row pass over V ----------------------------------------------------------------
     ArgMax best{-1.0, 0x7fffffff};
     double rs1 = 0.0;
-    tc_pass<STAGES>(Vb, ldv, K, Urow, lds, pend, Pc, wscr, noct, ring, nfw, [&](int64_t r0) {
+    tc_pass<STAGES>(Vb, ldv, K, Urow, lds, pend, Pc, wscr, noct, ring, nfw, bar_sa, phase, [&](int64_t r0) {
       // lanes 0..15: point j = r0 / 3 + lane, rows 3 lane + c of the block
       const int p = lane;
       const int j = (int)(r0 / 3) + p;
@@ -1084,7 +1098,7 @@ __global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
 
     // ---- column pass over U ---------------------------------------------------------------
     best = ArgMax{-1.0, 0x7fffffff};
-    tc_pass<STAGES>(Ub, ldu, K, Vrow, lds, pend, Pc, wscr, noct, ring, nfw, [&](int64_t r0) {
+    tc_pass<STAGES>(Ub, ldu, K, Vrow, lds, pend, Pc, wscr, noct, ring, nfw, bar_sa, phase, [&](int64_t r0) {
       const int p = lane;
       const int i = (int)(r0 / 3) + p;
       if (p < kTcRows / 3 && i < m) {
@@ -1207,6 +1221,11 @@ int launch_aca(Ctx& c, int d, const GreenParams& P, const PointsSoA& pts, const 
     // 3-stage ring when it fits in shared memory, else 2 stages, else the CUDA-core kernel
     int smem_max = 0;
     HMX_CUDA_TRY(cudaDeviceGetAttribute(&smem_max, cudaDevAttrMaxSharedMemoryPerBlockOptin, c.device));
+    {
+      cudaFuncAttributes fa;  // static shared memory (Shared + mbarriers) shares the opt-in limit
+      HMX_CUDA_TRY(cudaFuncGetAttributes(&fa, aca_tc_kernel<1, 3>));
+      smem_max -= (int)fa.sharedSizeBytes;
+    }
     const int want = tc_stages > 0 ? tc_stages : 3;
     const int stages = want >= 3 && aca_tc_smem(kcap_max, m_max, 3) <= (size_t)smem_max ? 3
                        : aca_tc_smem(kcap_max, m_max, 2) <= (size_t)smem_max ? 2
