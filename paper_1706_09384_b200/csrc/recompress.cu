@@ -159,6 +159,100 @@ __device__ void cta_zgemm(int M, int N, int Kd, const double2* A, int lda, const
   __syncthreads();
 }
 
+// The same product on the FP64 tensor cores for 512-thread CTAs (the large-K class): 16 warps,
+// 64 x 64 complex output tiles, k chunks of 16 staged (conjugated / transposed as op() asks) in
+// shared memory; each warp owns 32 rows x 8 complex columns as two real mma.sync m8n8k4 f64 per
+// 8 x 4 block with B = [op(B)_re | op(B)_im] (the fragment layout of form_gemm below).
+constexpr int kGemmTileTc = 2 * 16 * 66;
+HMX_D void dmma_acc(double& c0, double& c1, double a, double b) {
+  asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+               : "+d"(c0), "+d"(c1)
+               : "d"(a), "d"(b));
+}
+template <bool ACT, bool BCT>
+__device__ void cta_zgemm_tc(int M, int N, int Kd, const double2* A, int lda, const double2* B, int ldb, double2* C,
+                             int ldc, double2* tile) {
+  constexpr int NT = 512, BM = 64, BN = 64, BK = 16, LDS = BM + 2;
+  double2* As = tile;             // [BK][LDS]: op(A)(i0 + ii, k0 + kk) at kk * LDS + ii
+  double2* Bs = tile + BK * LDS;  // [BK][LDS]: op(B)(k0 + kk, j0 + jj) at kk * LDS + jj
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int wm = warp & 1, wn = warp >> 1;  // warp tile: rows wm*32 + [0,32), cols wn*8 + [0,8)
+  const int fr = lane >> 2, fk = lane & 3, t4 = lane & 3;
+  for (int i0 = 0; i0 < M; i0 += BM)
+    for (int j0 = 0; j0 < N; j0 += BN) {
+      double c1[4][2][2], c2[4][2][2];
+#pragma unroll
+      for (int o = 0; o < 4; ++o)
+#pragma unroll
+        for (int g = 0; g < 2; ++g) c1[o][g][0] = c1[o][g][1] = c2[o][g][0] = c2[o][g][1] = 0.0;
+      for (int k0 = 0; k0 < Kd; k0 += BK) {
+        for (int t = tid; t < BM * BK; t += NT) {
+          int ii, kk;
+          if (ACT) {
+            kk = t % BK;
+            ii = t / BK;
+          } else {
+            ii = t % BM;
+            kk = t / BM;
+          }
+          const int gi = i0 + ii, gk = k0 + kk;
+          double2 v = cmk(0.0, 0.0);
+          if (gi < M && gk < Kd) v = ACT ? cconj(A[gk + (int64_t)gi * lda]) : A[gi + (int64_t)gk * lda];
+          As[kk * LDS + ii] = v;
+        }
+        for (int t = tid; t < BK * BN; t += NT) {
+          int kk, jj;
+          if (BCT) {
+            jj = t % BN;
+            kk = t / BN;
+          } else {
+            kk = t % BK;
+            jj = t / BK;
+          }
+          const int gk = k0 + kk, gj = j0 + jj;
+          double2 v = cmk(0.0, 0.0);
+          if (gk < Kd && gj < N) v = BCT ? cconj(B[gj + (int64_t)gk * ldb]) : B[gk + (int64_t)gj * ldb];
+          Bs[kk * LDS + jj] = v;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int ks = 0; ks < BK; ks += 4) {
+          double2 av[4];
+#pragma unroll
+          for (int o = 0; o < 4; ++o) av[o] = As[(ks + fk) * LDS + wm * 32 + o * 8 + fr];
+          double bv[2];
+#pragma unroll
+          for (int g = 0; g < 2; ++g) {
+            const double2 w = Bs[(ks + fk) * LDS + wn * 8 + g * 4 + (fr & 3)];
+            bv[g] = fr < 4 ? w.x : w.y;
+          }
+#pragma unroll
+          for (int o = 0; o < 4; ++o)
+#pragma unroll
+            for (int g = 0; g < 2; ++g) {
+              dmma_acc(c1[o][g][0], c1[o][g][1], av[o].x, bv[g]);
+              dmma_acc(c2[o][g][0], c2[o][g][1], av[o].y, bv[g]);
+            }
+        }
+        __syncthreads();
+      }
+#pragma unroll
+      for (int o = 0; o < 4; ++o)
+#pragma unroll
+        for (int g = 0; g < 2; ++g)
+#pragma unroll
+          for (int i = 0; i < 2; ++i) {
+            const double p1 = __shfl_xor_sync(0xffffffffu, c1[o][g][i], 2);
+            const double p2 = __shfl_xor_sync(0xffffffffu, c2[o][g][i], 2);
+            if (t4 < 2) {
+              const int gr = i0 + wm * 32 + o * 8 + fr, gc = j0 + wn * 8 + g * 4 + 2 * t4 + i;
+              if (gr < M && gc < N) C[gr + (int64_t)gc * ldc] = cmk(c1[o][g][i] - p2, p1 + c2[o][g][i]);
+            }
+          }
+    }
+  __syncthreads();
+}
+
 // Householder reduction of the Hermitian E (K x K, ld K, full storage) to a
 // real symmetric tridiagonal (d, e): E = Q T Q^H, Q = H_0 ... H_{K-2},
 // H_k = I - tau_k v_k v_k^H (LAPACK zhetd2 / zlarfg conventions, beta real).
@@ -771,8 +865,13 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : (
   // ---- T = R G_U (B), E = T R^H --------------------------------------------------
   if constexpr (!SMEM) {
     // large K: shared-memory tiled products (the naive loops are L2-latency bound)
-    cta_zgemm<NT, false, false>(K, K, K, A, K, GU, kcap, B, K, gtile);
-    cta_zgemm<NT, false, true>(K, K, K, B, K, A, K, E, K, gtile);
+    if constexpr (NT == 512) {
+      cta_zgemm_tc<false, false>(K, K, K, A, K, GU, kcap, B, K, gtile);
+      cta_zgemm_tc<false, true>(K, K, K, B, K, A, K, E, K, gtile);
+    } else {
+      cta_zgemm<NT, false, false>(K, K, K, A, K, GU, kcap, B, K, gtile);
+      cta_zgemm<NT, false, true>(K, K, K, B, K, A, K, E, K, gtile);
+    }
   } else {
     for (int t = tid; t < K * K; t += NT) {
       const int i = t % K, j = t / K;
@@ -900,7 +999,10 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : (
   double2* Wu = Wuv;
   double2* Wv = Wuv + (int64_t)K * r;
   if constexpr (!SMEM) {
-    cta_zgemm<NT, true, false>(K, r, K, A, K, B, K, Wu, K, gtile);
+    if constexpr (NT == 512)
+      cta_zgemm_tc<true, false>(K, r, K, A, K, B, K, Wu, K, gtile);
+    else
+      cta_zgemm<NT, true, false>(K, r, K, A, K, B, K, Wu, K, gtile);
     for (int t = tid; t < K * r; t += NT) Wu[t] = cscale(Wu[t], 1.0 / sqrt(sqrt(lam[ordr[t / K]])));
   } else {
     for (int t = tid; t < K * r; t += NT) {
@@ -1102,7 +1204,7 @@ int launch_recompress_core(Ctx& c, const RecDesc* d_desc, int64_t nblk, int kmax
     }
   } else {
     // large K: few long CTAs whose O(K^3) phases are L2-latency bound -> more warps
-    const size_t smem = vec + sizeof(double2) * kGemmTile;
+    const size_t smem = vec + sizeof(double2) * kGemmTileTc;
     constexpr int nt = 512;
     if (nt == 1024) {
       HMX_CUDA_TRY(cudaFuncSetAttribute(recompress_core<0, 1024>, cudaFuncAttributeMaxDynamicSharedMemorySize,
