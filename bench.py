@@ -732,6 +732,11 @@ def shard_arm(args):
     if ws > 1:
         tdist.barrier()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    from paper_1706_09384_b200 import _lib
+
+    L = _lib.lib()
+    if sh.local is not None:
+        _lib.check(L.hmx_profile_begin(sh.local.handle), "profile")
     with ClockSampler(local) as clk:
         torch.cuda.synchronize()
         e0.record()
@@ -740,6 +745,16 @@ def shard_arm(args):
         e1.record()
         torch.cuda.synchronize()
     ms = max_over_ranks(e0.elapsed_time(e1), f"cuda:{local}")
+    # roofline of the dominant kernel (this rank's row GEMV), the slowest rank's rate
+    ph = np.zeros(4)
+    ncalls = C.c_int64()
+    if sh.local is not None:
+        _lib.check(L.hmx_profile_end(sh.local.handle, C.byref(ncalls), _lib.ptr(ph)), "profile")
+    p2_ms = ph[2] / max(int(ncalls.value), 1)
+    p2_gbs = st["phase2_bytes"] / (p2_ms * 1e-3) / 1e9 if p2_ms > 0 else 0.0
+    p2_gbs = -max_over_ranks(-p2_gbs, f"cuda:{local}")  # min over ranks
+    peaks, peak_kind = measured_peaks()
+    hbm_peak = float(peaks.get("hbm_gbs", FALLBACK_HBM_GBS))
     # e2e: pinned host x -> device, sharded matvec, y -> pinned host, every step
     Xh = X.pin_memory()
     Yh = torch.empty(n, dtype=torch.complex128).pin_memory()
@@ -766,6 +781,11 @@ def shard_arm(args):
         "gpu_launches": 4 * K,
         "e2e": {"value": mv_bytes * K / (e2e_ms * 1e-3) / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 16 * n,
                 "d2h_bytes_per_step": 16 * n, "ms_per_step": e2e_ms / K},
+        "roofline": {"bound": "hbm", "kernel": "mv_phase2", "achieved": p2_gbs, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": p2_gbs / hbm_peak, "traffic": None,
+                     "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)" if peak_kind == "measured"
+                     else "fallback 6.65 TB/s (B200_PROFILING.md)",
+                     "note": "per-rank row-GEMV rate, slowest rank"},
         "assembly": {"wall_s_max_over_ranks": t_asm, "leaves_this_rank": int(len(sh.part_idx)),
                      "row_bounds": [int(v) for v in sh.bounds]},
         "clocks": clk.summary(),

@@ -1,7 +1,7 @@
-# Refresh the round's profile evidence on one B200 (run under gpurun; the
-# gpurun_out/ merge limit is 64 MiB, so the recompress capture is part 2):
-#   bash tools/profile_round.sh 1   bench line, ncu launch list, ncu --set full of aca / mv / estimator / form
-#   bash tools/profile_round.sh 2   ncu --set full of recompress_core (4 launches)
+# Refresh the round's profile evidence on one B200 (run under gpurun; the gpurun_out/ merge limit is
+# 64 MiB, so the captures are split in two parts):
+#   bash tools/profile_round.sh 1   bench line, ncu launch list, ncu --set full of the TC ACA / matvec / form
+#   bash tools/profile_round.sh 2   ncu --set full of recompress_core (both modes) and the estimator
 set -x
 mkdir -p gpurun_out
 if [ "${1:-1}" = "1" ]; then
@@ -13,11 +13,11 @@ ncu --set full --import-source on --clock-control none -k regex:"aca_(tc_)?kerne
     python tools/ncu_target.py U32k 1 > gpurun_out/ncu_aca.log 2>&1
 ncu --set full --import-source on --clock-control none -k regex:mv_phase -c 2 -o gpurun_out/prof_mv \
     python tools/ncu_target.py U32k 1 > gpurun_out/ncu_mv.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:err_tiles -c 1 -o gpurun_out/prof_est \
-    python tools/est_target.py U32k > gpurun_out/ncu_est.log 2>&1
-ncu --set full --import-source on --clock-control none -k regex:form_gemm -c 2 -o gpurun_out/prof_form \
+ncu --set full --import-source on --clock-control none -k regex:form_gemm -c 1 -o gpurun_out/prof_form \
     python tools/ncu_target.py U32k 1 > gpurun_out/ncu_form.log 2>&1
 else
-ncu --set full --clock-control none -k regex:recompress_core -c 4 -o gpurun_out/prof_rc \
+ncu --set full --clock-control none -k regex:recompress_core -c 3 -o gpurun_out/prof_rc \
     python tools/ncu_target.py U32k 1 > gpurun_out/ncu_rc.log 2>&1
+ncu --set full --import-source on --clock-control none -k regex:err_tiles -c 1 -o gpurun_out/prof_est \
+    python tools/est_target.py U32k > gpurun_out/ncu_est.log 2>&1
 fi
