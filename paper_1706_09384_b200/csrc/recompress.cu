@@ -1081,10 +1081,10 @@ __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __rest
   const int fr = lane >> 2, fk = lane & 3;  // fragment row / k (A), column group lane / k (B)
   const int row0 = tm * TM, col0 = tn * TN;
   const int nk = (ds.K + TK - 1) / TK;
-  // valid row octets / 4-column groups of this warp's 32 x 8 sub-tile (small r,
-  // short last row tile: the MMAs on the zero padding are skipped)
+  // valid row octets of this warp's 32 x 8 sub-tile, and whether any of its 8 columns is inside
+  // the item (small r, short last row tile: the MMAs on the padding are skipped)
   const int no = min(4, max(0, (ds.rows - (row0 + wm * 32) + 7) / 8));
-  const int ng = min(2, max(0, (ds.r - (col0 + wn * 8) + 3) / 4));
+  const bool colv = col0 + wn * 8 < ds.r;
   auto stage = [&](int kc, int buf) {
     const int k0 = kc * TK;
     for (int t = tid; t < TK * TM; t += kFormThreads) {
@@ -1100,11 +1100,12 @@ __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __rest
       cp_async16(&Ws[buf][kk][cc], W + (v ? gk + (int64_t)gc * ds.K : 0), v);
     }
   };
-  double c1[4][2][2], c2[4][2][2];  // [row octet][column group][2]
+  // complex product with three real products (Gauss): T1 = A_re W_re, T2 = A_im W_im,
+  // T3 = (A_re + A_im)(W_re + W_im); C = (T1 - T2) + i (T3 - T1 - T2) -- 3 MMAs per row octet and
+  // 8 complex columns instead of 4
+  double t1[4][2], t2[4][2], t3[4][2];  // [row octet][2]: C[r][2 t + i] at lane 4 r + t
 #pragma unroll
-  for (int o = 0; o < 4; ++o)
-#pragma unroll
-    for (int g = 0; g < 2; ++g) c1[o][g][0] = c1[o][g][1] = c2[o][g][0] = c2[o][g][1] = 0.0;
+  for (int o = 0; o < 4; ++o) t1[o][0] = t1[o][1] = t2[o][0] = t2[o][1] = t3[o][0] = t3[o][1] = 0.0;
 #pragma unroll
   for (int sidx = 0; sidx < kFormStages - 1; ++sidx) {
     if (sidx < nk) stage(sidx, sidx);
@@ -1118,43 +1119,29 @@ __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __rest
     const int buf = kc % kFormStages;
 #pragma unroll
     for (int ks = 0; ks < TK; ks += 4) {
-      double2 av[4];
-#pragma unroll
-      for (int o = 0; o < 4; ++o) av[o] = As[buf][ks + fk][wm * 32 + o * 8 + fr];
-      double bv[2];
-#pragma unroll
-      for (int g = 0; g < 2; ++g) {
-        // B[k][n], n = fr: n < 4 -> W_re(k, 4 g + n), else W_im(k, 4 g + n - 4)
-        const double2 w = Ws[buf][ks + fk][wn * 8 + g * 4 + (fr & 3)];
-        bv[g] = fr < 4 ? w.x : w.y;
-      }
+      // B[k][n] at lane 4 n + k: column wn * 8 + fr of W, row ks + fk
+      const double2 w = Ws[buf][ks + fk][wn * 8 + fr];
+      const double br = w.x, bi = w.y, bs = w.x + w.y;
 #pragma unroll
       for (int o = 0; o < 4; ++o)
-#pragma unroll
-        for (int g = 0; g < 2; ++g)
-          if (o < no && g < ng) {  // warp-uniform: no MMAs on row octets / column groups past the item
-            dmma_8x8x4(c1[o][g][0], c1[o][g][1], av[o].x, bv[g]);
-            dmma_8x8x4(c2[o][g][0], c2[o][g][1], av[o].y, bv[g]);
-          }
+        if (o < no && colv) {  // warp-uniform
+          const double2 a = As[buf][ks + fk][wm * 32 + o * 8 + fr];
+          dmma_8x8x4(t1[o][0], t1[o][1], a.x, br);
+          dmma_8x8x4(t2[o][0], t2[o][1], a.y, bi);
+          dmma_8x8x4(t3[o][0], t3[o][1], a.x + a.y, bs);
+        }
     }
   }
   cp_async_wait<0>();
-  // lane (r, t): t < 2 holds re*re / im*re parts of columns 2t, 2t+1; the
-  // partner lane t + 2 the re*im / im*im parts of the same columns
   const int t = lane & 3;
 #pragma unroll
   for (int o = 0; o < 4; ++o)
 #pragma unroll
-    for (int g = 0; g < 2; ++g)
-#pragma unroll
-      for (int i = 0; i < 2; ++i) {
-        const double p1 = __shfl_xor_sync(0xffffffffu, c1[o][g][i], 2);
-        const double p2 = __shfl_xor_sync(0xffffffffu, c2[o][g][i], 2);
-        if (t < 2) {
-          const int gr = row0 + wm * 32 + o * 8 + fr, gc = col0 + wn * 8 + g * 4 + 2 * t + i;
-          if (gr < ds.rows && gc < ds.r) C[gr + (int64_t)gc * ds.ldc] = cmk(c1[o][g][i] - p2, p1 + c2[o][g][i]);
-        }
-      }
+    for (int i = 0; i < 2; ++i) {
+      const int gr = row0 + wm * 32 + o * 8 + fr, gc = col0 + wn * 8 + 2 * t + i;
+      if (gr < ds.rows && gc < ds.r)
+        C[gr + (int64_t)gc * ds.ldc] = cmk(t1[o][i] - t2[o][i], t3[o][i] - t1[o][i] - t2[o][i]);
+    }
 }
 constexpr size_t kFormSmem = sizeof(double2) * kFormStages * TK * ((TM + 2) + (TN + 2));
 
