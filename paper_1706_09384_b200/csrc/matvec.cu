@@ -304,10 +304,19 @@ int build_matvec_plan(DeviceH& H, const PlanPre* pre_in) {
   }
   H.v_elems = vo;
   std::vector<MvTile2> tiles;
+  // tile height: 256 rows (one thread per row), lowered to 128 / 64 / 32 rows for segments whose
+  // 256-row tile would carry more than a fair share of the phase-2 bytes (the kernel then splits the
+  // columns over 2 / 4 / 8 thread groups): the widest segments no longer leave one long CTA per
+  // tile running after the rest (small configurations, few tiles per SM)
+  double p2_total = 0.0;
+  for (int64_t g = 0; g < ns; ++g) p2_total += 16.0 * (double)d * (segs[g].second - segs[g].first) * ncols[g];
+  const double fair = p2_total / (4.0 * (double)std::max(1, H.ctx->num_sms));
   for (int64_t g = 0; g < ns; ++g) {
     if (ncols[g] == 0) continue;
     const int64_t rows = d * (segs[g].second - segs[g].first);
-    for (int64_t r0 = 0; r0 < rows; r0 += kThreads) {
+    int64_t th = kThreads;
+    while (th > 32 && 16.0 * (double)std::min<int64_t>(th, rows) * ncols[g] > fair) th /= 2;
+    for (int64_t r0 = 0; r0 < rows; r0 += th) {
       MvTile2 t;
       t.moff = moff[g];
       t.soff = soff[g];
@@ -315,7 +324,7 @@ int build_matvec_plan(DeviceH& H, const PlanPre* pre_in) {
       t.ld = (int32_t)rows;
       t.ncols = (int32_t)ncols[g];
       t.row0 = (int32_t)r0;
-      t.nrows = (int32_t)std::min<int64_t>(kThreads, rows - r0);
+      t.nrows = (int32_t)std::min<int64_t>(th, rows - r0);
       tiles.push_back(t);
     }
   }
