@@ -515,6 +515,18 @@ __device__ void tridiag_ql(double* d, double* e, double* Z, int ldz, int K, doub
 // in descending-eigenvalue order.  A vector that is mostly in the span of the
 // previous ones (near-degenerate cluster) makes the caller fall back to QL.
 // three shifts at once (independent recurrences interleave in the pipeline)
+// Reciprocal from the MUFU approximation (rcp.approx.ftz.f64, ~23 bits) refined by NR Newton steps
+// (each squares the relative error: 2 steps ~2^-46, 3 steps full precision): the Sturm and twisted
+// recurrences are chains of divisions, and a full IEEE division is a longer dependent sequence.
+template <int NR>
+HMX_D double rcp_nr(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+#pragma unroll
+  for (int k = 0; k < NR; ++k) r = fma(r, fma(-q, r, 1.0), r);
+  return r;
+}
+
 HMX_D void sturm_count3(const double* d, const double* e2, int K, double x1, double x2, double x3, double pivmin,
                         int& c1, int& c2, int& c3) {
   double q1 = d[0] - x1, q2 = d[0] - x2, q3 = d[0] - x3;
@@ -524,9 +536,11 @@ HMX_D void sturm_count3(const double* d, const double* e2, int K, double x1, dou
   int n1 = q1 < 0.0, n2 = q2 < 0.0, n3 = q3 < 0.0;
   for (int i = 1; i < K; ++i) {
     const double di = d[i], ei = e2[i - 1];
-    q1 = (di - x1) - ei / q1;
-    q2 = (di - x2) - ei / q2;
-    q3 = (di - x3) - ei / q3;
+    // a Sturm count is backward stable: the ~2^-46 reciprocal perturbs T by far less than dstebz's
+    // absolute tolerance (ulp ||T||) the bisection stops at
+    q1 = (di - x1) - ei * rcp_nr<2>(q1);
+    q2 = (di - x2) - ei * rcp_nr<2>(q2);
+    q3 = (di - x3) - ei * rcp_nr<2>(q3);
     if (fabs(q1) < pivmin) q1 = -pivmin;
     if (fabs(q2) < pivmin) q2 = -pivmin;
     if (fabs(q3) < pivmin) q3 = -pivmin;
@@ -652,7 +666,7 @@ HMX_D void twisted_vector(const double* d, const double* e, int K, double lam, d
   double dp = d[0] - lam;
   for (int i = 0; i + 1 < K; ++i) {
     if (fabs(dp) < pivmin) dp = dp < 0.0 ? -pivmin : pivmin;
-    const double L = e[i] / dp;
+    const double L = e[i] * rcp_nr<3>(dp);
     zc[i] = cmk(L, dp);
     dp = (d[i + 1] - lam) - L * e[i];
   }
@@ -664,7 +678,7 @@ HMX_D void twisted_vector(const double* d, const double* e, int K, double lam, d
   int k = K - 1;
   for (int i = K - 1; i >= 1; --i) {
     if (fabs(dm) < pivmin) dm = dm < 0.0 ? -pivmin : pivmin;
-    const double U = e[i - 1] / dm;
+    const double U = e[i - 1] * rcp_nr<3>(dm);
     scratch[i] = U;
     dm = (d[i - 1] - lam) - U * e[i - 1];
     const double g = fabs(zc[i - 1].y + dm - (d[i - 1] - lam));
