@@ -50,6 +50,16 @@ constexpr int kGramGroup = HMX_GRAM_GROUP;  // factor columns per warp in the Gr
 #endif
 constexpr int kGramBatch = HMX_GRAM_BATCH;  // steps per Gram pass (max)
 
+// Reciprocal from the MUFU approximation refined by three Newton steps (full double precision):
+// the sigma Newton iterations below are chains of divisions
+HMX_D double rcp3(double q) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(q));
+#pragma unroll
+  for (int k = 0; k < 3; ++k) r = fma(r, fma(-q, r, 1.0), r);
+  return r;
+}
+
 // sigma_1 and sigma_3 of a 3x3 complex matrix from the characteristic
 // polynomial of R^H R: c2 = ||R||_F^2, c1 = sum |2x2 minors|^2 (Cauchy-Binet),
 // c0 = |det R|^2.  Smallest root by Newton from c0/c1 (monotone from below on
@@ -91,7 +101,7 @@ HMX_D void svals3(const double2* R, double& s1, double& s3) {
     const double f = ((lam - c2) * lam + c1) * lam - c0;
     const double fp = (3.0 * lam - 2.0 * c2) * lam + c1;
     if (!(fp > 0.0)) break;
-    const double nl = lam - f / fp;
+    const double nl = lam - f * rcp3(fp);
     if (!(nl < lam)) break;
     lam = nl;
   }
@@ -100,13 +110,13 @@ HMX_D void svals3(const double2* R, double& s1, double& s3) {
     s3 = 0.0;
     return;
   }
-  double mu = c0 / c1;
+  double mu = c0 * rcp3(c1);
 #pragma unroll 1
   for (int it = 0; it < 60; ++it) {
     const double f = ((mu - c2) * mu + c1) * mu - c0;
     const double fp = (3.0 * mu - 2.0 * c2) * mu + c1;
     if (!(fp > 0.0)) break;
-    const double nm = mu - f / fp;
+    const double nm = mu - f * rcp3(fp);
     if (!(nm > mu)) break;
     mu = nm;
   }
