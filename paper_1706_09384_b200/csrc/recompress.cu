@@ -740,6 +740,73 @@ __device__ bool cgs2_columns(double2* Zr, int K, int r, double* h, double* red) 
   return s_bad == 0;
 }
 
+// L_r = Q Z_r with Q = H_0 H_1 ... H_{K-2} (H_k = I - tau_k v_k v_k^H, v_k zero above row k + 1 and
+// 1 there) applied to B (K x r) in blocks of NB reflectors as the compact WY form (LAPACK zlarft,
+// forward / columnwise): Q_blk = I - V T V^H, B <- B - V (T (V^H B)), last block first.  A handful
+// of barriers per block instead of two per reflector.  scr: 2 NB r + NB^2 complex (L2).
+template <int NT, int NB>
+__device__ void backxf_blocked(const double2* E, const double2* Hv, bool hv_packed, const double2* tau, int K, int r,
+                               double2* B, double2* scr) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double2* Wm = scr;           // NB x r: V^H B
+  double2* W2 = scr + NB * r;  // NB x r: T V^H B
+  double2* S = W2 + NB * r;    // NB x NB: V^H V, overwritten by the strictly upper T
+  auto vget = [&](int i, int k) -> double2 {  // v_k at global row i
+    if (i <= k) return cmk(0.0, 0.0);
+    if (i == k + 1) return cmk(1.0, 0.0);
+    return hv_packed ? E[pk_col(k, K) + (i - k)] : Hv[i + (int64_t)k * K];
+  };
+  const int nref = K - 1;
+  for (int k0 = ((nref - 1) / NB) * NB; k0 >= 0; k0 -= NB) {
+    const int nb = min(NB, nref - k0);
+    for (int t = tid; t < nb * nb + nb * r; t += NT) {
+      if (t < nb * nb) {  // S(q, i) = v_q^H v_i, q < i
+        const int q = t % nb, i = t / nb;
+        if (q >= i) continue;
+        double2 acc = cmk(0.0, 0.0);
+        for (int row = k0 + i + 1; row < K; ++row) acc = cfma_ca(vget(row, k0 + q), vget(row, k0 + i), acc);
+        S[q + i * NB] = acc;
+      } else {  // Wm(j, c) = v_j^H B(:, c)
+        const int u = t - nb * nb, j = u % nb, c = u / nb;
+        double2 acc = cmk(0.0, 0.0);
+        for (int row = k0 + j + 1; row < K; ++row) acc = cfma_ca(vget(row, k0 + j), B[row + (int64_t)c * K], acc);
+        Wm[j + c * NB] = acc;
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {  // T(q, i) = -tau_i sum_{p = q..i-1} T(q, p) S(p, i), T(p, p) = tau_p
+      for (int i = 1; i < nb; ++i) {
+        double2 val = cmk(0.0, 0.0);
+        if (lane < i) {
+          val = cmul(tau[k0 + lane], S[lane + i * NB]);
+          for (int p2 = lane + 1; p2 < i; ++p2) val = cfma(S[lane + p2 * NB], S[p2 + i * NB], val);
+          val = cmul(cscale(tau[k0 + i], -1.0), val);
+        }
+        __syncwarp();
+        if (lane < i) S[lane + i * NB] = val;
+        __syncwarp();
+      }
+    }
+    __syncthreads();
+    for (int t = tid; t < nb * r; t += NT) {  // W2 = T Wm
+      const int j = t % nb, c = t / nb;
+      double2 acc = cmul(tau[k0 + j], Wm[j + c * NB]);
+      for (int p2 = j + 1; p2 < nb; ++p2) acc = cfma(S[j + p2 * NB], Wm[p2 + c * NB], acc);
+      W2[j + c * NB] = acc;
+    }
+    __syncthreads();
+    const int nrow = K - (k0 + 1);
+    for (int t = tid; t < nrow * r; t += NT) {  // B -= V W2
+      const int i = k0 + 1 + t % nrow, c = t / nrow;
+      double2 acc = cmk(0.0, 0.0);
+      const int jmax = min(nb, i - k0);  // v_{k0 + j} is zero at row i for k0 + j >= i
+      for (int j = 0; j < jmax; ++j) acc = cfma(vget(i, k0 + j), W2[j + c * NB], acc);
+      B[i + (int64_t)c * K] = csub(B[i + (int64_t)c * K], acc);
+    }
+    __syncthreads();
+  }
+}
+
 // truncation rank (oracle/lowrank.py truncation_rank) from eigenvalues
 // lam[ordr[k]] in descending order; thread 0 writes r
 HMX_D void recompress_truncate(const double* lam, const int* ordr, int K, double eps, int rule, int& r_out) {
@@ -988,7 +1055,9 @@ __global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : (
   if (r == 0) return;
   // ---- L_r = Q Z_r : B (K x r) ------------------------------------------------------
   RC_MARK(5);
-  for (int k = K - 2; k >= 0; --k) {
+  constexpr int kWyBlock = 16;
+  if (K >= 24) backxf_blocked<NT, kWyBlock>(E, Hv, hv_packed, tau, K, r, B, Wuv);
+  for (int k = K >= 24 ? -1 : K - 2; k >= 0; --k) {
     const double2 tk = tau[k];
     if (tk.x == 0.0 && tk.y == 0.0) continue;
     const int n = K - k - 1;
