@@ -133,13 +133,12 @@ int rsvd_dense(Ctx& c, const double2* A, int64_t m, int64_t n, double eps, int o
   RS_BLAS(cublasSetStream(blas, c.stream));
   RS_SOLVER(cusolverDnSetStream(sol, c.stream));
   RS_BLAS(cublasSetPointerMode(blas, CUBLAS_POINTER_MODE_HOST));
-  double nA = 0.0;
-  RS_BLAS(cublasDznrm2(blas, (int)std::min<int64_t>(m * n, INT32_MAX), reinterpret_cast<const cuDoubleComplex*>(A),
-                       1, &nA));
-  if (m * n > INT32_MAX) {
+  if (m * n > INT32_MAX) {  // cuBLAS / cuSOLVER 32-bit sizes
     hmx_set_error("rsvd: block of %lld entries too large", (long long)(m * n));
     return HMX_EINVAL;
   }
+  double nA = 0.0;
+  RS_BLAS(cublasDznrm2(blas, (int)(m * n), reinterpret_cast<const cuDoubleComplex*>(A), 1, &nA));
   if (nA == 0.0) return HMX_OK;  // zero block: rank 0
   Scratch s(c);
   double2 *Om, *B, *tau, *work;
