@@ -205,6 +205,54 @@ HMX_D void gram_columns(const double2* __restrict__ Ub, const double2* __restric
           }
         }
       }
+      constexpr int NV = 2 * kGramGroup * NC;  // doubles to sum over the warp
+      if constexpr (NV <= 32) {
+        // butterfly reduce-scatter (as mv_phase1): each xor stage halves the vector a lane carries,
+        // so NV values cost ~NV shuffles instead of 5 NV; lane (q << kFin) ends with value q =
+        // 2 (t NC + c) + {re, im}, and the even ones write their complex Gram entry
+        constexpr int P = NV <= 8 ? 8 : (NV <= 16 ? 16 : 32);
+        constexpr int kHalv = P == 8 ? 3 : (P == 16 ? 4 : 5);
+        constexpr int kFin = 5 - kHalv;
+        double v[P];
+#pragma unroll
+        for (int t = 0; t < kGramGroup; ++t)
+#pragma unroll
+          for (int c = 0; c < NC; ++c) {
+            v[2 * (t * NC + c)] = acc[t][c].x;
+            v[2 * (t * NC + c) + 1] = acc[t][c].y;
+          }
+#pragma unroll
+        for (int q = NV; q < P; ++q) v[q] = 0.0;
+#pragma unroll
+        for (int st = 0; st < kHalv; ++st) {
+          const int mask = 16 >> st, half = (P / 2) >> st;
+          const bool hi = (lane & mask) != 0;
+#pragma unroll
+          for (int i = 0; i < half; ++i) {
+            const double send = hi ? v[i] : v[i + half];
+            const double keep = hi ? v[i + half] : v[i];
+            v[i] = keep + __shfl_xor_sync(0xffffffffu, send, mask);
+          }
+        }
+#pragma unroll
+        for (int st = 0; st < kFin; ++st) v[0] += __shfl_xor_sync(0xffffffffu, v[0], 1 << st);
+        const double im = __shfl_down_sync(0xffffffffu, v[0], 1 << kFin);
+        const int q = lane >> kFin;
+        if ((lane & ((1 << kFin) - 1)) == 0 && (q & 1) == 0 && q < NV) {
+          const int t = (q >> 1) / NC, c = (q >> 1) % NC;
+          const int l = l0 + t, col = Kc + c;
+          const double2 val = cmk(v[0], im);
+          if (l < Kn) {
+            if (l < Kc || l < col) {
+              Gm[l + (int64_t)col * kcap] = val;
+              Gm[col + (int64_t)l * kcap] = cconj(val);
+            } else if (l == col) {
+              Gm[l + (int64_t)col * kcap] = cmk(val.x, 0.0);
+            }
+          }
+        }
+        continue;
+      }
 #pragma unroll
       for (int t = 0; t < kGramGroup; ++t)
 #pragma unroll
