@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define HMX_ABI_VERSION 2
+#define HMX_ABI_VERSION 3
 
 /* status codes */
 #define HMX_OK 0
@@ -39,6 +39,7 @@ extern "C" {
 #define HMX_EPIVOT 3    /* pivot exhaustion after the randomized-SVD fallback also failed (PivotExhaustionError) */
 #define HMX_ESINGULAR 4 /* r == 0 pair without a self rule (SingularEvaluationError)     */
 #define HMX_ENOMEM 5    /* device memory budget exceeded                               */
+#define HMX_EFACTOR 6   /* singular dense diagonal leaf in the H-LU (FactorizationError)  */
 
 /* kernel kinds (KernelSpec variant) */
 #define HMX_HELMHOLTZ 0 /* e^{i kappa r}/(4 pi r); kappa = 0 is Laplace, d = 1 */
@@ -227,6 +228,51 @@ int hmx_bench_read_bw(hmx_ctx* ctx, double* gbs);
 int hmx_gmres(hmx_hmatrix* h, const double* b, double* x, double tol, int32_t restart, int64_t max_iters,
               int32_t mem, int64_t* iters, double* history, int64_t history_cap, int64_t* history_len,
               int32_t* converged);
+
+/* ---- H-LU engine: formatted H-arithmetic, hlu, triangular solves ----------
+ * Replaces the reference's hmatx.hmatrix.formatted_addmul / hlu / triangular_solve and
+ * hmatx.solve.solve_direct (the module itself is absent from the mount,
+ * SURVEY 0.2).  An hmx_hlu is a device factor tree over a block tree (geometry.py:277-295): dense,
+ * low-rank (U V^H) and hierarchical nodes, every matrix complex128 column-major in HBM, driven from C++
+ * over cuBLAS / cuSOLVER and the assembly's truncation kernels.
+ *
+ * Tree descriptor: nnodes rows of 8 int64 in preorder (a hierarchical node's children follow it, grid
+ * row-major): kind (0 dense, 1 low-rank, 2 hierarchical, 3 low-rank from a dense block: truncated SVD
+ * with eps / rule), r0, r1, c0, c1 (dof ranges, tree order), nr, nc (grid of a hierarchical node),
+ * extra (dense: 1 = factored, the block is the packed LU of getrf with pivots; low-rank: rank).
+ * Payload: one row of 5 uint64 per leaf, preorder: dense (p0 = block, ld0 [, p4 = int64 pidx with
+ * P^T X = X[pidx] when factored]); low-rank (p0 = U, ld0, p1 = V, ld1); kind 3 (p0 = block, ld0).
+ * Device pointers; hmx_hlu_build copies them (the caller's buffers may be freed afterwards). */
+typedef struct hmx_hlu hmx_hlu;
+typedef struct {
+  int64_t n_truncations, n_truncate_calls, n_getrf, max_rank, dense_image_bytes, k_p50, k_p90, k_max;
+  double t_truncate_s, t_factor_s;
+} hmx_hlu_stats;
+int hmx_hlu_build(hmx_ctx* ctx, int64_t nnodes, const int64_t* desc, const uint64_t* payload, double eps,
+                  int32_t trunc_rule, int32_t finished, hmx_hlu** out);
+int hmx_hlu_count(const hmx_hlu* h, int64_t* nnodes, int64_t* nleaves);
+/* the same descriptor / payload format (payload pointers into the tree's own storage, valid until the
+ * tree is modified or freed) */
+int hmx_hlu_export(const hmx_hlu* h, int64_t* desc, uint64_t* payload);
+/* in-place recursive H-LU: LU(A11); U12 = L11^{-1} A12; L21 = A21 U11^{-1};
+ * A22 -= L21 U12 (formatted, truncation eps); recurse.  HMX_EFACTOR on a singular dense diagonal leaf. */
+int hmx_hlu_factor(hmx_hlu* h, double eps, int32_t trunc_rule, hmx_hlu_stats* st);
+/* mode 0: Y = U_H^{-1} L_H^{-1} X; mode 1: Y = L_H U_H X.  X, Y: device, n x nrhs
+ * column-major, tree order. */
+int hmx_hlu_apply(hmx_hlu* h, int32_t mode, const double* X, double* Y, int64_t n, int64_t nrhs);
+/* target <- target + alpha a b in the H-format of target, low-rank targets truncated with eps */
+int hmx_hlu_addmul(hmx_hlu* target, hmx_hlu* a, hmx_hlu* b, double alpha, double eps, int32_t trunc_rule);
+/* dense image (device, column-major, leading dimension ld) */
+int hmx_hlu_to_dense(hmx_hlu* h, double* out, int64_t ld);
+/* the engine's truncation of factor pairs (direct / dense-form / range-sketch / QR + SVD routes):
+ * U_i (dm_i x K_i), V_i (dn_i x K_i) column-major device -> r_i columns written into Uo_i / Vo_i
+ * (capacity K_i columns, ld = dm_i / dn_i). */
+int hmx_hlu_truncate(hmx_ctx* ctx, int64_t nb, const int64_t* dm, const int64_t* dn, const int64_t* K,
+                     const uint64_t* U, const uint64_t* V, const uint64_t* Uo, const uint64_t* Vo, double eps,
+                     int32_t trunc_rule, int64_t* ranks);
+/* trim the engine's memory pool */
+int hmx_hlu_release(hmx_ctx* ctx);
+void hmx_hlu_free(hmx_hlu* h);
 
 #ifdef __cplusplus
 }

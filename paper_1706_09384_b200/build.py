@@ -14,7 +14,7 @@ CSRC = os.path.join(HERE, "csrc")
 ROOT = os.path.dirname(HERE)
 OBJ = os.path.join(ROOT, "build", "obj")
 LIB = os.path.join(HERE, "libhmx.so")
-SOURCES = ["capi.cu", "aca.cu", "recompress.cu", "dense.cu", "matvec.cu", "gmres.cu", "estimate.cu", "rsvd.cu", "geometry.cpp"]
+SOURCES = ["capi.cu", "aca.cu", "recompress.cu", "dense.cu", "matvec.cu", "gmres.cu", "estimate.cu", "rsvd.cu", "hlu.cu", "geometry.cpp"]
 HEADERS = ["hmx_common.cuh", "green.cuh", "hmatrix.h", "hmx_host.h"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -37,9 +37,6 @@ void hmx_set_error(const char* fmt, ...) {
   g_last_error = buf;
 }
 
-struct hmx_ctx {
-  hmx::Ctx c;
-};
 
 namespace hmx {
 void release_cache(Ctx& c) {
@@ -342,6 +339,7 @@ int hmx_ctx_destroy(hmx_ctx* ctx) {
   if (ctx->c.aux) cudaStreamDestroy(ctx->c.aux);
   if (ctx->c.rerun) cudaStreamDestroy(ctx->c.rerun);
   if (ctx->c.pool) cudaMemPoolDestroy(ctx->c.pool);
+  hlu_pool_destroy(ctx->c);
   linalg_destroy(ctx->c);
   release_cache(ctx->c);
   delete ctx;
@@ -1866,32 +1864,26 @@ int hmx_rsvd(hmx_ctx* ctx, const double* A, int64_t m, int64_t n, double eps, in
   return HMX_OK;
 }
 
-int hmx_truncate_batch(hmx_ctx* ctx, int64_t nb, const int64_t* dm, const int64_t* dn, const int64_t* K,
-                       const uint64_t* U, const uint64_t* V, const uint64_t* Uo, const uint64_t* Vo, double eps,
-                       int32_t trunc_rule, int64_t* ranks, int32_t* flags) {
-  if (!ctx || nb < 0 || (nb > 0 && (!dm || !dn || !K || !U || !V || !Uo || !Vo || !ranks || !flags)))
-    return HMX_EINVAL;
-  if (nb == 0) return HMX_OK;
+}  // extern "C"
+
+namespace hmx {
+
+// Batched truncation core shared by hmx_truncate_batch and the H-LU engine (hlu.cu): Gram pairs,
+// recompression K classes, rank readback (one host synchronisation), then `outputs` supplies the
+// destination of every formed item (ranks / flags known) and U' = U W_U, V' = V W_V are launched.
+int truncate_pairs(Ctx& c, int64_t nb, const int64_t* dm, const int64_t* dn, const int64_t* K,
+                   const double2* const* U, const double2* const* V, double eps, int32_t trunc_rule, int64_t* ranks,
+                   int32_t* flags, const TruncOutputs& outputs) {
   for (int64_t i = 0; i < nb; ++i) {
-    if (dm[i] <= 0 || dn[i] <= 0 || K[i] < 0 || (K[i] > 0 && (!U[i] || !V[i] || !Uo[i] || !Vo[i]))) {
-      hmx_set_error("hmx_truncate_batch: item %lld has invalid sizes / pointers", (long long)i);
-      return HMX_EINVAL;
-    }
-    if (K[i] > 1020) {
-      hmx_set_error("hmx_truncate_batch: item %lld has %lld columns, above the device limit 1020", (long long)i,
-                    (long long)K[i]);
-      return HMX_EINVAL;
-    }
     ranks[i] = 0;
     flags[i] = 0;
   }
-  Ctx& c = ctx->c;
-  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  std::vector<double2*> uo((size_t)nb, nullptr), vo((size_t)nb, nullptr);
   // items with K > 0, largest K first (the recompression launches per K class)
   std::vector<int64_t> live;
   for (int64_t i = 0; i < nb; ++i)
     if (K[i] > 0) live.push_back(i);
-  if (live.empty()) return HMX_OK;
+  if (live.empty()) return outputs(ranks, flags, uo.data(), vo.data());
   std::stable_sort(live.begin(), live.end(), [&](int64_t a, int64_t b) { return K[a] > K[b]; });
   const int64_t nl = (int64_t)live.size();
   std::vector<RecDesc> rd((size_t)nl);
@@ -1915,7 +1907,7 @@ int hmx_truncate_batch(hmx_ctx* ctx, int64_t nb, const int64_t* dm, const int64_
     const int64_t i = live[q], k = K[i];
     for (int side = 0; side < 2; ++side) {
       GramItem& g = gi[2 * q + side];
-      g.F = reinterpret_cast<const double2*>(side == 0 ? U[i] : V[i]);
+      g.F = side == 0 ? U[i] : V[i];
       g.rows = side == 0 ? dm[i] : dn[i];
       g.K = (int32_t)k;
       g.pad = 0;
@@ -1924,17 +1916,24 @@ int hmx_truncate_batch(hmx_ctx* ctx, int64_t nb, const int64_t* dm, const int64_
       for (int t = 0; t < nt * nt; ++t) tiles.push_back(make_int2((int)(2 * q + side), t));
     }
   }
-  GramItem* d_gi;
-  int2* d_tiles;
-  RecDesc* d_rd;
-  int32_t *d_rank, *d_flag;
-  if ((rc = mem.alloc(&d_gi, 2 * nl)) || (rc = mem.alloc(&d_tiles, (int64_t)tiles.size())) ||
-      (rc = mem.alloc(&d_rd, nl)) || (rc = mem.alloc(&d_rank, nl)) || (rc = mem.alloc(&d_flag, nl)))
-    return rc;
-  HMX_CUDA_TRY(cudaMemcpyAsync(d_gi, gi.data(), sizeof(GramItem) * gi.size(), cudaMemcpyHostToDevice, c.stream));
-  HMX_CUDA_TRY(
-      cudaMemcpyAsync(d_tiles, tiles.data(), sizeof(int2) * tiles.size(), cudaMemcpyHostToDevice, c.stream));
-  HMX_CUDA_TRY(cudaMemcpyAsync(d_rd, rd.data(), sizeof(RecDesc) * rd.size(), cudaMemcpyHostToDevice, c.stream));
+  // descriptors in one upload: [Gram items | recompression descriptors | tiles | rank | flag]
+  const size_t b_gi = sizeof(GramItem) * gi.size(), b_rd = sizeof(RecDesc) * rd.size();
+  const size_t o_rd = (b_gi + 15) / 16 * 16, o_tl = o_rd + (b_rd + 15) / 16 * 16;
+  const size_t o_rk = o_tl + (sizeof(int2) * tiles.size() + 15) / 16 * 16;
+  const size_t o_fl = o_rk + (sizeof(int32_t) * nl + 15) / 16 * 16;
+  const size_t total = o_fl + sizeof(int32_t) * nl;
+  std::vector<unsigned char> host(o_rk);
+  memcpy(host.data(), gi.data(), b_gi);
+  memcpy(host.data() + o_rd, rd.data(), b_rd);
+  memcpy(host.data() + o_tl, tiles.data(), sizeof(int2) * tiles.size());
+  unsigned char* d_blob;
+  if ((rc = mem.alloc(&d_blob, (int64_t)total))) return rc;
+  HMX_CUDA_TRY(cudaMemcpyAsync(d_blob, host.data(), o_rk, cudaMemcpyHostToDevice, c.stream));
+  const GramItem* d_gi = reinterpret_cast<const GramItem*>(d_blob);
+  const RecDesc* d_rd = reinterpret_cast<const RecDesc*>(d_blob + o_rd);
+  const int2* d_tiles = reinterpret_cast<const int2*>(d_blob + o_tl);
+  int32_t* d_rank = reinterpret_cast<int32_t*>(d_blob + o_rk);
+  int32_t* d_flag = reinterpret_cast<int32_t*>(d_blob + o_fl);
   gram_batch<<<(unsigned)tiles.size(), 256, 0, c.stream>>>(d_gi, d_tiles);
   HMX_CUDA_TRY(cudaGetLastError());
   // K classes: > 112 (global-memory variant), 61..112, <= 60 (shared-memory variants, more CTAs per SM)
@@ -1948,25 +1947,29 @@ int hmx_truncate_batch(hmx_ctx* ctx, int64_t nb, const int64_t* dm, const int64_
       return rc;
     q0 = q1;
   }
-  std::vector<int32_t> hr((size_t)nl), hf((size_t)nl);
-  HMX_CUDA_TRY(cudaMemcpyAsync(hr.data(), d_rank, sizeof(int32_t) * nl, cudaMemcpyDeviceToHost, c.stream));
-  HMX_CUDA_TRY(cudaMemcpyAsync(hf.data(), d_flag, sizeof(int32_t) * nl, cudaMemcpyDeviceToHost, c.stream));
+  std::vector<int32_t> hrf((size_t)(o_fl - o_rk) / 4 + (size_t)nl);
+  HMX_CUDA_TRY(cudaMemcpyAsync(hrf.data(), d_rank, total - o_rk, cudaMemcpyDeviceToHost, c.stream));
   HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+  const int32_t* hr = hrf.data();
+  const int32_t* hf = hrf.data() + (o_fl - o_rk) / 4;
+  for (int64_t q = 0; q < nl; ++q) {
+    ranks[live[q]] = hr[q];
+    flags[live[q]] = hf[q];
+  }
+  if ((rc = outputs(ranks, flags, uo.data(), vo.data()))) return rc;
   std::vector<FormDesc> fd;
   std::vector<int64_t> ts;
   int64_t ntiles = 0;
   for (int64_t q = 0; q < nl; ++q) {
     const int64_t i = live[q], k = K[i];
     const int r = hr[q];
-    ranks[i] = r;
-    flags[i] = hf[q];
     if (r <= 0 || (hf[q] & 1)) continue;  // a regularised (rank-deficient V) item is not formed
     for (int side = 0; side < 2; ++side) {
       FormDesc f;
       const int64_t rows = side == 0 ? dm[i] : dn[i];
-      f.A = reinterpret_cast<const double2*>(side == 0 ? U[i] : V[i]);
+      f.A = side == 0 ? U[i] : V[i];
       f.W = W + rd[q].woff + 4 * k * k + (side == 0 ? 0 : k * r);
-      f.C = reinterpret_cast<double2*>(side == 0 ? Uo[i] : Vo[i]);
+      f.C = side == 0 ? uo[i] : vo[i];
       f.rows = (int32_t)rows;
       f.K = (int32_t)k;
       f.r = r;
@@ -1979,14 +1982,52 @@ int hmx_truncate_batch(hmx_ctx* ctx, int64_t nb, const int64_t* dm, const int64_
     }
   }
   if (!fd.empty()) {
-    FormDesc* d_fd;
-    int64_t* d_ts;
-    if ((rc = mem.alloc(&d_fd, (int64_t)fd.size())) || (rc = mem.alloc(&d_ts, (int64_t)ts.size()))) return rc;
-    HMX_CUDA_TRY(cudaMemcpyAsync(d_fd, fd.data(), sizeof(FormDesc) * fd.size(), cudaMemcpyHostToDevice, c.stream));
-    HMX_CUDA_TRY(cudaMemcpyAsync(d_ts, ts.data(), sizeof(int64_t) * ts.size(), cudaMemcpyHostToDevice, c.stream));
-    if ((rc = launch_form(c, d_fd, (int64_t)fd.size(), ntiles, d_ts))) return rc;
+    const size_t b_fd = (sizeof(FormDesc) * fd.size() + 15) / 16 * 16;
+    std::vector<unsigned char> hb(b_fd + sizeof(int64_t) * ts.size());
+    memcpy(hb.data(), fd.data(), sizeof(FormDesc) * fd.size());
+    memcpy(hb.data() + b_fd, ts.data(), sizeof(int64_t) * ts.size());
+    unsigned char* d_f;
+    if ((rc = mem.alloc(&d_f, (int64_t)hb.size()))) return rc;
+    HMX_CUDA_TRY(cudaMemcpyAsync(d_f, hb.data(), hb.size(), cudaMemcpyHostToDevice, c.stream));
+    if ((rc = launch_form(c, reinterpret_cast<const FormDesc*>(d_f), (int64_t)fd.size(), ntiles,
+                          reinterpret_cast<const int64_t*>(d_f + b_fd))))
+      return rc;
   }
   return HMX_OK;
+}
+
+}  // namespace hmx
+
+extern "C" {
+
+int hmx_truncate_batch(hmx_ctx* ctx, int64_t nb, const int64_t* dm, const int64_t* dn, const int64_t* K,
+                       const uint64_t* U, const uint64_t* V, const uint64_t* Uo, const uint64_t* Vo, double eps,
+                       int32_t trunc_rule, int64_t* ranks, int32_t* flags) {
+  if (!ctx || nb < 0 || (nb > 0 && (!dm || !dn || !K || !U || !V || !Uo || !Vo || !ranks || !flags)))
+    return HMX_EINVAL;
+  if (nb == 0) return HMX_OK;
+  for (int64_t i = 0; i < nb; ++i) {
+    if (dm[i] <= 0 || dn[i] <= 0 || K[i] < 0 || (K[i] > 0 && (!U[i] || !V[i] || !Uo[i] || !Vo[i]))) {
+      hmx_set_error("hmx_truncate_batch: item %lld has invalid sizes / pointers", (long long)i);
+      return HMX_EINVAL;
+    }
+    if (K[i] > 1020) {
+      hmx_set_error("hmx_truncate_batch: item %lld has %lld columns, above the device limit 1020", (long long)i,
+                    (long long)K[i]);
+      return HMX_EINVAL;
+    }
+  }
+  Ctx& c = ctx->c;
+  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  return truncate_pairs(c, nb, dm, dn, K, reinterpret_cast<const double2* const*>(U),
+                        reinterpret_cast<const double2* const*>(V), eps, trunc_rule, ranks, flags,
+                        [&](const int64_t*, const int32_t*, double2** uo, double2** vo) {
+                          for (int64_t i = 0; i < nb; ++i) {
+                            uo[i] = reinterpret_cast<double2*>(Uo[i]);
+                            vo[i] = reinterpret_cast<double2*>(Vo[i]);
+                          }
+                          return HMX_OK;
+                        });
 }
 
 }  // extern "C"

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <functional>
 #include <map>
 #include <memory>
 #include <mutex>
@@ -42,6 +43,7 @@ struct Ctx {
   size_t cached_bytes = 0;
   void* blas = nullptr;    // cublasHandle_t of the randomized-SVD fallback (rsvd.cu), lazy
   void* solver = nullptr;  // cusolverDnHandle_t, lazy
+  cudaMemPool_t lu_pool = nullptr;  // stream-ordered pool of the H-LU engine (hlu.cu), lazy
 };
 
 // phase-1 job: one warp computes s[soff] = V[voff : voff+len]^H x_tree[xoff : xoff+len]
@@ -125,6 +127,7 @@ struct DeviceH {
 
 // capi.cu: stream-ordered device memory from the context pool (no device-wide
 // synchronisation, memory reused across assemblies instead of re-mapped)
+void release_cache(Ctx& c);
 cudaError_t dev_alloc(Ctx& c, void** p, size_t bytes);
 void dev_free(Ctx& c, void* p);
 template <class T>
@@ -255,6 +258,19 @@ int bench_read_bw(Ctx& c, double* gbs);
 int rsvd_dense(Ctx& c, const double2* A, int64_t m, int64_t n, double eps, int oversample, int64_t cap, uint64_t seed,
                double2* U, double2* V, double2* G, int* K_out, int* converged);
 int linalg_handles(Ctx& c, void** blas, void** solver);
+// counter-based complex Gaussian fill (g1 + i g2, g ~ N(0, 1)) of `count` entries with `key`
+int launch_gaussian(Ctx& c, double2* out, int64_t count, uint64_t key);
+
+// capi.cu: batched truncation of factor pairs (hmx_truncate_batch and the H-LU engine).  Items:
+// U_i (dm_i x K_i), V_i (dn_i x K_i) column-major with ld = rows, K_i <= 1020.  After the rank
+// readback `outputs(ranks, flags, Uo, Vo)` fills the destinations (ld = rows, >= r_i columns) of
+// every item with r_i > 0 and flags_i bit 0 clear; the U' / V' products are then launched on
+// c.stream (not waited for).
+using TruncOutputs = std::function<int(const int64_t* ranks, const int32_t* flags, double2** Uo, double2** Vo)>;
+int truncate_pairs(Ctx& c, int64_t nb, const int64_t* dm, const int64_t* dn, const int64_t* K,
+                   const double2* const* U, const double2* const* V, double eps, int32_t trunc_rule, int64_t* ranks,
+                   int32_t* flags, const TruncOutputs& outputs);
+void hlu_pool_destroy(Ctx& c);
 void linalg_destroy(Ctx& c);
 
 // gmres.cu
@@ -262,3 +278,7 @@ int gmres_device(DeviceH& H, const double2* b_dev, double2* x_dev, double tol, i
                  int64_t* iters, std::vector<double>& history, int* converged, cudaStream_t s);
 
 }  // namespace hmx
+
+struct hmx_ctx {
+  hmx::Ctx c;
+};

@@ -113,6 +113,14 @@ int linalg_handles(Ctx& c, void** blas, void** solver) {
   return HMX_OK;
 }
 
+int launch_gaussian(Ctx& c, double2* out, int64_t count, uint64_t key) {
+  if (count <= 0) return HMX_OK;
+  gaussian_fill<<<(unsigned)std::min<int64_t>(hmx_cdiv(count, 256), 4 * c.num_sms), 256, 0, c.stream>>>(out, count,
+                                                                                                       key);
+  HMX_CUDA_TRY(cudaGetLastError());
+  return HMX_OK;
+}
+
 void linalg_destroy(Ctx& c) {
   if (c.blas) cublasDestroy(static_cast<cublasHandle_t>(c.blas));
   if (c.solver) cusolverDnDestroy(static_cast<cusolverDnHandle_t>(c.solver));
