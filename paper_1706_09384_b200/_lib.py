@@ -43,6 +43,14 @@ class HmxStats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class HmxHluStats(C.Structure):
+    _fields_ = [(n, i64) for n in ("n_truncations", "n_truncate_calls", "n_getrf", "max_rank", "dense_image_bytes",
+                                   "k_p50", "k_p90", "k_max")] + [(n, f64) for n in ("t_truncate_s", "t_factor_s")]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 # name -> (restype, argtypes); every symbol include/hmx.h declares
 SIGNATURES = {
     "hmx_abi_version": (C.c_int, []),
@@ -86,6 +94,16 @@ SIGNATURES = {
     "hmx_bench_read_bw": (C.c_int, [P, C.POINTER(f64)]),
     "hmx_gmres": (C.c_int, [P, P, P, f64, i32, i64, i32, C.POINTER(i64), P, i64,
                             C.POINTER(i64), C.POINTER(i32)]),
+    "hmx_hlu_build": (C.c_int, [P, i64, P, P, f64, i32, i32, C.POINTER(P)]),
+    "hmx_hlu_count": (C.c_int, [P, C.POINTER(i64), C.POINTER(i64)]),
+    "hmx_hlu_export": (C.c_int, [P, P, P]),
+    "hmx_hlu_factor": (C.c_int, [P, f64, i32, C.POINTER(HmxHluStats)]),
+    "hmx_hlu_apply": (C.c_int, [P, i32, P, P, i64, i64]),
+    "hmx_hlu_addmul": (C.c_int, [P, P, P, f64, f64, i32]),
+    "hmx_hlu_to_dense": (C.c_int, [P, P, i64]),
+    "hmx_hlu_truncate": (C.c_int, [P, i64, P, P, P, P, P, P, P, f64, i32, P]),
+    "hmx_hlu_release": (C.c_int, [P]),
+    "hmx_hlu_free": (None, [P]),
 }
 
 _lib = None

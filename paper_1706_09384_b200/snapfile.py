@@ -190,7 +190,7 @@ def _lu_struct(x, leaves):
         return {"S": box, "rs": x.rs, "cs": x.cs, "ch": [[_lu_struct(c, leaves) for c in row] for row in x.ch]}
     leaves.append(x)
     if isinstance(x, HL.Dense):
-        return {"D": box, "f": int(x.L is not None)}
+        return {"D": box, "f": int(x.factored)}
     return {"R": box, "k": x.rank}
 
 
@@ -211,10 +211,10 @@ def save_lu(f, path):
         w.write(perm.tobytes())
         for x in leaves:
             if isinstance(x, HL.Dense):
-                mats = [x.L, x.U] if x.L is not None else [x.a]
+                mats = [x.L, x.U] if x.factored else [x.a]
                 for m in mats:
                     w.write(np.ascontiguousarray(m.cpu().numpy()).tobytes())
-                if x.L is not None:
+                if x.factored:
                     w.write(np.ascontiguousarray(x.pidx.cpu().numpy().astype(np.int64)).tobytes())
             else:
                 w.write(np.ascontiguousarray(x.u.cpu().numpy()).tobytes())
@@ -240,19 +240,14 @@ def _load_lu(header, buf, nbody, device):
     def rec(js):
         if "S" in js:
             r0, r1, c0, c1 = js["S"]
-            x = HL.Sub(r0, r1, c0, c1, [tuple(q) for q in js["rs"]], [tuple(q) for q in js["cs"]],
-                       [[rec(c) for c in row] for row in js["ch"]])
-            x.fin = True
-            return x
+            return HL.Sub(r0, r1, c0, c1, [tuple(q) for q in js["rs"]], [tuple(q) for q in js["cs"]],
+                          [[rec(c) for c in row] for row in js["ch"]])
         if "D" in js:
             r0, r1, c0, c1 = js["D"]
             m, n = r1 - r0, c1 - c0
             if js["f"]:
-                x = HL.Dense(r0, r1, c0, c1, None)
-                x.L, x.U = arr((m, m)), arr((m, m))
-                x.pidx = arr((m,), np.int64)
-                x.pinv = torch.argsort(x.pidx)
-                return x
+                lo, up = arr((m, m)), arr((m, m))
+                return HL.Dense(r0, r1, c0, c1, torch.tril(lo, -1) + up, True, arr((m,), np.int64))
             return HL.Dense(r0, r1, c0, c1, arr((m, n)))
         r0, r1, c0, c1 = js["R"]
         k = js["k"]
@@ -261,8 +256,8 @@ def _load_lu(header, buf, nbody, device):
     root = rec(header["tree"])
     if buf.tell() != nbody:
         raise SnapshotCorruptError("snapshot payload size mismatch")
-    return HL.LUFactors(lower=HL._Tri(root, True), upper=HL._Tri(root, False), eps_lu=header["eps_lu"],
-                        d=header["d"], perm=perm, n=header["n"])
+    tree = HL.HTree.from_nodes(root, device)   # the engine copies the leaves into its own pool
+    return HL._factors(tree, header["eps_lu"], header["d"], perm, header["n"])
 
 
 def snapshot(op, path, h=None, device=0):

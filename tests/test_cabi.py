@@ -25,7 +25,7 @@ def test_every_declared_symbol_is_exported_and_bound():
     for name in decl:
         assert hasattr(L, name), name
         assert name in _lib.SIGNATURES, f"{name} not bound in _lib.SIGNATURES"
-    assert L.hmx_abi_version() == 2
+    assert L.hmx_abi_version() == 3
 
 
 def test_host_error_paths():

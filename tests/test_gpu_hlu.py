@@ -121,23 +121,23 @@ def test_addmul_all_dense_exact():
     t = HL.from_dense(bt, 1, C, 0.0)
     HL.formatted_addmul(t, HL.from_dense(bt, 1, A, 0.0), HL.from_dense(bt, 1, B, 0.0), 1e-4)
     ref = C + A @ B
-    assert np.linalg.norm(t.a.cpu().numpy() - ref) <= 1e-14 * np.linalg.norm(ref)
+    assert isinstance(t.nodes(), HL.Dense)
+    assert np.linalg.norm(HL.to_dense(t).cpu().numpy() - ref) <= 1e-14 * np.linalg.norm(ref)
 
 
 def test_identity_and_singular():
     pb = Problem("H4k", 300)
     I = np.eye(300, dtype=complex)
-    f = HL.LUFactors  # noqa: F841
     root = HL.from_dense(pb.bt, 1, I, 1e-8)
-    ar = HL.Arith(1e-4)
-    HL._lu(ar, root, ())
+    root.factor(1e-4)
     b = torch.as_tensor(_rand(300, 7), device="cuda")[:, None]
-    x = HL._usolve(ar, root, HL._lsolve(ar, root, b))
+    x = root.apply(b, 0)
     assert torch.allclose(x, b, rtol=0, atol=1e-13)
+    assert torch.allclose(root.apply(b, 1), b, rtol=0, atol=1e-13)
     I[5, 5] = 0.0
     root = HL.from_dense(pb.bt, 1, I, 1e-8)
     with pytest.raises(hmx.FactorizationError, match="block path"):
-        HL._lu(HL.Arith(1e-4), root, ())
+        root.factor(1e-4)
 
 
 def test_source_h_unchanged():
@@ -195,7 +195,7 @@ def test_lu_snapshot_round_trip(tmp_path):
     for x, y in zip(HL._walk(f.root), HL._walk(g.root)):
         assert type(x) is type(y) and (x.r0, x.r1, x.c0, x.c1) == (y.r0, y.r1, y.c0, y.c1)
         pairs = ([(x.u, y.u), (x.v, y.v)] if isinstance(x, HL.LowRank) else
-                 [(x.L, y.L), (x.U, y.U), (x.pidx, y.pidx)] if x.L is not None else [(x.a, y.a)])
+                 [(x.L, y.L), (x.U, y.U), (x.pidx, y.pidx)] if x.factored else [(x.a, y.a)])
         for p_, q_ in pairs:
             assert torch.equal(p_, q_)
     b = pb.rhs(9)

@@ -1,4 +1,4 @@
-"""hmx_truncate_batch (the H-arithmetic truncation kernel) against numpy's SVD truncation
+"""hmx_hlu_truncate (the H-arithmetic truncation of the H-LU engine: direct / dense-form / range-sketch routes) against numpy's SVD truncation
 on random factor pairs: full-rank, numerically low-rank with dependent columns, K above
 the row count, single columns; Frobenius and spectral rules."""
 
@@ -36,8 +36,7 @@ def test_truncate_batch_matches_svd(rule):
         items.append((torch.as_tensor(U, device="cuda"), torch.as_tensor(V, device="cuda")))
         ref.append(U @ V.conj().T)
     eps = 1e-6
-    ar = HL.Arith(eps, rule)
-    out = HL._truncate_batch(ar, items)
+    out = HL.truncate_pairs(items, eps, rule)
     for (u, v), A, (dm, dn, K, _, _) in zip(out, ref, cases):
         s = np.linalg.svd(A, compute_uv=False)
         r_ref = truncation_rank(s, eps, rule)
@@ -62,8 +61,7 @@ def test_sketched_dense_form():
         V = rng.standard_normal((dn, K)) + 1j * rng.standard_normal((dn, K))
         items.append((torch.as_tensor(U, device="cuda"), torch.as_tensor(V, device="cuda")))
         ref.append(U @ V.conj().T)
-    ar = HL.Arith(eps)
-    out = HL._truncate_batch(ar, items)
+    out = HL.truncate_pairs(items, eps)
     for (u, v), A, c in zip(out, ref, cases):
         sv = np.linalg.svd(A, compute_uv=False)
         r_ref = truncation_rank(sv, eps, "frobenius")
