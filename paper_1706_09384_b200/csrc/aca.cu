@@ -679,6 +679,12 @@ constexpr int kTcCol = kTcRows + 4, kTcStage = 8 * kTcCol;  // double2 units; ri
 // warp for 8 = streaming loop, 9 = epilogue), read by hmx_debug_tc_prof.
 #ifdef HMX_TC_PROF
 __device__ unsigned long long g_tc_prof[16];
+__device__ unsigned long long g_tc_cta[4 * 8192];  // per launched CTA: globaltimer start, end, SM id, (m + n) << 32 | K
+HMX_D unsigned long long tc_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
 #define TC_MARK(i)                                                                   \
   do {                                                                               \
     if (threadIdx.x == 0) {                                                          \
@@ -751,7 +757,7 @@ HMX_D void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::
 // Fused pass over panel F (rows = 3 npts, ld = rows, K columns) for the row
 // blocks of this warp.  Each column octet of a row block is brought into the
 // warp's shared-memory ring by eight bulk copies (one 48-row column run each,
-// issued by lanes 0-7 on the stage's mbarrier) kTcStages - 1 octets ahead, then
+// issued by one elected lane on the stage's mbarrier) kTcStages - 1 octets ahead, then
 // feeds both contractions from shared memory.  Residual fragments of each row
 // block are left in resb (aliases the ring: kTcRows x 12 doubles, C1 n = 0..5
 // then C2 n = 0..5) and `epi(rb_row0)` is called by the whole warp; with pend,
@@ -761,11 +767,19 @@ HMX_D void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::
 // ring stage (bit s), carried across passes.  Rows past the panel's end (last
 // row block) are zeroed in shared memory after the copy lands (the bulk copy
 // writes only the valid rows, so the two proxies never touch the same bytes).
+HMX_D bool elect_one() {
+  unsigned pred;
+  asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}\n" : "=r"(pred));
+  return pred != 0;
+}
+
 template <int kTcStages, class Epi>
 HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const double2* piv, int lds, bool pend,
                    int Pc, double* __restrict__ scr, int noct, double2* ring, double2* nfs, unsigned bar_sa,
                    unsigned& phase, Epi&& epi) {
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  // the warp index through a shuffle: the compiler then keeps everything derived from it (row
+  // block, copy addresses) in uniform registers
+  const int lane = threadIdx.x & 31, warp = __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0);
   const int fr = lane >> 2, fk = lane & 3;
   double* resb = reinterpret_cast<double*>(ring);
   constexpr unsigned kStageBytes = sizeof(double2) * kTcStage;
@@ -787,14 +801,24 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
       const int clim = min(8, K - co * 8);  // columns of this octet inside the panel
       const unsigned mb = bar_sa + 8u * (unsigned)buf;
       const bool with_pend = pend && co == 0;
-      if (lane == 0) mbar_expect_tx(mb, run * (unsigned)(clim + (with_pend ? 3 : 0)));
-      __syncwarp();
-      if (lane < clim)
-        bulk_g2s(ring_sa + (unsigned)buf * kStageBytes + (unsigned)(lane * kTcCol) * (unsigned)sizeof(double2),
-                 Fr + (int64_t)(co * 8 + lane) * rows, run, mb);
-      else if (with_pend && lane >= 8 && lane < 11)
-        bulk_g2s(nfs_sa + (unsigned)((lane - 8) * kTcRows) * (unsigned)sizeof(double2),
-                 Fr + (int64_t)(Pc + lane - 8) * rows, run, mb);
+      // one elected lane issues the octet's copies from warp-uniform operands (uniform datapath:
+      // no per-lane address broadcast), the pending columns riding on the first octet's barrier
+      if (elect_one()) {
+        mbar_expect_tx(mb, run * (unsigned)(clim + (with_pend ? 3 : 0)));
+        const double2* src = Fr + (int64_t)(co * 8) * rows;
+        unsigned dst = ring_sa + (unsigned)buf * kStageBytes;
+        for (int c = 0; c < clim; ++c) {
+          bulk_g2s(dst, src, run, mb);
+          src += rows;
+          dst += (unsigned)kTcCol * (unsigned)sizeof(double2);
+        }
+        if (with_pend) {
+          const double2* ps = Fr + (int64_t)Pc * rows;
+#pragma unroll
+          for (int c = 0; c < 3; ++c)
+            bulk_g2s(nfs_sa + (unsigned)(c * kTcRows) * (unsigned)sizeof(double2), ps + (int64_t)c * rows, run, mb);
+        }
+      }
     };
     auto wait = [&](int buf) {
       mbar_wait(bar_sa + 8u * (unsigned)buf, (phase >> buf) & 1u);
@@ -892,9 +916,9 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
         d[2] = (h4[0][0] + h4[1][0]) + (h4[2][0] + h4[3][0]);
         d[3] = (h4[0][1] + h4[1][1]) + (h4[2][1] + h4[3][1]);
       }
-      // this buffer is refilled by the next iteration's prefetch (async proxy): order
-      // this iteration's generic shared-memory accesses before it
-      fence_async_smem();
+      // this buffer is refilled by the next iteration's prefetch: every lane's reads of it have
+      // been consumed by the MMAs above, and the warp barrier orders them before the elected
+      // lane's copy (reads followed by an async-proxy write need no proxy fence)
       __syncwarp();
     }
     // residual fragments -> shared memory (rows of this block; the ring is idle now)
@@ -1006,6 +1030,12 @@ __global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
   int status = 0;
 #ifdef HMX_TC_PROF
   long long tc_t0 = clock64();
+  if (tid == 0 && blockIdx.x < 8192) {
+    unsigned smid;
+    asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+    g_tc_cta[4 * blockIdx.x] = tc_gtime();
+    g_tc_cta[4 * blockIdx.x + 2] = smid;
+  }
 #endif
 
   for (;;) {
@@ -1235,6 +1265,12 @@ __global__ void __launch_bounds__(kTcThreads, HMX_TC_MINB)
   }
   __syncthreads();
   TC_MARK(5);
+#ifdef HMX_TC_PROF
+  if (tid == 0 && blockIdx.x < 8192) {
+    g_tc_cta[4 * blockIdx.x + 1] = tc_gtime();
+    g_tc_cta[4 * blockIdx.x + 3] = ((unsigned long long)(m + n) << 32) | (unsigned)sh.K;
+  }
+#endif
   if (tid == 0) {
     AcaOut o;
     o.steps = sh.steps;
@@ -1334,5 +1370,8 @@ extern "C" int hmx_debug_tc_prof(unsigned long long* out) {
   unsigned long long z[16] = {};
   cudaMemcpyToSymbol(hmx::g_tc_prof, z, sizeof(z));
   return 0;
+}
+extern "C" int hmx_debug_tc_cta(unsigned long long* out) {
+  return cudaMemcpyFromSymbol(out, hmx::g_tc_cta, sizeof(hmx::g_tc_cta)) != cudaSuccess ? 2 : 0;
 }
 #endif
