@@ -838,11 +838,12 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
     for (int q = 0; q < kTcPf; ++q) {
       nx[q][0] = nx[q][1] = nx[q][2] = nx[q][3] = 0.0;
       if (pend && !first && q < noct) {
-        const double* dq = scr + ((int64_t)q * 32 + lane) * 4;
-        nx[q][0] = dq[0];
-        nx[q][1] = dq[1];
-        nx[q][2] = dq[2];
-        nx[q][3] = dq[3];
+        const double2* dq = reinterpret_cast<const double2*>(scr + ((int64_t)q * 32 + lane) * 4);
+        const double2 q0 = dq[0], q1 = dq[1];
+        nx[q][0] = q0.x;
+        nx[q][1] = q0.y;
+        nx[q][2] = q1.x;
+        nx[q][3] = q1.y;
       }
     }
     for (int co = 0; co < noct; ++co) {
@@ -854,11 +855,12 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
 #pragma unroll
         for (int t = 0; t < 4; ++t) nx[q][t] = nx[q + 1][t];
       if (pend && !first && co + kTcPf < noct) {
-        const double* dn = d + 128 * kTcPf;
-        nx[kTcPf - 1][0] = dn[0];
-        nx[kTcPf - 1][1] = dn[1];
-        nx[kTcPf - 1][2] = dn[2];
-        nx[kTcPf - 1][3] = dn[3];
+        const double2* dn = reinterpret_cast<const double2*>(d + 128 * kTcPf);
+        const double2 q0 = dn[0], q1 = dn[1];
+        nx[kTcPf - 1][0] = q0.x;
+        nx[kTcPf - 1][1] = q0.y;
+        nx[kTcPf - 1][2] = q1.x;
+        nx[kTcPf - 1][3] = q1.y;
       }
       const int buf = co % kTcStages;
       wait(buf);
@@ -896,25 +898,19 @@ HMX_D void tc_pass(const double2* __restrict__ F, int64_t rows, int K, const dou
         }
       }
       if (pend) {
-        // A' = F^T: m = column l0 + fr, k = row r0 + 4 j + fk; 4 independent
-        // accumulator chains per product (a single chain serialises on the MMA latency)
-        double h3[4][2], h4[4][2];
-#pragma unroll
-        for (int cidx = 0; cidx < 4; ++cidx) h3[cidx][0] = h3[cidx][1] = h4[cidx][0] = h4[cidx][1] = 0.0;
-        h3[0][0] = g3[0];
-        h3[0][1] = g3[1];
-        h4[0][0] = g4[0];
-        h4[0][1] = g4[1];
+        // A' = F^T: m = column l0 + fr, k = row r0 + 4 j + fk.  One accumulator per product,
+        // started from the earlier row blocks' partial: the re / im MMAs alternate, so each
+        // chain's next MMA issues two issue slots (32 cycles) after its predecessor, beyond
+        // the MMA latency (more chains only cost registers and adds: measured slower)
+        double h3[2] = {g3[0], g3[1]}, h4[2] = {g4[0], g4[1]};
 #pragma unroll
         for (int j = 0; j < kTcKs; ++j) {
           const double2 a = T[fr * kTcCol + 4 * j + fk];
-          dmma(h3[j % 4][0], h3[j % 4][1], a.x, bj[j]);
-          dmma(h4[j % 4][0], h4[j % 4][1], a.y, bj[j]);
+          dmma(h3[0], h3[1], a.x, bj[j]);
+          dmma(h4[0], h4[1], a.y, bj[j]);
         }
-        d[0] = (h3[0][0] + h3[1][0]) + (h3[2][0] + h3[3][0]);
-        d[1] = (h3[0][1] + h3[1][1]) + (h3[2][1] + h3[3][1]);
-        d[2] = (h4[0][0] + h4[1][0]) + (h4[2][0] + h4[3][0]);
-        d[3] = (h4[0][1] + h4[1][1]) + (h4[2][1] + h4[3][1]);
+        reinterpret_cast<double2*>(d)[0] = cmk(h3[0], h3[1]);
+        reinterpret_cast<double2*>(d)[1] = cmk(h4[0], h4[1]);
       }
       // this buffer is refilled by the next iteration's prefetch: every lane's reads of it have
       // been consumed by the MMAs above, and the warp barrier orders them before the elected

@@ -835,8 +835,23 @@ HMX_D void recompress_truncate(const double* lam, const int* ordr, int K, double
 // MODE 0: E, Z, R, T in L2 (large K); 1: E / Z in shared memory; 2: E / Z, R and
 // T / L_r all in shared memory (small K: the O(K) sequential phases then run
 // at shared-memory instead of L2 latency)
+#ifndef HMX_RC_M0_REGS
+#define HMX_RC_M0_REGS 128
+#endif
+#ifndef HMX_RC_M1W_REGS
+#define HMX_RC_M1W_REGS 128
+#endif
+// register caps per instantiation (what bounds the CTAs per SM next to the shared memory):
+// 64 for the small shared-memory classes (8 x 128-thread CTAs per SM)
+constexpr int rc_maxnreg(int mode, int nt) {
+  return (mode == 1 && nt == 128) ? 65536 / (128 * HMX_RC_MINB)
+         : (mode == 1 && nt == 64) ? 64
+         : (mode == 0 && nt == 512) ? HMX_RC_M0_REGS
+         : (mode == 1 && nt == 256) ? HMX_RC_M1W_REGS
+                                    : (65536 / nt > 255 ? 255 : 65536 / nt);
+}
 template <int MODE, int NT>
-__global__ void __launch_bounds__(NT, (NT == 128 && MODE == 1) ? HMX_RC_MINB : (NT == 64 && MODE == 1 ? 16 : 1)) recompress_core(const RecDesc* __restrict__ desc, double eps, int rule,
+__global__ void __launch_bounds__(NT) __maxnreg__(rc_maxnreg(MODE, NT)) recompress_core(const RecDesc* __restrict__ desc, double eps, int rule,
                                                             const double2* __restrict__ G, double2* __restrict__ W,
                                                             int32_t* __restrict__ rank_out,
                                                             int32_t* __restrict__ flags_out) {
