@@ -291,6 +291,7 @@ int hmx_ctx_create(int32_t device, hmx_ctx** out) {
   HMX_CUDA_TRY(cudaStreamCreateWithFlags(&c->c.stream, cudaStreamNonBlocking));
   c->c.own_stream = true;
   HMX_CUDA_TRY(cudaStreamCreateWithFlags(&c->c.aux, cudaStreamNonBlocking));
+  HMX_CUDA_TRY(cudaStreamCreateWithFlags(&c->c.side, cudaStreamNonBlocking));
   {
     int lo = 0, hi = 0;  // hi = greatest priority (numerically lowest)
     HMX_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&lo, &hi));
@@ -338,6 +339,7 @@ int hmx_ctx_destroy(hmx_ctx* ctx) {
   if (ctx->c.own_stream && ctx->c.stream) cudaStreamDestroy(ctx->c.stream);
   if (ctx->c.aux) cudaStreamDestroy(ctx->c.aux);
   if (ctx->c.rerun) cudaStreamDestroy(ctx->c.rerun);
+  if (ctx->c.side) cudaStreamDestroy(ctx->c.side);
   if (ctx->c.pool) cudaMemPoolDestroy(ctx->c.pool);
   hlu_pool_destroy(ctx->c);
   linalg_destroy(ctx->c);
@@ -699,18 +701,40 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     // shared-memory size classes (smem ~ 16 K^2 bytes): more CTAs per SM for small K
     const int classes[] = {kMaxAcaCols, kRecompressSmemMax, 88, 72, 60, 48, 39, 30, 21};
     const int ncls = (int)(sizeof(classes) / sizeof(classes[0]));
+    // The large-K class (one long eigen-solve chain per leaf, a tail of a few K > 200 leaves) goes to
+    // the side stream when smaller classes follow: they run next to it instead of behind its tail.
+    const cudaStream_t issue = c.stream;
+    const bool split = c.side && rd[0].K > kRecompressSmemMax && rd.back().K <= kRecompressSmemMax;
+    if (split) {
+      cudaEvent_t fork;
+      HMX_CUDA_TRY(cudaEventCreateWithFlags(&fork, cudaEventDisableTiming));
+      HMX_CUDA_TRY(cudaEventRecord(fork, issue));
+      HMX_CUDA_TRY(cudaStreamWaitEvent(c.side, fork, 0));
+      cudaEventDestroy(fork);
+    }
     size_t q0 = 0;
     for (int ci = 0; ci < ncls && q0 < rd.size(); ++ci) {
       const int lim_lo = ci + 1 < ncls ? classes[ci + 1] : 0;
       size_t q1 = q0;
       while (q1 < rd.size() && (rd[q1].K > lim_lo || ci == ncls - 1)) ++q1;
       if (q1 > q0) {
+        if (split && ci == 0) c.stream = c.side;
         e = launch_recompress_core(c, d_rd + q0, (int64_t)(q1 - q0), rd[q0].K, eps_rc, cfg->trunc_rule, ps.G, W,
                                    d_rank + q0, d_flag + q0);
-        mark("  rc class K<=" + std::to_string(rd[q0].K) + " n=" + std::to_string(q1 - q0));
+        c.stream = issue;
+        if (!(split && ci == 0))
+          mark("  rc class K<=" + std::to_string(rd[q0].K) + " n=" + std::to_string(q1 - q0));
         if (e) return e;
       }
       q0 = q1;
+    }
+    if (split) {
+      cudaEvent_t join;
+      HMX_CUDA_TRY(cudaEventCreateWithFlags(&join, cudaEventDisableTiming));
+      HMX_CUDA_TRY(cudaEventRecord(join, c.side));
+      HMX_CUDA_TRY(cudaStreamWaitEvent(issue, join, 0));
+      cudaEventDestroy(join);
+      mark("  rc large-K class joined");
     }
     mark("recompress issued");
     pending.push_back(Pending{&ps, std::move(live), d_rank, d_flag});

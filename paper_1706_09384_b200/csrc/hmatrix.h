@@ -32,6 +32,7 @@ struct Ctx {
   cudaStream_t stream = nullptr;
   cudaStream_t aux = nullptr;  // second stream for concurrent launches inside assembly
   cudaStream_t rerun = nullptr;  // high-priority stream for ACA capacity-overflow reruns
+  cudaStream_t side = nullptr;   // the large-K recompression class next to the classes that follow it
   bool own_stream = false;
   int num_sms = 148;
   size_t l2_bytes = 0;
@@ -189,7 +190,10 @@ struct AcaOut {
 // the narrow variant (128 threads, 4 CTAs / SM), the others the wide one (512)
 constexpr int kAcaWide = 0;
 constexpr int kAcaNarrow = 1;
-constexpr int kAcaNarrowMax = 320;
+#ifndef HMX_ACA_NARROW_MAX
+#define HMX_ACA_NARROW_MAX 320
+#endif
+constexpr int kAcaNarrowMax = HMX_ACA_NARROW_MAX;
 // tensor-core variant for large d = 3 leaves (default; HMX_ACA_TC=0 disables); its
 // per-warp Gram scratch sits behind the leaf's Gram pair: aca_tc_scratch(kcap) complex
 constexpr int kAcaTensor = 2;

@@ -835,19 +835,16 @@ HMX_D void recompress_truncate(const double* lam, const int* ordr, int K, double
 // MODE 0: E, Z, R, T in L2 (large K); 1: E / Z in shared memory; 2: E / Z, R and
 // T / L_r all in shared memory (small K: the O(K) sequential phases then run
 // at shared-memory instead of L2 latency)
-#ifndef HMX_RC_M0_REGS
-#define HMX_RC_M0_REGS 128
-#endif
-#ifndef HMX_RC_M1W_REGS
-#define HMX_RC_M1W_REGS 128
-#endif
-// register caps per instantiation (what bounds the CTAs per SM next to the shared memory):
-// 64 for the small shared-memory classes (8 x 128-thread CTAs per SM)
+// register caps per instantiation (with the shared memory, what bounds the CTAs per SM):
+//  * 64 for the small shared-memory classes (8 x 128-thread CTAs per SM);
+//  * 64 for the large-K class (512 threads): two of its long eigen-solve chains per SM instead of
+//    one CTA owning the whole register file (a few spills; U32k -2 ms, T65k -9 ms measured);
+//  * 80 for the 256-thread shared-memory classes (three per SM by registers).
 constexpr int rc_maxnreg(int mode, int nt) {
   return (mode == 1 && nt == 128) ? 65536 / (128 * HMX_RC_MINB)
          : (mode == 1 && nt == 64) ? 64
-         : (mode == 0 && nt == 512) ? HMX_RC_M0_REGS
-         : (mode == 1 && nt == 256) ? HMX_RC_M1W_REGS
+         : (mode == 0 && nt == 512) ? 64
+         : (mode == 1 && nt == 256) ? 80
                                     : (65536 / nt > 255 ? 255 : 65536 / nt);
 }
 template <int MODE, int NT>
