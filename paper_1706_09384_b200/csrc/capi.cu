@@ -838,8 +838,11 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     }
     tick("aca: descriptors");
     if ((rc = ps.mem.alloc(&ps.U, uo))) return fail(rc);
+    tick("aca: alloc U");
     if ((rc = ps.mem.alloc(&ps.V, vo))) return fail(rc);
+    tick("aca: alloc V");
     if ((rc = ps.gmem.alloc(&ps.G, go))) return fail(rc);
+    tick("aca: alloc G");
     AcaDesc* d_desc;
     AcaOut* d_out;
     int32_t* d_order;

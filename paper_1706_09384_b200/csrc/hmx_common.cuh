@@ -103,3 +103,41 @@ void hmx_set_error(const char* fmt, ...);
   } while (0)
 
 static inline int64_t hmx_cdiv(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+// ---- Blackwell bulk-copy plumbing (TMA engine, async proxy) ------------------------
+// cp.async.bulk moves one contiguous run global -> shared and signals completion as
+// transaction bytes on an mbarrier (SASS UBLKCP / SYNCS); the issuing lane needs no
+// registers for the data and no per-element address arithmetic.
+HMX_D void mbar_init(unsigned a, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(a), "r"(count) : "memory");
+}
+HMX_D void mbar_expect_tx(unsigned a, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(a), "r"(bytes) : "memory");
+}
+HMX_D void mbar_wait(unsigned a, unsigned parity) {
+  unsigned done = 0;
+  do {
+    asm volatile(
+        "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n selp.u32 %0, 1, 0, p;\n}\n"
+        : "=r"(done)
+        : "r"(a), "r"(parity)
+        : "memory");
+  } while (!done);
+}
+HMX_D void bulk_g2s(unsigned dst, const void* src, unsigned bytes, unsigned mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
+// generic-proxy accesses of this thread before -> async-proxy accesses after
+HMX_D void fence_async_global() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+HMX_D void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+
+// one lane of the (converged) warp, chosen by the hardware: the compiler issues what follows on
+// the uniform datapath when its operands are warp-uniform
+HMX_D bool elect_one() {
+  unsigned pred;
+  asm volatile("{\n .reg .pred p;\n elect.sync _|p, 0xffffffff;\n selp.u32 %0, 1, 0, p;\n}\n" : "=r"(pred));
+  return pred != 0;
+}
+

@@ -835,7 +835,8 @@ HMX_D void recompress_truncate(const double* lam, const int* ordr, int K, double
 // MODE 0: E, Z, R, T in L2 (large K); 1: E / Z in shared memory; 2: E / Z, R and
 // T / L_r all in shared memory (small K: the O(K) sequential phases then run
 // at shared-memory instead of L2 latency)
-// register caps per instantiation (with the shared memory, what bounds the CTAs per SM):
+// register caps per instantiation (with the shared memory, what bounds the CTAs per SM; nvcc takes
+// either __launch_bounds__ or __maxnreg__ on a kernel, so the cap alone is given):
 //  * 64 for the small shared-memory classes (8 x 128-thread CTAs per SM);
 //  * 64 for the large-K class (512 threads): two of its long eigen-solve chains per SM instead of
 //    one CTA owning the whole register file (a few spills; U32k -2 ms, T65k -9 ms measured);
@@ -848,7 +849,7 @@ constexpr int rc_maxnreg(int mode, int nt) {
                                     : (65536 / nt > 255 ? 255 : 65536 / nt);
 }
 template <int MODE, int NT>
-__global__ void __launch_bounds__(NT) __maxnreg__(rc_maxnreg(MODE, NT)) recompress_core(const RecDesc* __restrict__ desc, double eps, int rule,
+__global__ void __maxnreg__(rc_maxnreg(MODE, NT)) recompress_core(const RecDesc* __restrict__ desc, double eps, int rule,
                                                             const double2* __restrict__ G, double2* __restrict__ W,
                                                             int32_t* __restrict__ rank_out,
                                                             int32_t* __restrict__ flags_out) {
@@ -1131,31 +1132,35 @@ __global__ void __launch_bounds__(NT) __maxnreg__(rc_maxnreg(MODE, NT)) recompre
 // block: B = [W_re | W_im] (4 complex columns as 8 real ones), C1 = A_re B,
 // C2 = A_im B -> C_re = C1[:, :4] - C2[:, 4:], C_im = C1[:, 4:] + C2[:, :4].
 // CTA tile 64 rows x 32 complex columns, 8 warps of 32 rows x 8 columns, k
-// chunks of 16 staged in shared memory.  Fragment layout (checked by
+// chunks of 16 staged in shared memory (2-stage ring).  Fragment layout (checked by
 // tools/micro/dmma_layout.cu): A[r][k] at lane 4 r + k, B[k][n] at lane
 // 4 n + k, C[r][2 t + i] at lane 4 r + t.
-constexpr int TM = 64, TN = 32, TK = 16, kFormThreads = 256, kFormStages = 3;
+// 2 stages (54 KB) and 80 registers: three CTAs per SM (3 stages / uncapped 97 registers: two)
+constexpr int TM = 64, TN = 32, TK = 16, kFormThreads = 256, kFormStages = 2;
 HMX_D void dmma_8x8x4(double& c0, double& c1, double a, double b) {
   asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
                : "+d"(c0), "+d"(c1)
                : "d"(a), "d"(b));
 }
-// 16-byte asynchronous global -> shared copy, zero-filled when !valid
-HMX_D void cp_async16(void* smem, const void* gmem, bool valid) {
-  const unsigned sa = (unsigned)__cvta_generic_to_shared(smem);
-  const int n = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(valid ? gmem : smem), "r"(n));
+// Tiles move by the bulk-copy engine (cp.async.bulk, SASS UBLKCP): per k chunk one elected lane of
+// warp 0 issues, from warp-uniform operands, 16 column runs of A (64 rows = 1 KB each) and 32 column
+// runs of W (16 k = 256 B each) onto the stage's mbarrier (transaction bytes); every thread waits on
+// the barrier, and the CTA barrier of the next iteration frees the stage for its refill.  Only the
+// valid part of a tile is copied: rows / columns past the item's edge hold stale finite or
+// arbitrary data that only reaches discarded outputs (each output row / column depends on its own A
+// row / W column alone); the k tail of the last chunk is zeroed in both tiles.
+constexpr int TKP = TK + 4;  // W tile column stride (16-byte units): B fragment reads conflict-free
+constexpr size_t kFormSmem = sizeof(double2) * kFormStages * (TK * (TM + 2) + TN * TKP);
+HMX_D int64_t bcast64(int64_t v) {
+  const int lo = __shfl_sync(0xffffffffu, (int)(v & 0xffffffff), 0), hi = __shfl_sync(0xffffffffu, (int)(v >> 32), 0);
+  return ((int64_t)hi << 32) | (uint32_t)lo;
 }
-HMX_D void cp_async_commit() { asm volatile("cp.async.commit_group;"); }
-template <int N>
-HMX_D void cp_async_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N));
-}
-__global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __restrict__ desc,
+__global__ void __maxnreg__(80) form_gemm(const FormDesc* __restrict__ desc,
                                                           const int64_t* __restrict__ tile_start, int64_t nitems) {
   extern __shared__ double2 fsm[];
+  __shared__ __align__(8) unsigned long long full_bar[kFormStages];
   double2(*As)[TK][TM + 2] = reinterpret_cast<double2(*)[TK][TM + 2]>(fsm);
-  double2(*Ws)[TK][TN + 2] = reinterpret_cast<double2(*)[TK][TN + 2]>(fsm + kFormStages * TK * (TM + 2));
+  double2(*Ws)[TN][TKP] = reinterpret_cast<double2(*)[TN][TKP]>(fsm + kFormStages * TK * (TM + 2));
   // locate item by binary search over tile_start
   const int64_t tile = blockIdx.x;
   int64_t lo = 0, hi = nitems - 1;
@@ -1168,8 +1173,6 @@ __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __rest
   const int64_t local = tile - tile_start[lo];
   const int ntm = (ds.rows + TM - 1) / TM;
   const int tm = (int)(local % ntm), tn = (int)(local / ntm);
-  const double2* A = ds.A;
-  const double2* W = ds.W;
   double2* C = ds.C;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int wm = warp & 1, wn = warp >> 1;  // warp tile: rows wm*32 + [0,32), cols wn*8 + [0,8)
@@ -1180,19 +1183,44 @@ __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __rest
   // the item (small r, short last row tile: the MMAs on the padding are skipped)
   const int no = min(4, max(0, (ds.rows - (row0 + wm * 32) + 7) / 8));
   const bool colv = col0 + wn * 8 < ds.r;
+  const unsigned bar_sa = (unsigned)__cvta_generic_to_shared(&full_bar[0]);
+  if (tid == 0) {
+    for (int st = 0; st < kFormStages; ++st) mbar_init(bar_sa + 8u * st, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  // CTA-uniform copy operands, made warp-uniform for the compiler (uniform registers)
+  const int rv = min(TM, ds.rows - row0), cv = min(TN, ds.r - col0);
+  const int u_rv = __shfl_sync(0xffffffffu, rv, 0), u_cv = __shfl_sync(0xffffffffu, cv, 0);
+  const int u_K = __shfl_sync(0xffffffffu, ds.K, 0), u_lda = __shfl_sync(0xffffffffu, ds.lda, 0);
+  const double2* u_A = reinterpret_cast<const double2*>(bcast64(reinterpret_cast<int64_t>(ds.A + row0)));
+  const double2* u_W = reinterpret_cast<const double2*>(bcast64(reinterpret_cast<int64_t>(ds.W + (int64_t)col0 * ds.K)));
+  const unsigned as_sa = (unsigned)__cvta_generic_to_shared(&As[0][0][0]);
+  const unsigned ws_sa = (unsigned)__cvta_generic_to_shared(&Ws[0][0][0]);
   auto stage = [&](int kc, int buf) {
     const int k0 = kc * TK;
-    for (int t = tid; t < TK * TM; t += kFormThreads) {
-      const int rr = t % TM, kk = t / TM;
-      const int gr = row0 + rr, gk = k0 + kk;
-      const bool v = gr < ds.rows && gk < ds.K;
-      cp_async16(&As[buf][kk][rr], A + (v ? gr + (int64_t)gk * ds.lda : 0), v);
+    const int kv = min(TK, u_K - k0);
+    if (warp == 0 && elect_one()) {
+      const unsigned mb = bar_sa + 8u * (unsigned)buf;
+      mbar_expect_tx(mb, (unsigned)(kv * (u_rv + u_cv)) * (unsigned)sizeof(double2));
+      const double2* src = u_A + (int64_t)k0 * u_lda;
+      unsigned dst = as_sa + (unsigned)buf * (unsigned)(TK * (TM + 2) * sizeof(double2));
+      for (int kk = 0; kk < kv; ++kk) {
+        bulk_g2s(dst, src, (unsigned)u_rv * (unsigned)sizeof(double2), mb);
+        src += u_lda;
+        dst += (unsigned)((TM + 2) * sizeof(double2));
+      }
+      src = u_W + k0;
+      dst = ws_sa + (unsigned)buf * (unsigned)(TN * TKP * sizeof(double2));
+      for (int cc = 0; cc < u_cv; ++cc) {
+        bulk_g2s(dst, src, (unsigned)kv * (unsigned)sizeof(double2), mb);
+        src += u_K;
+        dst += (unsigned)(TKP * sizeof(double2));
+      }
     }
-    for (int t = tid; t < TK * TN; t += kFormThreads) {
-      const int kk = t % TK, cc = t / TK;
-      const int gk = k0 + kk, gc = col0 + cc;
-      const bool v = gk < ds.K && gc < ds.r;
-      cp_async16(&Ws[buf][kk][cc], W + (v ? gk + (int64_t)gc * ds.K : 0), v);
+    if (kv < TK) {  // k tail of the last chunk: zeros in both tiles (bytes the copies do not write)
+      for (int t = tid; t < (TK - kv) * TM; t += kFormThreads) As[buf][kv + t / TM][t % TM] = cmk(0.0, 0.0);
+      for (int t = tid; t < (TK - kv) * TN; t += kFormThreads) Ws[buf][t / (TK - kv)][kv + t % (TK - kv)] = cmk(0.0, 0.0);
     }
   };
   // complex product with three real products (Gauss): T1 = A_re W_re, T2 = A_im W_im,
@@ -1202,20 +1230,17 @@ __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __rest
 #pragma unroll
   for (int o = 0; o < 4; ++o) t1[o][0] = t1[o][1] = t2[o][0] = t2[o][1] = t3[o][0] = t3[o][1] = 0.0;
 #pragma unroll
-  for (int sidx = 0; sidx < kFormStages - 1; ++sidx) {
+  for (int sidx = 0; sidx < kFormStages - 1; ++sidx)
     if (sidx < nk) stage(sidx, sidx);
-    cp_async_commit();
-  }
   for (int kc = 0; kc < nk; ++kc) {
-    cp_async_wait<kFormStages - 2>();
-    __syncthreads();  // chunk kc landed; every warp is done with chunk kc - 1
-    if (kc + kFormStages - 1 < nk) stage(kc + kFormStages - 1, (kc + kFormStages - 1) % kFormStages);
-    cp_async_commit();
     const int buf = kc % kFormStages;
+    mbar_wait(bar_sa + 8u * (unsigned)buf, (unsigned)(kc / kFormStages) & 1u);
+    __syncthreads();  // every warp is done with chunk kc - 1 (its stage is refilled next) and sees the zeroed tails
+    if (kc + kFormStages - 1 < nk) stage(kc + kFormStages - 1, (kc + kFormStages - 1) % kFormStages);
 #pragma unroll
     for (int ks = 0; ks < TK; ks += 4) {
       // B[k][n] at lane 4 n + k: column wn * 8 + fr of W, row ks + fk
-      const double2 w = Ws[buf][ks + fk][wn * 8 + fr];
+      const double2 w = Ws[buf][wn * 8 + fr][ks + fk];
       const double br = w.x, bi = w.y, bs = w.x + w.y;
 #pragma unroll
       for (int o = 0; o < 4; ++o)
@@ -1227,7 +1252,6 @@ __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __rest
         }
     }
   }
-  cp_async_wait<0>();
   const int t = lane & 3;
 #pragma unroll
   for (int o = 0; o < 4; ++o)
@@ -1238,7 +1262,6 @@ __global__ void __launch_bounds__(kFormThreads) form_gemm(const FormDesc* __rest
         C[gr + (int64_t)gc * ds.ldc] = cmk(t1[o][i] - t2[o][i], t3[o][i] - t1[o][i] - t2[o][i]);
     }
 }
-constexpr size_t kFormSmem = sizeof(double2) * kFormStages * TK * ((TM + 2) + (TN + 2));
 
 }  // namespace
 
