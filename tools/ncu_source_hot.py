@@ -7,7 +7,13 @@ import sys
 
 rows = list(csv.reader(open(sys.argv[1])))
 ntop = int(sys.argv[2]) if len(sys.argv) > 2 else 45
-hdr, data = rows[1], rows[2:]
+hdr = rows[1]
+data = []
+for r in rows[2:]:  # the first kernel of the export only
+    if r and r[0] == "Kernel Name":
+        break
+    if len(r) == len(hdr):
+        data.append(r)
 ix = {h: i for i, h in enumerate(hdr)}
 stalls = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
 samp = [int(r[ix["# Samples"]]) for r in data]
