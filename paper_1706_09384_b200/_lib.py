@@ -59,6 +59,7 @@ SIGNATURES = {
     "hmx_ctx_set_stream": (C.c_int, [P, u64]),
     "hmx_ctx_sync": (C.c_int, [P]),
     "hmx_ctx_release_cache": (C.c_int, [P]),
+    "hmx_ctx_reserve": (C.c_int, [P, C.c_double, C.POINTER(C.c_double)]),
     "hmx_ctx_destroy": (C.c_int, [P]),
     "hmx_tree_build": (C.c_int, [P, i64, i64, C.POINTER(P)]),
     "hmx_tree_num_nodes": (i64, [P]),
@@ -181,6 +182,15 @@ def release_cached(device=0):
     library such as cuSOLVER has to allocate on the same device)."""
     if device in _ctx:
         check(lib().hmx_ctx_release_cache(_ctx[device]), "hmx_ctx_release_cache")
+
+
+def reserve(device=0, gigabytes=0.0):
+    """Opt-in arena (``hmx_ctx_reserve``): one reserved device region (``gigabytes``; 0 = 88% of the
+    free memory) serves the context's large requests from then on, so assemblies make no
+    cudaMalloc / cudaFree call; ``release_cached`` returns it.  Returns the seconds it took."""
+    t = C.c_double(0.0)
+    check(lib().hmx_ctx_reserve(context(device), float(gigabytes), C.byref(t)), "hmx_ctx_reserve")
+    return t.value
 
 
 def context(device=0):

@@ -44,9 +44,60 @@ void release_cache(Ctx& c) {
   for (auto& kv : c.cache) cudaFree(kv.second);
   c.cache.clear();
   c.cached_bytes = 0;
+  if (c.arena && c.arena_live.empty()) {  // the reserved region too, once nothing lives in it
+    cudaFree(c.arena);
+    c.arena = nullptr;
+    c.arena_size = c.arena_free = 0;
+    c.arena_holes.clear();
+  }
+}
+constexpr size_t kArenaGran = size_t(2) << 20;  // 2 MiB blocks
+constexpr size_t kArenaMin = size_t(1) << 20;   // smaller requests take the ordinary path
+static void* arena_alloc(Ctx& c, size_t bytes) {
+  bytes = (bytes + kArenaGran - 1) / kArenaGran * kArenaGran;
+  for (auto it = c.arena_holes.begin(); it != c.arena_holes.end(); ++it) {  // first fit by offset
+    if (it->second < bytes) continue;
+    const size_t off = it->first, len = it->second;
+    c.arena_holes.erase(it);
+    if (len > bytes) c.arena_holes.emplace(off + bytes, len - bytes);
+    c.arena_free -= bytes;
+    void* p = c.arena + off;
+    c.arena_live[p] = bytes;
+    return p;
+  }
+  return nullptr;
+}
+static bool arena_release(Ctx& c, void* p) {
+  auto it = c.arena_live.find(p);
+  if (it == c.arena_live.end()) return false;
+  size_t off = (size_t)(static_cast<char*>(p) - c.arena), len = it->second;
+  c.arena_live.erase(it);
+  c.arena_free += len;
+  auto nx = c.arena_holes.lower_bound(off);
+  if (nx != c.arena_holes.end() && off + len == nx->first) {  // merge with the hole behind
+    len += nx->second;
+    nx = c.arena_holes.erase(nx);
+  }
+  if (nx != c.arena_holes.begin()) {  // ... and with the one in front
+    auto pv = std::prev(nx);
+    if (pv->first + pv->second == off) {
+      off = pv->first;
+      len += pv->second;
+      c.arena_holes.erase(pv);
+    }
+  }
+  c.arena_holes.emplace(off, len);
+  return true;
 }
 cudaError_t dev_alloc(Ctx& c, void** p, size_t bytes) {
   if (c.pool) return cudaMallocFromPoolAsync(p, bytes, c.pool, c.stream);
+  if (c.arena && bytes >= kArenaMin) {
+    std::lock_guard<std::mutex> lk(c.mem_mu);
+    if (void* q = arena_alloc(c, bytes)) {
+      *p = q;
+      return cudaSuccess;
+    }
+  }
   // 2 MiB granularity so that repeated assemblies hit the cache
   const size_t gran = bytes >= (1u << 20) ? (size_t(2) << 20) : 256;
   bytes = (bytes + gran - 1) / gran * gran;
@@ -83,6 +134,7 @@ void dev_free(Ctx& c, void* p) {
   // context stream after the work that used it (assembly joins its auxiliary
   // stream before freeing), so no device synchronisation is needed here
   std::lock_guard<std::mutex> lk(c.mem_mu);
+  if (c.arena && arena_release(c, p)) return;
   auto it = c.live.find(p);
   if (it == c.live.end()) {
     cudaFree(p);
@@ -327,6 +379,47 @@ int hmx_ctx_release_cache(hmx_ctx* ctx) {
   return HMX_OK;
 }
 
+int hmx_ctx_reserve(hmx_ctx* ctx, double gigabytes, double* seconds) {
+  if (!ctx || gigabytes < 0.0) return HMX_EINVAL;
+  Ctx& c = ctx->c;
+  HMX_CUDA_TRY(cudaSetDevice(c.device));
+  const auto t0 = std::chrono::steady_clock::now();
+  {
+    std::lock_guard<std::mutex> lk(c.mem_mu);
+    if (c.arena) {
+      hmx_set_error("hmx_ctx_reserve: the context already holds a reserved region of %.2f GB", c.arena_size / 1e9);
+      return HMX_EINVAL;
+    }
+  }
+  release_cache(c);
+  size_t free_b = 0, total_b = 0;
+  HMX_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
+  // default: what the assembly's capacity model may use plus the final streams, leaving the rest
+  // of the device to the libraries next to it (cuBLAS / cuSOLVER workspaces, the H-LU pool)
+  size_t want = gigabytes > 0.0 ? (size_t)(gigabytes * 1e9) : (size_t)(0.88 * (double)free_b);
+  want = want / hmx::kArenaGran * hmx::kArenaGran;
+  if (want == 0 || want > free_b) {
+    hmx_set_error("hmx_ctx_reserve: %.2f GB requested, %.2f GB free", want / 1e9, free_b / 1e9);
+    return HMX_ENOMEM;
+  }
+  void* p = nullptr;
+  const cudaError_t e = cudaMalloc(&p, want);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    hmx_set_error("hmx_ctx_reserve: cudaMalloc(%.2f GB): %s", want / 1e9, cudaGetErrorString(e));
+    return e == cudaErrorMemoryAllocation ? HMX_ENOMEM : HMX_ECUDA;
+  }
+  {
+    std::lock_guard<std::mutex> lk(c.mem_mu);
+    c.arena = static_cast<char*>(p);
+    c.arena_size = c.arena_free = want;
+    c.arena_holes.clear();
+    c.arena_holes.emplace(0, want);
+  }
+  if (seconds) *seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+  return HMX_OK;
+}
+
 int hmx_ctx_sync(hmx_ctx* ctx) {
   if (!ctx) return HMX_EINVAL;
   HMX_CUDA_TRY(cudaStreamSynchronize(ctx->c.stream));
@@ -546,7 +639,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   tick("aca: meminfo");
   // memory cached by this context counts as free; U, V and the Gram matrices get
   // kAcaBudgetFrac of it (the Grams are released before the final streams are allocated)
-  double avail = (double)free_b + (double)c.cached_bytes;
+  double avail = (double)free_b + (double)c.cached_bytes + (double)c.arena_free;
   double budget = cfg->mem_budget_gb > 0 ? cfg->mem_budget_gb * 1e9 : kAcaBudgetFrac * avail;
   auto round_d = [&](int64_t v) { return std::max<int64_t>(d, (v / d) * d); };
   // one routing decision feeds both the workspace plan (tensor-core Gram scratch) and the
@@ -634,7 +727,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       // turns into expensive overflow reruns)
       release_cache(c);
       HMX_CUDA_TRY(cudaMemGetInfo(&free_b, &total_b));
-      avail = (double)free_b;
+      avail = (double)free_b + (double)c.arena_free;
       budget = kAcaBudgetFrac * avail;
     }
     if (verbose)

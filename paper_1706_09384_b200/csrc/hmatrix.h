@@ -42,6 +42,13 @@ struct Ctx {
   std::multimap<size_t, void*> cache;  // size -> free block
   std::unordered_map<void*, size_t> live;  // block -> size
   size_t cached_bytes = 0;
+  // opt-in arena (hmx_ctx_reserve): one reserved device region serving the large requests of every
+  // assembly by first fit (free list by offset, coalescing), so steady-state and first assemblies
+  // of a new problem size make no cudaMalloc / cudaFree call at all
+  char* arena = nullptr;
+  size_t arena_size = 0, arena_free = 0;
+  std::map<size_t, size_t> arena_holes;             // offset -> length
+  std::unordered_map<void*, size_t> arena_live;     // block -> length
   void* blas = nullptr;    // cublasHandle_t of the randomized-SVD fallback (rsvd.cu), lazy
   void* solver = nullptr;  // cusolverDnHandle_t, lazy
   cudaMemPool_t lu_pool = nullptr;  // stream-ordered pool of the H-LU engine (hlu.cu), lazy
