@@ -414,9 +414,16 @@ def config_summary(tag, device, dfma_tflops, steps=20):
     ct = hmx.build_cluster_tree(cloud, w.n_leaf)
     bt = hmx.build_block_tree(ct, ct, w.eta)
     H, rep = hmx.assemble(w.spec(), cloud, ct, bt, hmx.ACAConfig(eps_aca=w.eps), device=device)
-    del H  # the second assembly is the steady-state one
-    H, rep = hmx.assemble(w.spec(), cloud, ct, bt, hmx.ACAConfig(eps_aca=w.eps), device=device)
-    st = H.stats()
+    # steady state: the fastest of three repeated assemblies (a single sample of a 3-35 ms job is at the
+    # mercy of one host hiccup between its launches)
+    st, asm_ms = None, []
+    for _ in range(3):
+        del H
+        H, rep = hmx.assemble(w.spec(), cloud, ct, bt, hmx.ACAConfig(eps_aca=w.eps), device=device)
+        s_i = H.stats()
+        asm_ms.append(s_i["t_total_ms"])
+        if st is None or s_i["t_total_ms"] < st["t_total_ms"]:
+            st = s_i
     n = w.d * w.n_points
     x = torch.randn(n, dtype=torch.complex128, device=f"cuda:{device}")
     y = torch.empty_like(x)
@@ -436,6 +443,7 @@ def config_summary(tag, device, dfma_tflops, steps=20):
                          st["pairs_evaluated"])
     ex = st["flops_assembly"] + PAIR_FLOPS[w.kind] * st["pairs_evaluated"]
     out = {"n_points": w.n_points, "kind": w.kind, "n_leaf": w.n_leaf, "assembly_ms": st["t_total_ms"],
+           "assembly_ms_samples": asm_ms,
            "green_entries_per_s": w.d * w.d * st["pairs_evaluated"] / t,
            "fp64_frac_survey_model": sv / t / 1e12 / dfma_tflops, "fp64_frac_executed": ex / t / 1e12 / dfma_tflops,
            "matvec_ms": mv_ms, "matvec_GBps": st["matvec_bytes"] / (mv_ms * 1e-3) / 1e9,
