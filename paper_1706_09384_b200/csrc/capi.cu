@@ -612,6 +612,12 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
                  fr / 1e9, c.cached_bytes / 1e9);
   };
   tick("upload");
+  // host-only time stamps (no synchronisation), printed with the GPU timeline
+  std::vector<std::pair<std::string, double>> hl;
+  auto htick = [&](const char* what) {
+    if (verbose)
+      hl.emplace_back(what, std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count());
+  };
   // HMX_VERBOSE: GPU timeline of the launches (events on the issuing stream)
   std::vector<std::pair<std::string, cudaEvent_t>> tl;
   auto mark = [&](const std::string& what) {
@@ -756,6 +762,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   // Recompression of the live leaves [q0, q1) of a pass, on the current c.stream.
   auto recompress_subset = [&](AcaPass& ps, std::vector<int64_t> live) -> int {
     if (live.empty()) return HMX_OK;
+    htick("consume: live list built");
     // largest K first, launched in K classes so small leaves do not pay for big shared memory
     {
       // counting sort on the rank (descending), stable in position order: the
@@ -770,6 +777,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       for (int64_t x : live) sorted[(size_t)cnt[(size_t)(kmax - ps.out[x].rank)]++] = x;
       live.swap(sorted);
     }
+    htick("consume: class sort");
     std::vector<RecDesc> rd(live.size());
     int64_t wo = 0;
     for (size_t q = 0; q < live.size(); ++q) {
@@ -788,8 +796,10 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
     if ((e = rec_tmp.alloc(&d_rd, (int64_t)rd.size()))) return e;
     if ((e = rec_tmp.alloc(&d_rank, (int64_t)rd.size()))) return e;
     if ((e = rec_tmp.alloc(&d_flag, (int64_t)rd.size()))) return e;
+    htick("consume: descriptors + alloc");
     for (size_t q = 0; q < live.size(); ++q) ps.wptr[live[q]] = W + rd[q].woff;
     HMX_CUDA_TRY(cudaMemcpyAsync(d_rd, rd.data(), sizeof(RecDesc) * rd.size(), cudaMemcpyHostToDevice, c.stream));
+    htick("consume: upload");
     mark("recompress start");
     // shared-memory size classes (smem ~ 16 K^2 bytes): more CTAs per SM for small K
     const int classes[] = {kMaxAcaCols, kRecompressSmemMax, 88, 72, 60, 48, 39, 30, 21};
@@ -830,6 +840,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
       mark("  rc large-K class joined");
     }
     mark("recompress issued");
+    htick("consume: classes launched");
     pending.push_back(Pending{&ps, std::move(live), d_rank, d_flag});
     return HMX_OK;
   };
@@ -990,16 +1001,21 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
                            cfg->eps, s3f, ps.U, ps.V, ps.G, d_out, kAcaNarrow, 0)))
         return fail(rc);
       mark("aca narrow done");
+    }
+    // the rank-independent half of the matvec plan while the ACA runs: before the read-backs,
+    // which block the host until their kernel is done (device -> pageable host copies return only
+    // once complete)
+    if (pre.segs.empty()) build_plan_pre(H, pre);
+    htick("plan pre built");
+    if (todo.size() > nwide)
       HMX_CUDA_TRY(cudaMemcpyAsync(ps.out.data() + nwide, d_out + nwide, sizeof(AcaOut) * (todo.size() - nwide),
                                    cudaMemcpyDeviceToHost, c.stream));
-    }
-    // the rank-independent half of the matvec plan, while the ACA runs
-    if (pre.segs.empty()) build_plan_pre(H, pre);
     // narrow leaves (main stream) first, then the wide ones (aux stream): the wide leaves'
     // large-K recompression classes then queue on aux behind the wide ACA and overlap the
     // narrow leaves' recompression on the main stream
     if (todo.size() > nwide) {
       HMX_CUDA_TRY(cudaStreamSynchronize(c.stream));
+      htick("narrow ACA synced");
       if ((rc = consume(ps, nwide, todo.size()))) return fail(rc);
     }
     if (nwide) {
@@ -1075,6 +1091,7 @@ int hmx_assemble(hmx_ctx* ctx, const hmx_kernel* k, const double* pts_tree, cons
   tick("aca done");
   if (verbose) {
     cudaDeviceSynchronize();
+    for (auto& kv : hl) std::fprintf(stderr, "[hmx]   host %-35s %9.2f ms\n", kv.first.c_str(), kv.second);
     for (auto& kv : tl) {
       float ms = 0;
       cudaEventElapsedTime(&ms, ev[0], kv.second);
