@@ -487,7 +487,12 @@ def hmx_arm(args):
     # untimed set-up, like loading a model: one reserved device region serves every assembly's
     # workspaces and streams from here on (no cudaMalloc / cudaFree inside the timed regions, whose
     # cost varies 10x between the boxes of the pool)
-    reserve_s = None if args.no_reserve else _lib.reserve(local, 0.0)
+    reserve_s = None
+    if not args.no_reserve:
+        try:
+            reserve_s = _lib.reserve(local, 0.0)
+        except Exception as exc:  # e.g. a co-tenant holds the memory: per-assembly allocation instead
+            print(f"[bench] hmx_ctx_reserve failed ({exc!r}); continuing with per-assembly cudaMalloc", file=sys.stderr)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     H, rep = hmx.assemble(spec, cloud, ct, bt, hmx.ACAConfig(eps_aca=w.eps), device=local)
